@@ -1,0 +1,129 @@
+/*
+ * fpsa.h -- C ABI of the B200-native FPSAttention hot path (libfpsa.so).
+ *
+ * Drop-in boundary for the reference package fp8sta (arXiv 2506.04648,
+ * /root/reference/pkg/src/fp8sta).  The reference has no FFI: its boundary
+ * is the Python surface re-exported in fp8sta/__init__.py:10-48.  Each entry
+ * point below replaces one reference function (cited per function); the
+ * Python package paper_2506_04648_b200 binds them with ctypes and mirrors the
+ * reference names, argument meaning and exceptions on top.
+ *
+ * Conventions
+ *   - plain pointers and sizes, no torch types; every call returns an int
+ *     status (FPSA_OK == 0, see fpsa_status);
+ *   - device buffers are caller-owned; device calls are asynchronous on the
+ *     given cudaStream_t (passed as void*; NULL = legacy default stream) and
+ *     allocate nothing (workspaces are caller-provided);
+ *   - no global mutable state except a per-process table of driver entry
+ *     points, initialised once and thread-safe;
+ *   - token grids are (t, h, w) with w fastest (fp8sta/grid.py:1-8);
+ *   - "tile-major padded" code layout: for head h, tile u, local row r,
+ *     row index (h*M + u)*tile_pitch + r of a [rows][d] uint8 matrix, rows
+ *     r in [tile_volume, tile_pitch) zero.  tile_pitch == tile_volume gives
+ *     exactly the reference's tile-contiguous layout (fp8sta/grid.py:132-154).
+ */
+#ifndef FPSA_H_
+#define FPSA_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  FPSA_OK = 0,
+  FPSA_EINVAL = 1,        /* bad argument (reference: ValueError) */
+  FPSA_EINDIVISIBLE = 2,  /* tile does not divide grid (grid.py:95-99, ValueError) */
+  FPSA_ENONFINITE = 3,    /* non-finite input (quantize.py:105-106, attention.py:53-54) */
+  FPSA_ECUDA = 4,         /* CUDA runtime / driver error */
+  FPSA_EUNSUPPORTED = 5,  /* valid request this build does not implement (e.g. d not in {64,128}) */
+  FPSA_ERANGE = 6,        /* index out of range (reference: IndexError) */
+  FPSA_ECAPACITY = 7      /* caller buffer too small */
+} fpsa_status;
+
+typedef enum { FPSA_F32 = 0, FPSA_BF16 = 1, FPSA_F16 = 2 } fpsa_dtype;
+typedef enum { FPSA_E4M3 = 0, FPSA_E5M2 = 1 } fpsa_fmt;
+typedef enum { FPSA_ORDER_TILE = 0, FPSA_ORDER_NATURAL = 1 } fpsa_order;
+
+typedef struct {
+  int32_t t, h, w;
+} fpsa_dims3;
+
+/* Human-readable text of the last error on this thread ("" if none). */
+const char* fpsa_last_error(void);
+/* ABI version, major*10000 + minor*100 + patch. */
+int fpsa_version(void);
+
+/* ---------------------------------------------------------------- host layout */
+
+/* Tiles per axis of grid/tile; FPSA_EINDIVISIBLE with the reference message
+ * text in fpsa_last_error().  Replaces build_tile_map (fp8sta/grid.py:91-109). */
+int fpsa_tile_grid(fpsa_dims3 grid, fpsa_dims3 tile, fpsa_dims3* tile_dims);
+
+/* Gather permutation to tile-major order, perm[L].  Replaces
+ * tile_contiguous_order (fp8sta/grid.py:132-154). */
+int fpsa_tile_perm(fpsa_dims3 grid, fpsa_dims3 tile, int64_t* perm);
+
+/* Number of admissible (query tile, key tile) pairs of a window.  With
+ * fpsa_window_csr replaces build_block_mask / BlockMask.allowed /
+ * allowed_counts / density (fp8sta/sparsity.py:48-75, :112-144). */
+int fpsa_window_nnz(fpsa_dims3 tile_dims, fpsa_dims3 window, int64_t* nnz);
+
+/* CSR of ascending admissible key tiles per query tile:
+ * offs[M+1], ids[nnz] (capacity `cap`). */
+int fpsa_window_csr(fpsa_dims3 tile_dims, fpsa_dims3 window, int32_t* offs, int32_t* ids, int64_t cap,
+                    int64_t* nnz);
+
+/* Regime index (0 early, 1 mid, 2 late) of 1-based step t.  Replaces
+ * ScheduleConfig.regime_of / params_at (fp8sta/schedule.py:41-50, :71-73). */
+int fpsa_regime_of(int32_t t, int32_t total_steps, double alpha1, double alpha2, int32_t* regime);
+
+/* ---------------------------------------------------------------- device kernels */
+
+/* Per-3D-tile FP8 quantisation of q or k for `heads` heads in one pass:
+ * read x (dtype, element (token, head, c) at x + token*token_stride +
+ * head*head_stride + c, tokens in `in_order`), gather to tile-major order,
+ * per-tile amax, f64 scale = amax/max_value (1.0 for an all-zero tile), e4m3 /
+ * e5m2 codes bit-identical to the reference (round-to-nearest-even of the f64
+ * quotient).  codes: tile-major padded [heads*M*tile_pitch][d];
+ * scales: f64 [heads*M].  err_flag (device int32, may be NULL) gets bit 0 set
+ * on non-finite input.  Replaces quantize_qk_tilewise (fp8sta/quantize.py:111-124)
+ * together with tile_contiguous_order and fp8.encode (fp8.py:153-188). */
+int fpsa_quantize_qk(const void* x, int dtype, int64_t token_stride, int64_t head_stride, int32_t heads,
+                     fpsa_dims3 grid, fpsa_dims3 tile, int32_t d, int32_t tile_pitch, int in_order, int fmt,
+                     uint8_t* codes, double* scales, int32_t* err_flag, void* stream);
+
+/* Per-channel FP8 quantisation of v: column amax over all L tokens of each
+ * head, f64 scale per (head, channel), codes in the same tile-major padded
+ * layout as fpsa_quantize_qk.  workspace: device, >= heads*d*4 bytes.
+ * Replaces quantize_v_channelwise (fp8sta/quantize.py:127-134). */
+int fpsa_quantize_v(const void* x, int dtype, int64_t token_stride, int64_t head_stride, int32_t heads,
+                    fpsa_dims3 grid, fpsa_dims3 tile, int32_t d, int32_t tile_pitch, int in_order, int fmt,
+                    uint8_t* codes, double* scales, void* workspace, int32_t* err_flag, void* stream);
+
+/* Work list for fpsa_attn_fwd: one entry per (head, query tile, pair of
+ * 128-row query blocks), longest first.  Host-side; n_items returns the
+ * count, items (capacity `cap`, 3 int32 each: head, tile, first q-block). */
+int fpsa_attn_worklist(int32_t heads, fpsa_dims3 tile_dims, int32_t tile_volume, const int32_t* offs_host,
+                       int32_t* items, int64_t cap, int64_t* n_items);
+
+/* Sliding-tile sparse FP8 attention forward over quantised codes.
+ *   q/k/v codes: tile-major padded (fpsa_quantize_*), tile_pitch a multiple of 128
+ *   q/k scales: f64 [heads*M]; v scales f64 [heads*d]
+ *   offs/ids: device CSR from fpsa_window_csr; items/n_items: device work list
+ *   softmax_scale > 0 (the reference default is f32(1/sqrt(d)))
+ *   out: element (token, head, c) at out + token*out_token_stride +
+ *        head*out_head_stride + c, tokens in out_order, dtype out_dtype
+ *   tau_log2: lazy-rescale headroom of the one-pass softmax (0..8)
+ * Replaces fp8_sparse_forward / _engine (fp8sta/attention.py:91-149, :179-208). */
+int fpsa_attn_fwd(const uint8_t* q_codes, const uint8_t* k_codes, const uint8_t* v_codes, const double* q_scales,
+                  const double* k_scales, const double* v_scales, int32_t heads, fpsa_dims3 grid, fpsa_dims3 tile,
+                  int32_t d, int32_t tile_pitch, const int32_t* offs, const int32_t* ids, const int32_t* items,
+                  int32_t n_items, float softmax_scale, int fmt, float tau_log2, void* out, int out_dtype,
+                  int64_t out_token_stride, int64_t out_head_stride, int out_order, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FPSA_H_ */

@@ -1,0 +1,427 @@
+"""numpy restatement of the reference ``fp8sta`` hot path (test infrastructure).
+
+Written independently of the reference code: the FP8 encoder works on
+frexp/rint arithmetic instead of the reference's searchsorted boundary tables,
+the tile permutation is a reshape/transpose instead of index arithmetic, and
+the window lists are built per axis as integer intervals instead of an M x M
+boolean mask.  Semantics (rounding, saturation, signed zero, error types) are
+those of the cited reference lines and are pinned by the golden vectors in
+``tests/golden``.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+__all__ = [
+    "Fmt", "E4M3", "E5M2", "FORMATS",
+    "decode", "encode", "grid_round",
+    "block_scales", "quantize_qk_tilewise", "quantize_v_channelwise",
+    "tile_perm", "tile_grid_dims",
+    "axis_interval", "window_lists", "density_of", "flops_sparse_of",
+    "regime_of", "schedule_valid",
+    "fp8_sparse_forward", "sparse_forward_f32", "onepass_forward",
+    "cosine", "max_abs", "gen_inputs",
+]
+
+
+# --------------------------------------------------------------------------
+# FP8 formats -- fp8sta/fp8.py:28-61
+# --------------------------------------------------------------------------
+@dataclass(frozen=True)
+class Fmt:
+    name: str
+    ebits: int
+    mbits: int
+    bias: int
+    max_value: float
+    has_inf: bool
+
+    @property
+    def min_normal(self) -> float:
+        return 2.0 ** (1 - self.bias)
+
+    @property
+    def sub_step_exp(self) -> int:
+        # exponent of the subnormal spacing, fp8.py:79-80 (m * 2^(1-bias-mbits))
+        return 1 - self.bias - self.mbits
+
+    @property
+    def max_code(self) -> int:
+        # largest finite non-negative code: fp8.py:86-87
+        return 0x7E if not self.has_inf else 0x7B
+
+
+E4M3 = Fmt("e4m3", 4, 3, 7, 448.0, False)       # fp8.py:41-49
+E5M2 = Fmt("e5m2", 5, 2, 15, 57344.0, True)     # fp8.py:51-59
+FORMATS = {"e4m3": E4M3, "e5m2": E5M2}
+
+
+def _code_values(fmt: Fmt) -> np.ndarray:
+    """Value of each of the 256 codes (NaN where the pattern is NaN), fp8.py:73-84."""
+    codes = np.arange(256)
+    sign = np.where(codes & 0x80, -1.0, 1.0)
+    e = (codes >> fmt.mbits) & ((1 << fmt.ebits) - 1)
+    m = codes & ((1 << fmt.mbits) - 1)
+    mag = np.where(
+        e == 0,
+        np.ldexp(m.astype(np.float64), fmt.sub_step_exp),
+        np.ldexp((m + (1 << fmt.mbits)).astype(np.float64), e - fmt.bias - fmt.mbits),
+    )
+    top = (1 << fmt.ebits) - 1
+    if fmt.has_inf:
+        mag = np.where(e == top, np.where(m == 0, np.inf, np.nan), mag)
+    else:
+        mag = np.where((e == top) & (m == (1 << fmt.mbits) - 1), np.nan, mag)
+    return sign * mag
+
+
+_VALUES = {f.name: _code_values(f) for f in (E4M3, E5M2)}
+
+
+def decode(codes, fmt: Fmt = E4M3) -> np.ndarray:
+    """codes -> exact float32 values; NaN patterns raise (fp8.py:191-205)."""
+    c = np.asarray(codes, dtype=np.uint8)
+    out = _VALUES[fmt.name][c].astype(np.float32)
+    if np.isnan(out).any():
+        raise ValueError(f"NaN code pattern for {fmt.name}")
+    return out
+
+
+def encode(x, fmt: Fmt = E4M3) -> np.ndarray:
+    """Round to nearest, ties to even, saturating; sign kept on zero (fp8.py:153-188).
+
+    Restated with frexp arithmetic: the spacing of the grid around |x| is
+    2^max(e - mbits, 1 - bias - mbits); ``np.rint`` gives ties-to-even on the
+    multiple count, which coincides with ties to the even code.
+    """
+    a = np.asarray(x)
+    if a.dtype != np.float32:
+        a = a.astype(np.float64)
+    if np.isnan(a).any():
+        raise ValueError("cannot encode NaN")
+    mag = np.abs(a).astype(np.float64)
+    inf = np.isinf(mag)
+    if inf.any() and not fmt.has_inf:
+        raise ValueError(f"cannot encode infinity in {fmt.name}")
+    mag = np.where(inf, 0.0, mag)
+    _, ex = np.frexp(mag)
+    step_exp = np.maximum(ex - 1 - fmt.mbits, fmt.sub_step_exp)
+    k = np.rint(np.ldexp(mag, -step_exp))
+    val = np.minimum(np.ldexp(k, step_exp), fmt.max_value)
+    # value -> code
+    fr, ex2 = np.frexp(val)
+    normal = val >= fmt.min_normal
+    mant = np.where(normal, np.ldexp(fr, fmt.mbits + 1) - (1 << fmt.mbits), 0.0)
+    code_normal = ((ex2 - 1 + fmt.bias) << fmt.mbits) + mant.astype(np.int64)
+    code_sub = np.ldexp(val, -fmt.sub_step_exp).astype(np.int64)
+    code = np.where(normal, code_normal, code_sub).astype(np.uint8)
+    if fmt.has_inf:
+        code = np.where(inf, np.uint8(0x7C), code)
+    code = code | (np.signbit(a).astype(np.uint8) << 7)
+    return code.astype(np.uint8)
+
+
+def grid_round(v: np.ndarray, fmt: Fmt = E4M3) -> np.ndarray:
+    """RNE of non-negative float32 onto the fp8 grid, saturating (fp8.py:237-253)."""
+    if v.dtype != np.float32:
+        raise TypeError("grid_round expects float32")
+    return decode(encode(v, fmt), fmt)
+
+
+# --------------------------------------------------------------------------
+# quantisation policies -- fp8sta/quantize.py
+# --------------------------------------------------------------------------
+def block_scales(peaks: np.ndarray, fmt: Fmt = E4M3) -> np.ndarray:
+    """max(peak/max_value, f64 tiny); exactly 1.0 for an all-zero block (quantize.py:102-108)."""
+    peaks = np.asarray(peaks, dtype=np.float64)
+    if not np.isfinite(peaks).all():
+        raise ValueError("non-finite value in quantization input")
+    s = np.maximum(peaks / fmt.max_value, np.finfo(np.float64).tiny)
+    return np.where(peaks == 0.0, 1.0, s)
+
+
+def quantize_qk_tilewise(x: np.ndarray, tv: int, fmt: Fmt = E4M3):
+    """One f64 scale per tile of tv tile-contiguous rows (quantize.py:111-124)."""
+    m = np.asarray(x, dtype=np.float64)
+    L, d = m.shape
+    if L % tv:
+        raise ValueError(f"L={L} not a multiple of the tile volume {tv}")
+    tiles = m.reshape(L // tv, tv * d)
+    scales = block_scales(np.abs(tiles).max(axis=1), fmt)
+    codes = encode(tiles / scales[:, None], fmt).reshape(L, d)
+    return codes, scales
+
+
+def quantize_v_channelwise(x: np.ndarray, fmt: Fmt = E4M3):
+    """One f64 scale per column over all rows (quantize.py:127-134)."""
+    m = np.asarray(x, dtype=np.float64)
+    scales = block_scales(np.abs(m).max(axis=0), fmt)
+    return encode(m / scales[None, :], fmt), scales
+
+
+# --------------------------------------------------------------------------
+# layout -- fp8sta/grid.py
+# --------------------------------------------------------------------------
+def tile_grid_dims(grid: tuple[int, int, int], tile: tuple[int, int, int]) -> tuple[int, int, int]:
+    """Tiles per axis, rejecting indivisible axes with the reference message (grid.py:91-109)."""
+    out = []
+    for axis, g, s in zip("thw", grid, tile):
+        if g % s:
+            raise ValueError(f"indivisible grid: axis {axis} has {g} tokens, not divisible by tile extent {s}")
+        out.append(g // s)
+    return tuple(out)
+
+
+def tile_perm(grid: tuple[int, int, int], tile: tuple[int, int, int]) -> np.ndarray:
+    """Gather permutation to tile-major order (grid.py:132-154).
+
+    x[perm] lists tiles row-major over the tile grid, tokens row-major inside
+    a tile.  Restated as a 6-axis reshape/transpose of the token index grid.
+    """
+    gt, gh, gw = tile_grid_dims(grid, tile)
+    st, sh, sw = tile
+    idx = np.arange(grid[0] * grid[1] * grid[2], dtype=np.int64)
+    return idx.reshape(gt, st, gh, sh, gw, sw).transpose(0, 2, 4, 1, 3, 5).reshape(-1)
+
+
+# --------------------------------------------------------------------------
+# sliding-tile windows -- fp8sta/sparsity.py
+# --------------------------------------------------------------------------
+def axis_interval(x: int, dim: int, extent: int) -> tuple[int, int]:
+    """Admissible key coordinates [lo, hi] for query coordinate x (sparsity.py:43-45, :96-109)."""
+    back, fwd = (extent - 1) // 2, extent // 2
+    return max(0, x - back), min(dim - 1, x + fwd)
+
+
+def window_lists(dims: tuple[int, int, int], window: tuple[int, int, int]):
+    """CSR of ascending admissible key tiles per query tile (sparsity.py:63-75, :112-132)."""
+    dt, dh, dw = dims
+    if min(dims) < 1:
+        raise ValueError(f"tile grid dims must be >= 1, got {dims}")
+    offs = [0]
+    ids = []
+    for ut in range(dt):
+        t0, t1 = axis_interval(ut, dt, window[0])
+        for uh in range(dh):
+            h0, h1 = axis_interval(uh, dh, window[1])
+            for uw in range(dw):
+                w0, w1 = axis_interval(uw, dw, window[2])
+                for vt in range(t0, t1 + 1):
+                    for vh in range(h0, h1 + 1):
+                        base = (vt * dh + vh) * dw
+                        ids.extend(range(base + w0, base + w1 + 1))
+                offs.append(len(ids))
+    return np.asarray(offs, dtype=np.int32), np.asarray(ids, dtype=np.int32)
+
+
+def density_of(offs: np.ndarray) -> float:
+    """Admissible-pair fraction (sparsity.py:141-144)."""
+    m = len(offs) - 1
+    return int(offs[-1]) / (m * m)
+
+
+def flops_sparse_of(L: int, d: int, density: float) -> int:
+    """round(density * 4 L^2 d) (metrics.py:91-102)."""
+    if not 0.0 < density <= 1.0:
+        raise ValueError(f"density must be in (0, 1], got {density}")
+    return round(density * 4 * L * L * d)
+
+
+# --------------------------------------------------------------------------
+# schedule -- fp8sta/schedule.py
+# --------------------------------------------------------------------------
+def regime_of(t: int, total: int, alpha1: float, alpha2: float) -> str:
+    """Step -> regime with boundary steps in the earlier regime (schedule.py:41-50)."""
+    if not 1 <= t <= total:
+        raise ValueError(f"step {t} out of range [1, {total}]")
+    if t <= math.floor(alpha1 * total):
+        return "early"
+    if t <= math.floor(alpha2 * total):
+        return "mid"
+    return "late"
+
+
+def schedule_valid(alpha1, alpha2, total, tile_vols, win_vols) -> bool:
+    """Ordering rules of schedule.validate (schedule.py:76-104); vols = (early, mid, late)."""
+    ge, gm, gl = tile_vols
+    we, wm, wl = win_vols
+    return (0 < alpha1 < alpha2 < 1) and total >= 1 and ge > gl > gm and wm > wl > we
+
+
+# --------------------------------------------------------------------------
+# attention -- fp8sta/attention.py
+# --------------------------------------------------------------------------
+def _softmax_scale(d: int, scale) -> np.float32:
+    """f32(1/sqrt(d)) unless given; must be > 0 (attention.py:83-88)."""
+    if scale is None:
+        return np.float32(1.0 / math.sqrt(d))
+    if not scale > 0:
+        raise ValueError("softmax_scale must be > 0")
+    return np.float32(scale)
+
+
+def _tile_attention(qv, kv, vv, tv, offs, ids, q_fac, k_fac, v_fac, scale, quant_p: bool):
+    """Per-query-tile masked attention with a two-pass softmax (attention.py:91-149).
+
+    f32 logits from the decoded values, per-(tile,tile) factor applied after
+    the GEMM, f64 denominator, normalised weights rounded to E4M3 at 448 when
+    ``quant_p``, f32 output GEMM scaled by per-channel factors.
+    """
+    L, d = qv.shape
+    M = L // tv
+    out = np.empty((L, d), dtype=np.float32)
+    lanes = np.arange(tv, dtype=np.int64)
+    for u in range(M):
+        keys = ids[offs[u]:offs[u + 1]].astype(np.int64)
+        rows = (keys[:, None] * tv + lanes[None, :]).reshape(-1)
+        k_blk, v_blk = kv[rows], vv[rows]
+        col_fac = np.repeat(k_fac[keys], tv) * (q_fac[u] * scale)
+        for r0 in range(u * tv, (u + 1) * tv, 1024):
+            r1 = min(r0 + 1024, (u + 1) * tv)
+            s = qv[r0:r1] @ k_blk.T
+            s *= col_fac[None, :]
+            if not np.isfinite(s).all():
+                raise FloatingPointError("non-finite attention logits")
+            s -= s.max(axis=1, keepdims=True)
+            np.exp(s, out=s)
+            den = s.sum(axis=1, dtype=np.float64, keepdims=True)
+            s /= den.astype(np.float32)
+            if quant_p:
+                s *= np.float32(448.0)
+                s = grid_round(s, E4M3)
+            o = s @ v_blk
+            o *= v_fac[None, :]
+            out[r0:r1] = o
+    return out
+
+
+def fp8_sparse_forward(q, k, v, tv, offs, ids, fmt: Fmt = E4M3, softmax_scale=None):
+    """Quantised sparse forward on tile-contiguous single-head inputs (attention.py:179-208).
+
+    Returns (out f32 [L,d], dict of the intermediate codes/scales).
+    """
+    q = np.ascontiguousarray(q, dtype=np.float32)
+    k = np.ascontiguousarray(k, dtype=np.float32)
+    v = np.ascontiguousarray(v, dtype=np.float32)
+    for name, a in (("q", q), ("k", k), ("v", v)):
+        if not np.isfinite(a).all():
+            raise ValueError(f"{name} contains non-finite values")
+    scale = _softmax_scale(q.shape[1], softmax_scale)
+    qc, qs = quantize_qk_tilewise(q, tv, fmt)
+    kc, ks = quantize_qk_tilewise(k, tv, fmt)
+    vc, vs = quantize_v_channelwise(v, fmt)
+    out = _tile_attention(
+        decode(qc, fmt), decode(kc, fmt), decode(vc, fmt), tv, offs, ids,
+        qs.astype(np.float32), ks.astype(np.float32), (vs * (1.0 / 448.0)).astype(np.float32),
+        scale, quant_p=True,
+    )
+    return out, dict(q_codes=qc, q_scales=qs, k_codes=kc, k_scales=ks, v_codes=vc, v_scales=vs)
+
+
+def sparse_forward_f32(q, k, v, tv, offs, ids, softmax_scale=None):
+    """Full-precision sparse oracle == the passthrough branch (attention.py:165-176, :192-194)."""
+    q = np.ascontiguousarray(q, dtype=np.float32)
+    M = q.shape[0] // tv
+    ones = np.ones(M, dtype=np.float32)
+    return _tile_attention(q, np.asarray(k, np.float32), np.asarray(v, np.float32), tv, offs, ids,
+                           ones, ones, np.ones(q.shape[1], np.float32),
+                           _softmax_scale(q.shape[1], softmax_scale), quant_p=False)
+
+
+def onepass_forward(codes: dict, tv, offs, ids, fmt: Fmt = E4M3, softmax_scale=None, block=128, tau=0.0):
+    """Emulation of the GPU kernel's one-pass schedule (NOT the reference semantics).
+
+    Keys are visited per key tile in 128-key blocks (tiles padded to a multiple
+    of 128); the running row max m is updated per block, the unnormalised
+    weights 448*exp(x - m) are rounded to E4M3 before the PV product, the
+    denominator sums the unrounded weights.  Used to check the CUDA kernel
+    tightly; the reference-facing check is against ``fp8_sparse_forward``.
+    """
+    qv = decode(codes["q_codes"], fmt).astype(np.float64)
+    kv = decode(codes["k_codes"], fmt).astype(np.float64)
+    vv = decode(codes["v_codes"], fmt).astype(np.float64)
+    qs, ks, vs = codes["q_scales"], codes["k_scales"], codes["v_scales"]
+    L, d = qv.shape
+    M = L // tv
+    scale = float(_softmax_scale(d, softmax_scale))
+    log2e = 1.0 / math.log(2.0)
+    out = np.empty((L, d), dtype=np.float64)
+    for u in range(M):
+        qrows = qv[u * tv:(u + 1) * tv]
+        m = np.full(tv, -np.inf)
+        lsum = np.zeros(tv)
+        acc = np.zeros((tv, d))
+        for vt in ids[offs[u]:offs[u + 1]]:
+            c = float(np.float32(np.float32(qs[u]) * np.float32(ks[vt]) * np.float32(scale * log2e)))
+            for b0 in range(0, tv, block):
+                b1 = min(b0 + block, tv)
+                kb = kv[vt * tv + b0: vt * tv + b1]
+                vb = vv[vt * tv + b0: vt * tv + b1]
+                s = (qrows @ kb.T) * c
+                mb = s.max(axis=1)
+                if not np.isfinite(m).any():
+                    m_new = mb
+                elif tau > 0.0:
+                    # lazy rescale per 32-row warp: the kernel keeps the reference
+                    # max unless some row of the warp exceeds it by more than tau
+                    m_new = m.copy()
+                    for w0 in range(0, tv, 32):
+                        sl = slice(w0, min(w0 + 32, tv))
+                        if np.any(mb[sl] > m[sl] + tau):
+                            m_new[sl] = np.maximum(m[sl], mb[sl])
+                else:
+                    m_new = np.maximum(m, mb)
+                alpha = np.where(np.isfinite(m), np.exp2(m - m_new), 0.0)
+                p = np.exp2(s - m_new[:, None] + (math.log2(448.0) - tau))
+                lsum = lsum * alpha + p.sum(axis=1)
+                pq = grid_round(p.astype(np.float32), E4M3).astype(np.float64)
+                acc = acc * alpha[:, None] + pq @ vb
+                m = m_new
+        out[u * tv:(u + 1) * tv] = acc / lsum[:, None] * vs[None, :]
+    return out.astype(np.float32)
+
+
+# --------------------------------------------------------------------------
+# metrics used as parity checkers -- fp8sta/metrics.py:41-62
+# --------------------------------------------------------------------------
+def cosine(a, b) -> float:
+    x = np.asarray(a, np.float64).ravel()
+    y = np.asarray(b, np.float64).ravel()
+    mx, my = np.abs(x).max(), np.abs(y).max()
+    if mx == 0.0 and my == 0.0:
+        return 1.0
+    if mx == 0.0 or my == 0.0:
+        return 0.0
+    x, y = x / mx, y / my
+    return float(min(1.0, max(-1.0, np.dot(x, y) / math.sqrt(np.dot(x, x) * np.dot(y, y)))))
+
+
+def max_abs(a, b) -> float:
+    return float(np.max(np.abs(np.asarray(a, np.float64) - np.asarray(b, np.float64))))
+
+
+# --------------------------------------------------------------------------
+# synthetic inputs -- fp8sta/experiment.py:90-115 (Philox keyed by coordinates)
+# --------------------------------------------------------------------------
+def gen_inputs(seed: int, step: int, head: int, L: int, d: int, dist: str = "gaussian",
+               sigma: float = 1.0, lo: float = -1.0, hi: float = 1.0):
+    """q, k, v float32 [L, d] exactly as the reference draws them (tile-contiguous rows)."""
+    out = []
+    for tag in (1, 2, 3):  # q, k, v
+        key = ((((step << 24) | (head << 8) | tag)) << 64) | (seed & 0xFFFFFFFFFFFFFFFF)
+        gen = np.random.Generator(np.random.Philox(key=key))
+        if dist == "gaussian":
+            x = np.float32(sigma) * gen.standard_normal((L, d), dtype=np.float32)
+        elif dist == "uniform":
+            x = gen.random((L, d), dtype=np.float32) * np.float32(hi - lo) + np.float32(lo)
+        elif dist == "heavy":
+            col = (10.0 ** gen.uniform(-1.0, 1.0, size=d)).astype(np.float32)
+            x = gen.standard_normal((L, d), dtype=np.float32) * col[None, :]
+        else:
+            raise ValueError(f"unknown distribution {dist!r}")
+        out.append(x)
+    return tuple(out)

@@ -1,0 +1,221 @@
+"""Device path: quantise + sliding-tile sparse FP8 attention on B200 through libfpsa.
+
+``FpsaPlan`` owns the device state of one problem shape (window CSR, work
+list, FP8 code / scale buffers) so repeated calls allocate nothing;
+``fps_attention`` is the one-call functional form.  Tensors are torch CUDA
+tensors; torch supplies device memory and the current stream, all compute is
+in libfpsa's sm_100a kernels.  There is no CPU fallback.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+
+import numpy as np
+
+from . import _lib
+from .fp8 import E4M3, Fp8Format
+from .sparsity import BlockMask, WindowSpec, build_block_mask
+
+BLOCK = 128  # rows per query block / keys per key block of the attention kernel
+
+
+def _torch():
+    import torch  # local import: host-only users of the package need no CUDA
+
+    return torch
+
+
+def _ptr(t) -> int:
+    return t.data_ptr()
+
+
+def _stream():
+    return _torch().cuda.current_stream().cuda_stream
+
+
+def _dtype_id(t) -> int:
+    torch = _torch()
+    if t.dtype == torch.float32:
+        return _lib.F32
+    if t.dtype == torch.bfloat16:
+        return _lib.BF16
+    raise NotImplementedError(f"input dtype {t.dtype} not supported (float32 / bfloat16)")
+
+
+def tile_pitch(tile_volume: int) -> int:
+    """Rows per tile slot in the padded code layout (multiple of 128)."""
+    return -(-tile_volume // BLOCK) * BLOCK
+
+
+def worklist(heads: int, mask: BlockMask, tile_volume: int) -> np.ndarray:
+    """(head, query tile, first q-block) items, longest first within each head."""
+    L = _lib.lib()
+    n = ctypes.c_int64(0)
+    td = _lib.dims3(mask.tile_grid_dims)
+    offs = np.ascontiguousarray(mask.offsets, dtype=np.int32)
+    _lib.check(L.fpsa_attn_worklist(heads, td, tile_volume, offs.ctypes.data_as(_lib._pi32), None, 0,
+                                    ctypes.byref(n)))
+    items = np.empty(3 * n.value, dtype=np.int32)
+    _lib.check(L.fpsa_attn_worklist(heads, td, tile_volume, offs.ctypes.data_as(_lib._pi32),
+                                    items.ctypes.data_as(_lib._pi32), n.value, ctypes.byref(n)))
+    return items
+
+
+class FpsaPlan:
+    """Device buffers + launch parameters for one (grid, tile, window, heads, d, fmt).
+
+    Layouts accepted by :meth:`quantize` / :meth:`__call__`:
+      ``"lhd"``  [L, H, d]  (one sample of Wan's [B, L, H, d])
+      ``"hld"``  [H, L, d]
+      ``"ld"``   [L, d]     single head
+    in natural (t, h, w) token order, or with ``tile_order=True`` rows already
+    tile-contiguous (the reference's convention, fp8sta/attention.py:36-61).
+    """
+
+    def __init__(self, grid, tile, window, heads: int, d: int, fmt: Fp8Format = E4M3, *,
+                 device="cuda", tau: float = 8.0, pitch: int | None = None):
+        torch = _torch()
+        self.grid = tuple(int(x) for x in grid)
+        self.tile = tuple(int(x) for x in tile)
+        self.window = window if isinstance(window, WindowSpec) else WindowSpec(*window)
+        self.heads, self.d, self.fmt, self.tau = int(heads), int(d), fmt, float(tau)
+        out = _lib.Dims3()
+        _lib.check(_lib.lib().fpsa_tile_grid(_lib.dims3(self.grid), _lib.dims3(self.tile), out))
+        self.tile_dims = (out.t, out.h, out.w)
+        self.M = out.t * out.h * out.w
+        self.tv = self.tile[0] * self.tile[1] * self.tile[2]
+        self.L = self.grid[0] * self.grid[1] * self.grid[2]
+        self.pitch = tile_pitch(self.tv) if pitch is None else int(pitch)
+        self.mask = build_block_mask(self.window, self.tile_dims)
+        self.device = torch.device(device)
+        dev = self.device
+        self.offs = torch.from_numpy(self.mask.offsets.astype(np.int32)).to(dev)
+        self.ids = torch.from_numpy(np.ascontiguousarray(self.mask.ids, dtype=np.int32)).to(dev)
+        items = worklist(self.heads, self.mask, self.tv)
+        self.n_items = items.size // 3
+        self.items = torch.from_numpy(items).to(dev)
+        rows = self.heads * self.M * self.pitch
+        self.q_codes = torch.empty(rows * self.d, dtype=torch.uint8, device=dev)
+        self.k_codes = torch.empty_like(self.q_codes)
+        self.v_codes = torch.empty_like(self.q_codes)
+        self.q_scales = torch.empty(self.heads * self.M, dtype=torch.float64, device=dev)
+        self.k_scales = torch.empty_like(self.q_scales)
+        self.v_scales = torch.empty(self.heads * self.d, dtype=torch.float64, device=dev)
+        self.workspace = torch.empty(self.heads * self.d, dtype=torch.int32, device=dev)
+        self.err = torch.zeros(1, dtype=torch.int32, device=dev)
+
+    # ------------------------------------------------------------------ accounting
+    @property
+    def density(self) -> float:
+        return self.mask.nnz / (self.M * self.M)
+
+    @property
+    def flops(self) -> int:
+        """Algorithmic FLOPs of one call: heads * sum_u |W(u)| * 4 tv^2 d (metrics.py:91-102)."""
+        return self.heads * self.mask.nnz * 4 * self.tv * self.tv * self.d
+
+    # ------------------------------------------------------------------ strides
+    def _strides(self, x, layout: str):
+        if x.device.type != "cuda":
+            raise ValueError("inputs must be CUDA tensors")
+        if x.stride(-1) != 1:
+            raise ValueError("channel dimension must be contiguous")
+        if layout == "lhd":
+            if tuple(x.shape) != (self.L, self.heads, self.d):
+                raise ValueError(f"expected [L, H, d] = {(self.L, self.heads, self.d)}, got {tuple(x.shape)}")
+            return x.stride(0), x.stride(1)
+        if layout == "hld":
+            if tuple(x.shape) != (self.heads, self.L, self.d):
+                raise ValueError(f"expected [H, L, d] = {(self.heads, self.L, self.d)}, got {tuple(x.shape)}")
+            return x.stride(1), x.stride(0)
+        if layout == "ld":
+            if self.heads != 1 or tuple(x.shape) != (self.L, self.d):
+                raise ValueError(f"expected [L, d] = {(self.L, self.d)}, got {tuple(x.shape)}")
+            return x.stride(0), 0
+        raise ValueError(f"unknown layout {layout!r}")
+
+    # ------------------------------------------------------------------ kernels
+    def quantize(self, q, k, v, layout: str = "lhd", tile_order: bool = False, stream=None) -> None:
+        """K1/K2: per-tile Q/K and per-channel V codes into the plan's buffers."""
+        L = _lib.lib()
+        st = _stream() if stream is None else stream
+        order = _lib.ORDER_TILE if tile_order else _lib.ORDER_NATURAL
+        g, t = _lib.dims3(self.grid), _lib.dims3(self.tile)
+        f = self.fmt.abi_id
+        for x, codes, scales in ((q, self.q_codes, self.q_scales), (k, self.k_codes, self.k_scales)):
+            ts, hs = self._strides(x, layout)
+            _lib.check(L.fpsa_quantize_qk(_ptr(x), _dtype_id(x), ts, hs, self.heads, g, t, self.d, self.pitch,
+                                          order, f, _ptr(codes), _ptr(scales), _ptr(self.err), st))
+        ts, hs = self._strides(v, layout)
+        _lib.check(L.fpsa_quantize_v(_ptr(v), _dtype_id(v), ts, hs, self.heads, g, t, self.d, self.pitch, order,
+                                     f, _ptr(self.v_codes), _ptr(self.v_scales), _ptr(self.workspace),
+                                     _ptr(self.err), st))
+
+    def attention(self, out, layout: str = "lhd", tile_order: bool = False, softmax_scale: float | None = None,
+                  stream=None) -> None:
+        """K4 over the quantised buffers; writes `out` (f32 or bf16)."""
+        torch = _torch()
+        scale = np.float32(1.0 / math.sqrt(self.d)) if softmax_scale is None else np.float32(softmax_scale)
+        if not scale > 0:
+            raise ValueError("softmax_scale must be > 0")
+        ts, hs = self._strides(out, layout)
+        odt = {torch.float32: _lib.F32, torch.bfloat16: _lib.BF16}.get(out.dtype)
+        if odt is None:
+            raise NotImplementedError(f"output dtype {out.dtype} not supported")
+        st = _stream() if stream is None else stream
+        _lib.check(_lib.lib().fpsa_attn_fwd(
+            _ptr(self.q_codes), _ptr(self.k_codes), _ptr(self.v_codes), _ptr(self.q_scales), _ptr(self.k_scales),
+            _ptr(self.v_scales), self.heads, _lib.dims3(self.grid), _lib.dims3(self.tile), self.d, self.pitch,
+            _ptr(self.offs), _ptr(self.ids), _ptr(self.items), self.n_items, float(scale), self.fmt.abi_id,
+            self.tau, _ptr(out), odt, ts, hs, _lib.ORDER_TILE if tile_order else _lib.ORDER_NATURAL, st))
+
+    def check_finite(self) -> None:
+        """Raise ValueError if a quantised input held a non-finite value (synchronises)."""
+        if int(self.err.item()) != 0:
+            self.err.zero_()
+            raise ValueError("non-finite value in quantization input")
+
+    def __call__(self, q, k, v, layout: str = "lhd", out=None, out_dtype=None, tile_order: bool = False,
+                 softmax_scale: float | None = None):
+        torch = _torch()
+        if out is None:
+            dt = out_dtype or (q.dtype if q.dtype in (torch.float32, torch.bfloat16) else torch.float32)
+            out = torch.empty(q.shape, dtype=dt, device=q.device)
+        self.quantize(q, k, v, layout, tile_order)
+        self.attention(out, layout, tile_order, softmax_scale)
+        return out
+
+
+_PLANS: dict = {}
+
+
+def fps_attention(q, k, v, grid, tile, window, *, fmt: Fp8Format = E4M3, softmax_scale: float | None = None,
+                  layout: str = "blhd", out_dtype=None, tau: float = 8.0):
+    """Joint tile-wise FP8 quantisation + sliding-tile sparse attention, natural token order.
+
+    q, k, v: [B, L, H, d] (``layout="blhd"``, Wan / HunyuanVideo convention)
+    or [L, H, d] (``"lhd"``), bf16 or f32 CUDA tensors.  Returns the same
+    shape in ``out_dtype`` (default: input dtype).
+    """
+    batched = layout == "blhd"
+    if batched:
+        B, L, H, d = q.shape
+    elif layout == "lhd":
+        B, (L, H, d) = 1, q.shape
+    else:
+        raise ValueError(f"unknown layout {layout!r}")
+    win = window if isinstance(window, WindowSpec) else WindowSpec(*window)
+    key = (tuple(grid), tuple(tile), win.dims, H, d, fmt.name, str(q.device), tau)
+    plan = _PLANS.get(key)
+    if plan is None:
+        plan = FpsaPlan(grid, tile, win, H, d, fmt, device=q.device, tau=tau)
+        _PLANS[key] = plan
+    torch = _torch()
+    out = torch.empty(q.shape, dtype=out_dtype or q.dtype, device=q.device)
+    for b in range(B):
+        sl = (lambda x: x[b]) if batched else (lambda x: x)
+        plan.quantize(sl(q), sl(k), sl(v), "lhd")
+        plan.attention(sl(out), "lhd", softmax_scale=softmax_scale)
+    return out
