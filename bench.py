@@ -1,0 +1,390 @@
+"""Benchmark: sliding-tile sparse FP8 attention forward at the Wan2.1-14B 720p shape.
+
+One step = the hot path over one batch element: per-tile Q/K and per-channel
+V FP8 quantisation of bf16 [L, H, d] inputs in natural (t,h,w) order, then
+the sparse FP8 attention forward writing bf16 [L, H, d] (libfpsa kernels).
+N GPUs: one process per GPU (torchrun), each rank owns one batch element of
+all 40 heads (weak scaling, no data-path collective), timing = max over ranks.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "sparse FP8 attn fwd ms + eff. TFLOPS (% FP8 peak) @Wan2.1-14B 720p, 1/2/4/8 GPU"
+FP8_SPEC_TFLOPS = 4500.0
+
+CONFIGS = {
+    # name: grid, heads, d, tile, window
+    "wan14b_720p": ((21, 45, 80), 40, 128, (3, 5, 16), (5, 5, 3)),
+    "wan14b_720p_w333": ((21, 45, 80), 40, 128, (3, 5, 16), (3, 3, 3)),
+    "wan13b_480p": ((21, 30, 52), 12, 128, (3, 10, 4), (3, 3, 5)),
+    "hunyuan_720p": ((33, 45, 80), 24, 128, (3, 5, 16), (5, 5, 3)),
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default="wan14b_720p", choices=sorted(CONFIGS))
+    ap.add_argument("--tau", type=float, default=8.0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0, help="budget of the cpu_baseline sample")
+    return ap.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# ---------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """NVML sampling of SM clock and throttle reasons during the timed region."""
+
+    REASONS = {
+        0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+        0x80: "hw_power_brake_slowdown", 0x4: "sw_power_cap", 0x1: "gpu_idle", 0x2: "applications_clocks_setting",
+    }
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nvml = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception as exc:  # pragma: no cover - reported in the JSON
+            self.nvml, self.err = None, str(exc)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nvml.nvmlDeviceGetClockInfo(self.h, self.nvml.NVML_CLOCK_SM))
+                r = self.nvml.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def __enter__(self):
+        if self.nvml:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nvml:
+            self.t.join()
+
+    def summary(self):
+        if not self.nvml:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"]}
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None, "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------- peaks
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+def fp8_gemm_peak(torch):
+    """Same-run dense FP8 GEMM throughput (cuBLAS via torch._scaled_mm, 8192^3, best of 10), TF/s."""
+    try:
+        n = 8192
+        a = torch.randn(n, n, device="cuda").to(torch.float8_e4m3fn)
+        b = torch.randn(n, n, device="cuda").to(torch.float8_e4m3fn).t()
+        one = torch.ones((), device="cuda")
+        for _ in range(3):
+            torch._scaled_mm(a, b, scale_a=one, scale_b=one, out_dtype=torch.bfloat16)
+        best = 1e9
+        for _ in range(10):
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            torch._scaled_mm(a, b, scale_a=one, scale_b=one, out_dtype=torch.bfloat16)
+            e.record()
+            e.synchronize()
+            best = min(best, s.elapsed_time(e))
+        return 2 * n ** 3 / (best * 1e-3) / 1e12
+    except Exception:
+        return None
+
+
+def ncu_traffic(config_name: str):
+    """dram bytes per attention launch from the committed ncu --set full summary, if any."""
+    path = os.path.join(ROOT, "profiles", "attn_ncu_summary.json")
+    try:
+        with open(path) as f:
+            data = json.load(f)
+        return data.get(config_name, {}).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+# ---------------------------------------------------------------------------- CPU legs
+def cpu_leg(cfg, budget_s: float, seed: int = 0):
+    """Oracle port (reference algorithm) on a bounded sample of one head; returns dict."""
+    import oracle as O
+    from oracle.cpu_sample import sample_forward, sample_tiles
+
+    grid, H, d, tile, win = cfg
+    L = grid[0] * grid[1] * grid[2]
+    tv = tile[0] * tile[1] * tile[2]
+    q, k, v = O.gen_inputs(seed, 1, 0, L, d)
+    dims = O.tile_grid_dims(grid, tile)
+    offs, ids = O.window_lists(dims, win)
+    M = dims[0] * dims[1] * dims[2]
+    # calibrate on a few tiles, then size the sample to the budget
+    _, fl0, s0 = sample_forward(q, k, v, tv, offs, ids, sample_tiles(M, 4))
+    n = int(max(4, min(M, 4 * budget_s / max(s0, 1e-3) * 0.8)))
+    tiles = sample_tiles(M, n)
+    _, fl, secs = sample_forward(q, k, v, tv, offs, ids, tiles)
+    return {"flops": fl, "seconds": secs, "tiles": len(tiles), "M": M, "L": L}
+
+
+def run_reference(args):
+    """--impl reference: the reference algorithm (oracle port) on the host cores, rank 0 only."""
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    cfg = CONFIGS[args.config]
+    grid, H, d, tile, win = cfg
+    import oracle as O
+    from oracle.cpu_sample import sample_forward, sample_tiles
+
+    L = grid[0] * grid[1] * grid[2]
+    tv = tile[0] * tile[1] * tile[2]
+    q, k, v = O.gen_inputs(0, 1, 0, L, d)
+    dims = O.tile_grid_dims(grid, tile)
+    offs, ids = O.window_lists(dims, win)
+    M = dims[0] * dims[1] * dims[2]
+    _, _, s0 = sample_forward(q, k, v, tv, offs, ids, sample_tiles(M, 4))
+    per_step = 150.0 / max(1, args.steps + args.warmup)  # whole run within a few minutes
+    n = int(max(2, min(M, 4 * per_step / max(s0, 1e-3) * 0.8)))
+    tiles = sample_tiles(M, n)
+    for _ in range(args.warmup):
+        sample_forward(q, k, v, tv, offs, ids, tiles)
+    fl = secs = 0.0
+    for _ in range(args.steps):
+        _, f, s = sample_forward(q, k, v, tv, offs, ids, tiles)
+        fl += f
+        secs += s
+    tflops = fl / secs / 1e12
+    cores = os.cpu_count()
+    sample = (f"{len(tiles)} of {M} query tiles of 1 of {H} heads per step (reference algorithm: "
+              f"oracle port of fp8sta.fp8_sparse_forward, numpy, {cores} threads)")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": tflops, "unit": "TFLOPS", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": secs / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (Philox gaussian, reference generator)",
+        "config": {"workload": args.config, "grid": grid, "heads": H, "d": d, "tile": tile, "window": win},
+        "cpu_baseline": {"value": tflops, "unit": "TFLOPS", "cores": cores, "kind": "port", "sample": sample},
+        "e2e": {"value": tflops, "unit": "TFLOPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+# ---------------------------------------------------------------------------- GPU leg
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import torch
+    import torch.distributed as dist
+
+    import paper_2506_04648_b200 as fpsa
+
+    world, rank, local = dist_env()
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    grid, H, d, tile, win = CONFIGS[args.config]
+    L = grid[0] * grid[1] * grid[2]
+
+    gen = torch.Generator(device=dev).manual_seed(1234 + rank)
+    q = torch.randn((L, H, d), generator=gen, device=dev).to(torch.bfloat16)
+    k = torch.randn((L, H, d), generator=gen, device=dev).to(torch.bfloat16)
+    v = torch.randn((L, H, d), generator=gen, device=dev).to(torch.bfloat16)
+    out = torch.empty_like(q)
+    plan = fpsa.FpsaPlan(grid, tile, win, H, d, tau=args.tau, device=dev)
+    flops = plan.flops  # per rank (one batch element, all heads)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    stream = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        plan.quantize(q, k, v, "lhd")
+        plan.attention(out, "lhd")
+    torch.cuda.synchronize()
+    plan.check_finite()
+
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+           torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(dev.index) as clocks:
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        for i in range(args.steps):
+            ev[i][0].record(stream)
+            plan.quantize(q, k, v, "lhd")
+            ev[i][1].record(stream)
+            plan.attention(out, "lhd")
+            ev[i][2].record(stream)
+        t1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    ms_total = t0.elapsed_time(t1)
+    ms_quant = sum(a.elapsed_time(b) for a, b, _ in ev) / args.steps
+    ms_attn = sum(b.elapsed_time(c) for _, b, c in ev) / args.steps
+    ms_step = ms_total / args.steps
+    if world > 1:
+        tt = torch.tensor([ms_step, ms_attn, ms_quant], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms_step, ms_attn, ms_quant = tt.tolist()
+    total_flops = flops * world
+    value = total_flops / (ms_step * 1e-3) / 1e12
+
+    # ---------------- e2e through the public API with pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        qh, kh, vh = (x.cpu().pin_memory() for x in (q, k, v))
+        oh = torch.empty(out.shape, dtype=out.dtype).pin_memory()
+        qd, kd, vd = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
+        steps_e2e = max(3, min(args.steps, 10))
+        for _ in range(2):
+            qd.copy_(qh, non_blocking=True); kd.copy_(kh, non_blocking=True); vd.copy_(vh, non_blocking=True)
+            plan(qd, kd, vd, "lhd", out=out)
+            oh.copy_(out, non_blocking=True)
+        torch.cuda.synchronize()
+        barrier()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record(stream)
+        for _ in range(steps_e2e):
+            qd.copy_(qh, non_blocking=True); kd.copy_(kh, non_blocking=True); vd.copy_(vh, non_blocking=True)
+            plan(qd, kd, vd, "lhd", out=out)
+            oh.copy_(out, non_blocking=True)
+        e.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        ms_e2e = s.elapsed_time(e) / steps_e2e
+        if world > 1:
+            tt = torch.tensor([ms_e2e], device=dev, dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            ms_e2e = tt.item()
+        e2e = {"value": total_flops / (ms_e2e * 1e-3) / 1e12, "unit": "TFLOPS", "ms_per_step": ms_e2e,
+               "h2d_bytes_per_step": 3 * q.numel() * q.element_size(),
+               "d2h_bytes_per_step": out.numel() * out.element_size(),
+               "api": "paper_2506_04648_b200.FpsaPlan.__call__ (quantize + attention via the C ABI), pinned host"}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return 0
+
+    peaks = measured_peaks()
+    fp8_meas = fp8_gemm_peak(torch)
+    if fp8_meas:
+        peak, peak_src = fp8_meas, "same-run cuBLAS FP8 e4m3 GEMM 8192^3 (torch._scaled_mm), burst"
+    else:
+        peak = 2.0 * float(peaks.get("bf16_tflops", 1590.0))
+        peak_src = "2 x measured bf16 dense (MEASURED_PEAKS.json)"
+    attn_tflops = flops / (ms_attn * 1e-3) / 1e12
+    # quantiser: algorithmic bytes = bf16 q,k,v read once + e4m3 codes written (9 B per element)
+    qbytes = 3 * L * H * d * 2 + 3 * L * H * d
+    hbm = float(peaks.get("hbm_gbs", 6650.0))
+    line = {
+        "metric": METRIC,
+        "value": value,
+        "unit": "TFLOPS",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms_step,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "e4m3",
+        "data": "synthetic (torch.randn bf16 q/k/v, natural (t,h,w) token order)",
+        "config": {
+            "workload": args.config, "grid": grid, "heads": H, "d": d, "tile": tile, "window": win,
+            "density": plan.density, "global_batch": world, "per_gpu_batch": 1,
+            "flops_per_step_per_gpu": flops, "tau_log2": args.tau,
+            "parallelism": f"head-parallel x batch, {world} rank(s), no collective",
+            "l2": "inputs larger than L2 (bf16 q,k,v = %.2f GB per rank; codes %.2f GB)" % (
+                3 * q.numel() * 2 / 1e9, 3 * plan.q_codes.numel() / 1e9),
+        },
+        "ms_attention": ms_attn,
+        "ms_quantize": ms_quant,
+        "frac_fp8_spec": attn_tflops / FP8_SPEC_TFLOPS,
+        "step_frac_fp8_spec": value / world / FP8_SPEC_TFLOPS,
+        "roofline": {
+            "bound": "tensor", "kernel": "fpsa_attn_kernel", "achieved": attn_tflops, "peak": peak,
+            "unit": "TFLOP/s", "frac": attn_tflops / peak, "peak_source": peak_src,
+            "traffic": ncu_traffic(args.config),
+            "algorithmic": "sum_u |W(u)| * 4 tv^2 d per head (metrics.py:91-102), %d FLOP per launch" % flops,
+        },
+        "roofline_quantize": {
+            "bound": "hbm", "kernels": "chan_amax_kernel + quant_kernel (q,k,v fused)",
+            "achieved": qbytes / (ms_quant * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
+            "frac": qbytes / (ms_quant * 1e-3) / 1e9 / hbm, "algorithmic_bytes": qbytes,
+        },
+        "clocks": clocks.summary(),
+        "gpu_launches": 3 * args.steps,
+        "e2e": e2e,
+    }
+    if world == 1 and not args.no_cpu:
+        cb = cpu_leg(CONFIGS[args.config], args.cpu_seconds)
+        line["cpu_baseline"] = {
+            "value": cb["flops"] / cb["seconds"] / 1e12, "unit": "TFLOPS", "cores": os.cpu_count(), "kind": "port",
+            "sample": f"{cb['tiles']} of {cb['M']} query tiles of 1 of {H} heads (oracle port of "
+                      f"fp8sta.fp8_sparse_forward, numpy, thread pool), {cb['seconds']:.1f} s",
+        }
+    print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -102,6 +102,16 @@ int fpsa_quantize_v(const void* x, int dtype, int64_t token_stride, int64_t head
                     fpsa_dims3 grid, fpsa_dims3 tile, int32_t d, int32_t tile_pitch, int in_order, int fmt,
                     uint8_t* codes, double* scales, void* workspace, int32_t* err_flag, void* stream);
 
+/* Fused form of fpsa_quantize_qk(q) + fpsa_quantize_qk(k) + fpsa_quantize_v(v)
+ * for three tensors with the same dtype and strides: one channel-amax pass
+ * over v, then a single launch that quantises all three (bit-identical to the
+ * separate calls).  workspace: device, >= heads*d*4 bytes. */
+int fpsa_quantize_qkv(const void* q, const void* k, const void* v, int dtype, int64_t token_stride,
+                      int64_t head_stride, int32_t heads, fpsa_dims3 grid, fpsa_dims3 tile, int32_t d,
+                      int32_t tile_pitch, int in_order, int fmt, uint8_t* q_codes, uint8_t* k_codes,
+                      uint8_t* v_codes, double* q_scales, double* k_scales, double* v_scales, void* workspace,
+                      int32_t* err_flag, void* stream);
+
 /* Work list for fpsa_attn_fwd: one entry per (head, query tile, pair of
  * 128-row query blocks), longest first.  Host-side; n_items returns the
  * count, items (capacity `cap`, 3 int32 each: head, tile, first q-block). */

@@ -47,6 +47,8 @@ constexpr int kThreads = 320;
 constexpr int kStages = 4;
 constexpr int kBlk = 128;  // rows per query block and keys per key block
 constexpr float kLog2_448 = 8.807354922057604f;
+// Columns [kPolyFrom, 128) of every key block take the FMA-pipe exp2; the rest MUFU ex2.
+constexpr int kPolyFrom = 96;
 
 struct AttnParams {
   const double* q_scales;
@@ -97,6 +99,47 @@ __device__ __forceinline__ float max3(float a, float b, float c) {
   asm("max.f32 %0, %1, %2, %3;" : "=f"(y) : "f"(a), "f"(b), "f"(c));
   return y;
 }
+// ---- packed f32x2 arithmetic (sm_100 FFMA2 / FADD2): two lanes per instruction
+struct f2 {
+  float x, y;
+};
+__device__ __forceinline__ f2 fma2(f2 a, f2 b, f2 c) {
+  f2 d;
+  asm("{\n\t.reg .b64 ra, rb, rc, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\tmov.b64 rc, {%6, %7};\n\t"
+      "fma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return d;
+}
+__device__ __forceinline__ f2 add2(f2 a, f2 b) {
+  f2 d;
+  asm("{\n\t.reg .b64 ra, rb, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+      "add.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
+__device__ __forceinline__ f2 bcast(float v) { return f2{v, v}; }
+
+// 2^x for a pair on the FMA pipe (Cody-Waite split + degree-3 minimax, rel. err 7.5e-5),
+// used for a fraction of the columns so that the MUFU pipe is not the only exp source.
+__device__ __forceinline__ f2 exp2_poly(f2 x) {
+  constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23: x + kMagic rounds x to an integer
+  x.x = fmaxf(x.x, -126.0f);  // keeps the exponent add below in range; 2^-126 -> code 0
+  x.y = fmaxf(x.y, -126.0f);
+  const f2 t = add2(x, bcast(kMagic));
+  const f2 j = add2(t, bcast(-kMagic));
+  const f2 f = add2(x, f2{-j.x, -j.y});
+  f2 y = fma2(bcast(0.055180370807647705f), f, bcast(0.24261191487312317f));
+  y = fma2(y, f, bcast(0.6932594180107117f));
+  y = fma2(y, f, bcast(0.9999279975891113f));
+  // scale by 2^j: add j to the exponent field (t's low mantissa bits hold j)
+  return f2{__uint_as_float(__float_as_uint(y.x) + (__float_as_uint(t.x) << 23)),
+            __uint_as_float(__float_as_uint(y.y) + (__float_as_uint(t.y) << 23))};
+}
+
 __device__ __forceinline__ uint32_t e4m3x2(float hi, float lo) {
   uint16_t r;
   asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(r) : "f"(hi), "f"(lo));
@@ -114,6 +157,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __shared__ uint64_t bar_kv_full[kStages], bar_kv_empty[kStages];
   __shared__ uint64_t bar_s_full[2], bar_p_ready[2];
   __shared__ uint32_t s_tmem;
+  __shared__ float s_vscale[D];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int32_t h = p.items[3 * blockIdx.x + 0];
@@ -139,6 +183,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 8) {
     tmem_alloc(&s_tmem, 512);
     tmem_relinquish();
+  }
+  if (warp == 9) {
+    for (int i = lane; i < D; i += 32) s_vscale[i] = (float)p.v_scales[(int64_t)h * D + i];
   }
   tc_fence_before();
   __syncthreads();
@@ -226,9 +273,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       tmem_ld32(tm_s[q] + lane_off + 64, reinterpret_cast<uint32_t*>(s + 64));
       tmem_ld32(tm_s[q] + lane_off + 96, reinterpret_cast<uint32_t*>(s + 96));
       tmem_wait_ld();
+      // Key columns >= valid are padding (zero K/V rows of a key tile's last
+      // block): set to -inf so they drop out of the max, the sum and P
+      // (valid is a multiple of 8, checked on the host).
       if (valid < kBlk) {
 #pragma unroll
-        for (int i = 0; i < kBlk; ++i) s[i] = i < valid ? s[i] : -INFINITY;
+        for (int i = 0; i < kBlk; i += 8) {
+          const bool ok = i < valid;
+#pragma unroll
+          for (int k = i; k < i + 8; ++k) s[k] = ok ? s[k] : -INFINITY;
+        }
       }
       float mx0 = -INFINITY, mx1 = -INFINITY;
 #pragma unroll
@@ -255,24 +309,30 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         tmem_wait_st();
       }
-      const float off = m_ref + tau - kLog2_448;
-      float lsum0 = 0.0f, lsum1 = 0.0f;
+      const f2 cc2 = bcast(c), noff = bcast(kLog2_448 - m_ref - tau);
+      f2 lsum0 = bcast(0.0f), lsum1 = bcast(0.0f);
 #pragma unroll
       for (int i0 = 0; i0 < kBlk; i0 += 32) {
         uint32_t w[8];
 #pragma unroll
-        for (int i = i0; i < i0 + 32; i += 4) {
-          const float p0 = ex2(fmaf(s[i + 0], c, -off));
-          const float p1 = ex2(fmaf(s[i + 1], c, -off));
-          const float p2 = ex2(fmaf(s[i + 2], c, -off));
-          const float p3 = ex2(fmaf(s[i + 3], c, -off));
-          lsum0 += p0 + p1;
-          lsum1 += p2 + p3;
-          w[(i - i0) / 4] = e4m3x2(p1, p0) | (e4m3x2(p3, p2) << 16);
+        for (int k = i0; k < i0 + 32; k += 4) {
+          f2 pa = fma2(f2{s[k], s[k + 1]}, cc2, noff);
+          f2 pb = fma2(f2{s[k + 2], s[k + 3]}, cc2, noff);
+          if (k >= kPolyFrom) {
+            pa = exp2_poly(pa);
+            pb = exp2_poly(pb);
+          } else {
+            pa = f2{ex2(pa.x), ex2(pa.y)};
+            pb = f2{ex2(pb.x), ex2(pb.y)};
+          }
+          lsum0 = add2(lsum0, pa);
+          lsum1 = add2(lsum1, pb);
+          w[(k - i0) / 4] = e4m3x2(pa.y, pa.x) | (e4m3x2(pb.y, pb.x) << 16);
         }
         tmem_st8(tm_s[q] + lane_off + i0 / 4, w);
       }
-      l += lsum0 + lsum1;
+      const f2 lsum = add2(lsum0, lsum1);
+      l += lsum.x + lsum.y;
       tmem_wait_st();
       tc_fence_before();
       mbar_arrive(&bar_p_ready[q]);
@@ -290,7 +350,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     } else {
       token = (int64_t)u * p.tv + r;
     }
-    const double* vs = p.v_scales + (int64_t)h * D;
+    const float* vs = s_vscale;
 #pragma unroll
     for (int cc = 0; cc < D; cc += 32) {
       uint32_t o[32];
@@ -299,7 +359,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (r < p.tv) {
         float f[32];
 #pragma unroll
-        for (int i = 0; i < 32; ++i) f[i] = __uint_as_float(o[i]) * inv_l * (float)__ldg(vs + cc + i);
+        for (int i = 0; i < 32; ++i) f[i] = __uint_as_float(o[i]) * inv_l * vs[cc + i];
         if constexpr (OUT == FPSA_F32) {
           float4* dst = reinterpret_cast<float4*>(static_cast<float*>(p.out) + token * p.out_ts + h * p.out_hs + cc);
 #pragma unroll
@@ -389,6 +449,7 @@ extern "C" int fpsa_attn_fwd(const uint8_t* q_codes, const uint8_t* k_codes, con
   if (d != 64 && d != 128) return fail(FPSA_EUNSUPPORTED, "head dim must be 64 or 128, got " + std::to_string(d));
   const int32_t tv = tile.t * tile.h * tile.w;
   if (tile_pitch < tv || tile_pitch % kBlk) return fail(FPSA_EINVAL, "tile_pitch must be a multiple of 128 >= tile volume");
+  if (tv % 8) return fail(FPSA_EUNSUPPORTED, "tile volume must be a multiple of 8, got " + std::to_string(tv));
   if (!(softmax_scale > 0.0f)) return fail(FPSA_EINVAL, "softmax_scale must be > 0");
   if (fmt != FPSA_E4M3 && fmt != FPSA_E5M2) return fail(FPSA_EINVAL, "fmt must be e4m3 or e5m2");
   if (out_dtype != FPSA_F32 && out_dtype != FPSA_BF16) return fail(FPSA_EUNSUPPORTED, "out dtype must be f32 or bf16");

@@ -17,19 +17,25 @@
 // recomputed exactly: q = x / s in f64, rounded to f32 with round-to-odd,
 // then converted (round-to-odd to 24 bits followed by RNE to <= 4 bits equals
 // direct RNE).  Compile without FTZ: signed zeros and f32 subnormals matter.
+#include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <mutex>
 
 #include <cfloat>
 #include <cstdint>
 
 #include "../../include/fpsa.h"
 #include "fpsa_internal.h"
+#include "sm100.cuh"
 
 namespace fpsa {
 namespace {
 
-constexpr int kQuantThreads = 256;
+constexpr int kQuantThreads = 512;
 constexpr int kQuantWarps = kQuantThreads / 32;
 
 struct Geometry {
@@ -42,41 +48,67 @@ struct Geometry {
   int32_t natural;     // input in natural (t,h,w) order; else tile-contiguous
 };
 
-// Token index of local row r of flat tile u.
-__device__ __forceinline__ int64_t token_of(const Geometry& g, int32_t u, int32_t r) {
-  if (!g.natural) return (int64_t)u * g.tv + r;
+// First token of flat tile u (natural order) or of its tile-contiguous row block.
+__device__ __forceinline__ int32_t tile_base(const Geometry& g, int32_t u) {
+  if (!g.natural) return u * g.tv;
   const int32_t ut = u / (g.dh * g.dw), uh = (u / g.dw) % g.dh, uw = u % g.dw;
+  return ((ut * g.st) * g.gh + uh * g.sh) * g.gw + uw * g.sw;
+}
+// Token offset of local row r from the tile base (identical for every tile).
+__device__ __forceinline__ int32_t local_offset(const Geometry& g, int32_t r) {
+  if (!g.natural) return r;
   const int32_t lt = r / (g.sh * g.sw), lh = (r / g.sw) % g.sh, lw = r % g.sw;
-  const int64_t t = (int64_t)ut * g.st + lt, h = (int64_t)uh * g.sh + lh, w = (int64_t)uw * g.sw + lw;
-  return (t * g.gh + h) * g.gw + w;
+  return (lt * g.gh + lh) * g.gw + lw;
 }
 
+// Per-CTA table of row offsets (in elements), built once with one division
+// chain per row instead of per row per pass.
+constexpr int kMaxTableRows = 2048;
+__device__ __forceinline__ void build_row_table(const Geometry& g, int64_t token_stride, int64_t* table) {
+  if (g.natural)
+    for (int32_t r = threadIdx.x; r < g.tv; r += blockDim.x) table[r] = (int64_t)local_offset(g, r) * token_stride;
+  __syncthreads();
+}
+// Element offset of local row r from the tile's first token.
+__device__ __forceinline__ int64_t row_offset(const Geometry& g, const int64_t* table, int32_t r, int64_t ts) {
+  return g.natural ? table[r] : (int64_t)r * ts;
+}
+
+// Raw vector of VEC consecutive channels (16-bit inputs stay packed in registers).
 template <typename T, int VEC>
-struct Loader;
-template <int VEC>
-struct Loader<float, VEC> {
-  static __device__ __forceinline__ void load(const float* p, float (&v)[VEC]) {
-    if constexpr (VEC == 4) {
-      float4 a = __ldg(reinterpret_cast<const float4*>(p));
-      v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
-    } else {
-      float2 a = __ldg(reinterpret_cast<const float2*>(p));
-      v[0] = a.x; v[1] = a.y;
-    }
+struct Vec;
+template <>
+struct Vec<float, 4> {
+  using raw = float4;
+  static __device__ __forceinline__ raw load(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
+  static __device__ __forceinline__ void unpack(const raw& a, float (&v)[4]) { v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; }
+};
+template <>
+struct Vec<float, 2> {
+  using raw = float2;
+  static __device__ __forceinline__ raw load(const float* p) { return __ldg(reinterpret_cast<const float2*>(p)); }
+  static __device__ __forceinline__ void unpack(const raw& a, float (&v)[2]) { v[0] = a.x; v[1] = a.y; }
+};
+template <>
+struct Vec<__nv_bfloat16, 4> {
+  using raw = uint2;
+  static __device__ __forceinline__ raw load(const __nv_bfloat16* p) { return __ldg(reinterpret_cast<const uint2*>(p)); }
+  static __device__ __forceinline__ void unpack(const raw& a, float (&v)[4]) {
+    v[0] = __uint_as_float(a.x << 16); v[1] = __uint_as_float(a.x & 0xFFFF0000u);
+    v[2] = __uint_as_float(a.y << 16); v[3] = __uint_as_float(a.y & 0xFFFF0000u);
   }
 };
-template <int VEC>
-struct Loader<__nv_bfloat16, VEC> {
-  static __device__ __forceinline__ void load(const __nv_bfloat16* p, float (&v)[VEC]) {
-    if constexpr (VEC == 4) {
-      uint2 a = __ldg(reinterpret_cast<const uint2*>(p));
-      v[0] = __uint_as_float(a.x << 16); v[1] = __uint_as_float(a.x & 0xFFFF0000u);
-      v[2] = __uint_as_float(a.y << 16); v[3] = __uint_as_float(a.y & 0xFFFF0000u);
-    } else {
-      uint32_t a = __ldg(reinterpret_cast<const unsigned int*>(p));
-      v[0] = __uint_as_float(a << 16); v[1] = __uint_as_float(a & 0xFFFF0000u);
-    }
+template <>
+struct Vec<__nv_bfloat16, 2> {
+  using raw = uint32_t;
+  static __device__ __forceinline__ raw load(const __nv_bfloat16* p) { return __ldg(reinterpret_cast<const unsigned int*>(p)); }
+  static __device__ __forceinline__ void unpack(const raw& a, float (&v)[2]) {
+    v[0] = __uint_as_float(a << 16); v[1] = __uint_as_float(a & 0xFFFF0000u);
   }
+};
+template <typename T, int VEC>
+struct Loader {
+  static __device__ __forceinline__ void load(const T* p, float (&v)[VEC]) { Vec<T, VEC>::unpack(Vec<T, VEC>::load(p), v); }
 };
 
 // cvt.rn.satfinite of a pair; `hi` lands in the upper byte.
@@ -99,177 +131,520 @@ __device__ __noinline__ uint32_t encode_exact(float x, double s) {
   return cvt_pair<FMT>(0.0f, f) & 0xFFu;
 }
 
-// Codes of two elements sharing (or not) a scale.
-template <int FMT>
-__device__ __forceinline__ uint32_t encode2(float x0, float x1, double s0, double s1, float r0, float r1,
-                                            bool fast_ok) {
-  const float a0 = x0 * r0, a1 = x1 * r1;
-  const float kLo = 0.99999904632568359375f, kHi = 1.00000095367431640625f;  // 1 -+ 2^-20
-  const uint32_t clo = cvt_pair<FMT>(a1 * kLo, a0 * kLo);
-  const uint32_t chi = cvt_pair<FMT>(a1 * kHi, a0 * kHi);
-  if (fast_ok && clo == chi) return clo;
-  uint32_t c0 = clo & 0xFFu, c1 = clo >> 8;
-  if (!fast_ok || c0 != (chi & 0xFFu)) c0 = encode_exact<FMT>(x0, s0);
-  if (!fast_ok || c1 != (chi >> 8)) c1 = encode_exact<FMT>(x1, s1);
-  return c0 | (c1 << 8);
-}
-
-__device__ __forceinline__ bool finite_f(float v) { return fabsf(v) <= FLT_MAX; }
-
 __device__ __forceinline__ double scale_of(float peak, double maxv) {
   if (peak == 0.0f) return 1.0;
   const double s = __ddiv_rn((double)peak, maxv);
   return s > DBL_MIN ? s : DBL_MIN;
 }
-__device__ __forceinline__ bool rcp_ok(float r) { return r >= FLT_MIN && r <= FLT_MAX; }
 
-template <typename T, int D, int FMT>
-__global__ void __launch_bounds__(kQuantThreads)
-    quant_tile_kernel(const T* __restrict__ x, int64_t token_stride, int64_t head_stride, Geometry g,
-                      uint8_t* __restrict__ codes, double* __restrict__ scales, int32_t* err) {
-  constexpr int VEC = D / 32;
-  constexpr double kMax = FMT == FPSA_E4M3 ? 448.0 : 57344.0;
-  const int32_t u = blockIdx.x, h = blockIdx.y;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const T* xh = x + (int64_t)h * head_stride + lane * VEC;
-
-  // pass 1: tile amax (exact: max of |x| over the tile)
-  float peak = 0.0f;
-  bool bad = false;
-#pragma unroll 4
-  for (int32_t r = warp; r < g.tv; r += kQuantWarps) {
-    float v[VEC];
-    Loader<T, VEC>::load(xh + token_of(g, u, r) * token_stride, v);
-#pragma unroll
-    for (int i = 0; i < VEC; ++i) {
-      bad |= !finite_f(v[i]);
-      peak = fmaxf(peak, fabsf(v[i]));
-    }
-  }
-  __shared__ float s_peak[kQuantWarps];
-  __shared__ int s_bad;
-  if (threadIdx.x == 0) s_bad = 0;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) peak = fmaxf(peak, __shfl_xor_sync(0xffffffffu, peak, o));
-  __syncthreads();
-  if (bad) s_bad = 1;
-  if (lane == 0) s_peak[warp] = peak;
-  __syncthreads();
-  peak = s_peak[0];
-#pragma unroll
-  for (int i = 1; i < kQuantWarps; ++i) peak = fmaxf(peak, s_peak[i]);
-  if (s_bad && err) {
-    if (threadIdx.x == 0) atomicOr(err, 1);
-  }
-  const double s = scale_of(peak, kMax);
+// Per-scale constants of the fast path: f32(1/s) * (1 -+ 2^-20).
+struct Bracket {
+  float lo, hi;
+  bool ok;
+};
+__device__ __forceinline__ Bracket bracket_of(double s) {
   const float r = (float)(1.0 / s);
-  const bool fast = rcp_ok(r);
-
-  // pass 2: codes (re-read hits L2)
-  uint8_t* out = codes + ((int64_t)h * g.M + u) * g.pitch * D + lane * VEC;
-#pragma unroll 4
-  for (int32_t row = warp; row < g.tv; row += kQuantWarps) {
-    float v[VEC];
-    Loader<T, VEC>::load(xh + token_of(g, u, row) * token_stride, v);
-    if constexpr (VEC == 4) {
-      const uint32_t lo = encode2<FMT>(v[0], v[1], s, s, r, r, fast);
-      const uint32_t hi = encode2<FMT>(v[2], v[3], s, s, r, r, fast);
-      *reinterpret_cast<uint32_t*>(out + (int64_t)row * D) = lo | (hi << 16);
-    } else {
-      *reinterpret_cast<uint16_t*>(out + (int64_t)row * D) = (uint16_t)encode2<FMT>(v[0], v[1], s, s, r, r, fast);
-    }
-  }
-  for (int32_t row = g.tv + warp; row < g.pitch; row += kQuantWarps) {
-    if constexpr (VEC == 4)
-      *reinterpret_cast<uint32_t*>(out + (int64_t)row * D) = 0u;
-    else
-      *reinterpret_cast<uint16_t*>(out + (int64_t)row * D) = 0;
-  }
-  if (threadIdx.x == 0) scales[(int64_t)h * g.M + u] = s;
+  const bool ok = r >= FLT_MIN && r <= FLT_MAX / 2;
+  return Bracket{r * 0.99999904632568359375f, r * 1.00000095367431640625f, ok};
 }
 
-// V pass A: per-(head, channel) amax over all tokens, as uint bits of |x|.
+// Same bracket from the f32 peak without f64 arithmetic: r = f32(max_value/peak)
+// is within one f32 ulp of f32(1/s) with s = f64(peak/max_value), and the
+// bracket margin (2^-20) covers that ulp plus the two roundings below.
+template <int FMT>
+__device__ __forceinline__ Bracket bracket_f32(float peak) {
+  constexpr float kMaxF = FMT == FPSA_E4M3 ? 448.0f : 57344.0f;
+  if (peak == 0.0f) return Bracket{0.99999904632568359375f, 1.00000095367431640625f, true};
+  const float r = __fdiv_rn(kMaxF, peak);
+  const bool ok = r >= FLT_MIN && r <= FLT_MAX / 2 && peak >= FLT_MIN;
+  return Bracket{r * 0.99999904632568359375f, r * 1.00000095367431640625f, ok};
+}
+
+__device__ __forceinline__ void mul2(float a0, float a1, float b0, float b1, float& d0, float& d1) {
+  asm("{\n\t.reg .b64 ra, rb, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+      "mul.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(d0), "=f"(d1)
+      : "f"(a0), "f"(a1), "f"(b0), "f"(b1));
+}
+
+// Fast codes of VEC elements: the two bracket values x*lo and x*hi round to
+// the same fp8 code iff that code is the RNE of the exact f64 quotient (see
+// header).  `slow` is raised when any element needs the exact path.
+template <int FMT, int VEC>
+__device__ __forceinline__ uint32_t encode_fast(const float (&v)[VEC], const Bracket (&b)[VEC], bool& slow) {
+  uint32_t clo = 0, chi = 0;
+#pragma unroll
+  for (int e = 0; e < VEC; e += 2) {
+    float l0, l1, h0, h1;
+    mul2(v[e], v[e + 1], b[e].lo, b[e + 1].lo, l0, l1);
+    mul2(v[e], v[e + 1], b[e].hi, b[e + 1].hi, h0, h1);
+    clo |= cvt_pair<FMT>(l1, l0) << (8 * e);
+    chi |= cvt_pair<FMT>(h1, h0) << (8 * e);
+  }
+  slow |= clo != chi;
+  return clo;
+}
+
+template <int FMT, int VEC>
+__device__ __noinline__ uint32_t encode_slow(const float (&v)[VEC], const float (&peak)[VEC]) {
+  constexpr double kMax = FMT == FPSA_E4M3 ? 448.0 : 57344.0;
+  uint32_t c = 0;
+#pragma unroll
+  for (int e = 0; e < VEC; ++e) c |= encode_exact<FMT>(v[e], scale_of(peak[e], kMax)) << (8 * e);
+  return c;
+}
+
+template <int VEC>
+__device__ __forceinline__ void store_codes(uint8_t* p, uint32_t c) {
+  if constexpr (VEC == 4)
+    *reinterpret_cast<uint32_t*>(p) = c;
+  else
+    *reinterpret_cast<uint16_t*>(p) = (uint16_t)c;
+}
+
+// |x| max in the bit domain (exact for floats; NaN/inf bit patterns sort above
+// every finite value, so one compare at the end detects non-finite input).
+template <typename T, int VEC>
+__device__ __forceinline__ uint32_t absmax_bits(const typename Vec<T, VEC>::raw& a, uint32_t m);
+template <>
+__device__ __forceinline__ uint32_t absmax_bits<__nv_bfloat16, 4>(const uint2& a, uint32_t m) {
+  return __vmaxu2(__vmaxu2(m, a.x & 0x7FFF7FFFu), a.y & 0x7FFF7FFFu);
+}
+template <>
+__device__ __forceinline__ uint32_t absmax_bits<__nv_bfloat16, 2>(const uint32_t& a, uint32_t m) {
+  return __vmaxu2(m, a & 0x7FFF7FFFu);
+}
+template <>
+__device__ __forceinline__ uint32_t absmax_bits<float, 4>(const float4& a, uint32_t m) {
+  m = max(m, __float_as_uint(a.x) & 0x7FFFFFFFu);
+  m = max(m, __float_as_uint(a.y) & 0x7FFFFFFFu);
+  m = max(m, __float_as_uint(a.z) & 0x7FFFFFFFu);
+  return max(m, __float_as_uint(a.w) & 0x7FFFFFFFu);
+}
+template <>
+__device__ __forceinline__ uint32_t absmax_bits<float, 2>(const float2& a, uint32_t m) {
+  m = max(m, __float_as_uint(a.x) & 0x7FFFFFFFu);
+  return max(m, __float_as_uint(a.y) & 0x7FFFFFFFu);
+}
+// Reduce the packed accumulator to a float |x| max.
+template <typename T>
+__device__ __forceinline__ float bits_to_peak(uint32_t m) {
+  if constexpr (sizeof(T) == 2) {
+    const uint32_t hi = max(m & 0xFFFFu, m >> 16);
+    return __uint_as_float(hi << 16);
+  } else {
+    return __uint_as_float(m);
+  }
+}
+
+constexpr int kRegRows = 16;  // rows per warp kept in registers (16-bit inputs, tv <= 256)
+
+// One tensor of a fused quantisation launch.
+struct QuantJob {
+  const void* x;
+  int64_t ts, hs;    // token / head strides (elements)
+  uint8_t* codes;    // tile-major padded [heads*M*pitch][D]
+  double* scales;    // per-tile [heads*M] or per-channel [heads*D]
+  int32_t channel;   // 0: one scale per 3D tile, 1: per-channel scale from `amax`
+};
+struct QuantArgs {
+  QuantJob job[3];
+  const uint32_t* amax;  // per-(head, channel) |x| max bits for channel jobs
+  int32_t* err;
+};
+
+// blockIdx = (tile u, head h, job z).  Q/K: tile amax -> f64 scale -> codes;
+// V: codes with the per-channel scales of a preceding chan_amax_kernel.
+template <typename T, int D, int FMT>
+__global__ void __launch_bounds__(kQuantThreads, 1)
+    quant_kernel(Geometry g, QuantArgs a) {
+  constexpr int VEC = D / 32;
+  constexpr double kMax = FMT == FPSA_E4M3 ? 448.0 : 57344.0;
+  constexpr bool kRegCapable = sizeof(T) == 2;
+  using V = Vec<T, VEC>;
+  __shared__ int64_t s_row[kMaxTableRows];
+  __shared__ uint32_t s_peak[kQuantWarps];
+  const QuantJob job = a.job[blockIdx.z];
+  const int32_t u = blockIdx.x, h = blockIdx.y;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  build_row_table(g, job.ts, s_row);
+  const T* xt = static_cast<const T*>(job.x) + (int64_t)h * job.hs + (int64_t)tile_base(g, u) * job.ts + lane * VEC;
+  uint8_t* out = job.codes + ((int64_t)h * g.M + u) * g.pitch * D + lane * VEC;
+  const bool in_regs = kRegCapable && g.tv <= kQuantWarps * kRegRows;
+  typename V::raw raw[kRegCapable ? kRegRows : 1];
+  if (in_regs) {
+#pragma unroll
+    for (int i = 0; i < (kRegCapable ? kRegRows : 1); ++i) {
+      const int32_t r = min(warp + i * kQuantWarps, g.tv - 1);  // clamped: no branch around the load
+      raw[i] = V::load(xt + row_offset(g, s_row, r, job.ts));
+    }
+  }
+  float pk[VEC];  // |x| max behind each element's scale (0 for non-finite input)
+  Bracket b[VEC];
+  if (!job.channel) {
+    uint32_t m = 0;
+    if (in_regs) {
+#pragma unroll
+      for (int i = 0; i < (kRegCapable ? kRegRows : 1); ++i)
+        if (warp + i * kQuantWarps < g.tv) m = absmax_bits<T, VEC>(raw[i], m);
+    } else {
+#pragma unroll 4
+      for (int32_t r = warp; r < g.tv; r += kQuantWarps) m = absmax_bits<T, VEC>(V::load(xt + row_offset(g, s_row, r, job.ts)), m);
+    }
+    // fold the packed lanes to f32 bit patterns first: those compare as integers
+    m = __float_as_uint(bits_to_peak<T>(m));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (lane == 0) s_peak[warp] = m;
+    __syncthreads();
+    m = s_peak[0];
+#pragma unroll
+    for (int i = 1; i < kQuantWarps; ++i) m = max(m, s_peak[i]);
+    float peak = __uint_as_float(m);
+    if (!(peak <= FLT_MAX)) {
+      if (threadIdx.x == 0 && a.err) atomicOr(a.err, 1);
+      peak = 0.0f;
+    }
+    const double sc = scale_of(peak, kMax);
+    const Bracket bb = bracket_of(sc);
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) {
+      pk[e] = peak;
+      b[e] = bb;
+    }
+    if (threadIdx.x == 0) job.scales[(int64_t)h * g.M + u] = sc;
+  } else {
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) {
+      const float peak = __uint_as_float(a.amax[(int64_t)h * D + lane * VEC + e]);
+      pk[e] = peak <= FLT_MAX ? peak : 0.0f;
+      const double sc = scale_of(pk[e], kMax);
+      b[e] = bracket_of(sc);
+      if (u == 0 && warp == 0) job.scales[(int64_t)h * D + lane * VEC + e] = sc;
+    }
+  }
+  bool fast_ok = true;
+#pragma unroll
+  for (int e = 0; e < VEC; ++e) fast_ok &= b[e].ok;
+
+  // Fast codes for every row; the rare rows whose bracket straddles a rounding
+  // boundary are redone exactly afterwards, outside the streaming loop.
+  bool any_slow = !fast_ok;
+  auto emit = [&](int32_t row, const typename V::raw& rw) {
+    float v[VEC];
+    V::unpack(rw, v);
+    bool slow = false;
+    const uint32_t c = encode_fast<FMT, VEC>(v, b, slow);
+    any_slow |= slow;
+    store_codes<VEC>(out + (int64_t)row * D, c);
+  };
+  auto fixup = [&](int32_t row, const typename V::raw& rw) {
+    float v[VEC];
+    V::unpack(rw, v);
+    bool slow = !fast_ok;
+    encode_fast<FMT, VEC>(v, b, slow);
+    if (slow) store_codes<VEC>(out + (int64_t)row * D, encode_slow<FMT, VEC>(v, pk));
+  };
+  if (in_regs) {
+#pragma unroll
+    for (int i = 0; i < (kRegCapable ? kRegRows : 1); ++i) {
+      const int32_t row = warp + i * kQuantWarps;
+      if (row < g.tv) emit(row, raw[i]);
+    }
+    if (__any_sync(0xffffffffu, any_slow)) {
+#pragma unroll
+      for (int i = 0; i < (kRegCapable ? kRegRows : 1); ++i) {
+        const int32_t row = warp + i * kQuantWarps;
+        if (row < g.tv) fixup(row, raw[i]);
+      }
+    }
+  } else {
+#pragma unroll 4
+    for (int32_t row = warp; row < g.tv; row += kQuantWarps) emit(row, V::load(xt + row_offset(g, s_row, row, job.ts)));
+    if (__any_sync(0xffffffffu, any_slow)) {
+#pragma unroll 1
+      for (int32_t row = warp; row < g.tv; row += kQuantWarps) fixup(row, V::load(xt + row_offset(g, s_row, row, job.ts)));
+    }
+  }
+  for (int32_t row = g.tv + warp; row < g.pitch; row += kQuantWarps) store_codes<VEC>(out + (int64_t)row * D, 0u);
+}
+
+// V pass A: per-(head, channel) |x| max over all tokens (bit domain, atomicMax).
 template <typename T, int D>
 __global__ void __launch_bounds__(kQuantThreads)
     chan_amax_kernel(const T* __restrict__ x, int64_t token_stride, int64_t head_stride, int64_t L,
                      int32_t rows_per_block, uint32_t* __restrict__ amax, int32_t* err) {
   constexpr int VEC = D / 32;
+  using V = Vec<T, VEC>;
   const int32_t h = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t t0 = (int64_t)blockIdx.x * rows_per_block;
   const int64_t t1 = min(L, t0 + rows_per_block);
   const T* xh = x + (int64_t)h * head_stride + lane * VEC;
-  float m[VEC];
+  uint32_t m[VEC];
 #pragma unroll
-  for (int i = 0; i < VEC; ++i) m[i] = 0.0f;
-  bool bad = false;
-#pragma unroll 4
+  for (int e = 0; e < VEC; ++e) m[e] = 0;
+#pragma unroll 8
   for (int64_t t = t0 + warp; t < t1; t += kQuantWarps) {
     float v[VEC];
-    Loader<T, VEC>::load(xh + t * token_stride, v);
+    V::unpack(V::load(xh + t * token_stride), v);
 #pragma unroll
-    for (int i = 0; i < VEC; ++i) {
-      bad |= !finite_f(v[i]);
-      m[i] = fmaxf(m[i], fabsf(v[i]));
-    }
+    for (int e = 0; e < VEC; ++e) m[e] = max(m[e], __float_as_uint(v[e]) & 0x7FFFFFFFu);
   }
-  __shared__ float s_m[kQuantWarps][D];
+  __shared__ uint32_t s_m[kQuantWarps][D];
 #pragma unroll
-  for (int i = 0; i < VEC; ++i) s_m[warp][lane * VEC + i] = m[i];
-  if (bad && err) atomicOr(err, 1);
+  for (int e = 0; e < VEC; ++e) s_m[warp][lane * VEC + e] = m[e];
   __syncthreads();
   for (int c = threadIdx.x; c < D; c += kQuantThreads) {
-    float mm = s_m[0][c];
+    uint32_t mm = s_m[0][c];
 #pragma unroll
-    for (int w = 1; w < kQuantWarps; ++w) mm = fmaxf(mm, s_m[w][c]);
-    atomicMax(amax + (int64_t)h * D + c, __float_as_uint(mm));
+    for (int w = 1; w < kQuantWarps; ++w) mm = max(mm, s_m[w][c]);
+    if (mm > 0x7F7FFFFFu && err) atomicOr(err, 1);
+    atomicMax(amax + (int64_t)h * D + c, mm);
   }
 }
 
-// V pass B: codes with per-channel scales, tile-major padded layout.
-template <typename T, int D, int FMT>
-__global__ void __launch_bounds__(kQuantThreads)
-    quant_chan_kernel(const T* __restrict__ x, int64_t token_stride, int64_t head_stride, Geometry g,
-                      const uint32_t* __restrict__ amax, uint8_t* __restrict__ codes, double* __restrict__ scales) {
-  constexpr int VEC = D / 32;
+// ---------------------------------------------------------------------------
+// TMA-fed persistent quantiser (bf16 input, d = 128, tile volume <= 256).
+//
+// One CTA per SM loops over (tensor, head, tile) items.  A producer warp
+// streams each tile into shared memory with 3D TMA loads (one box per run
+// of tile_w consecutive tokens, strided by the token stride, so the gather
+// to tile-major order is done by the copy engine), kTmaStages tiles ahead;
+// 8 consumer warps reduce the tile amax from shared memory and write the
+// codes.  HBM traffic is one read of q/k/v and one write of the codes.
+constexpr int kTmaConsumerWarps = 16;
+constexpr int kTmaThreads = (kTmaConsumerWarps + 1) * 32;
+constexpr int kTmaStages = 3;
+constexpr int kTmaMaxRows = 256;
+constexpr int kTmaD = 128;
+constexpr int kTmaStageBytes = kTmaMaxRows * kTmaD * 2;
+constexpr uint32_t kTmaQueueCap = 2048;
+
+struct TmaQuantArgs {
+  uint8_t* codes[3];
+  double* scales[3];
+  int32_t channel[3];
+  int32_t njobs, heads;
+  const uint32_t* amax;
+  int32_t* err;
+};
+
+template <int FMT>
+__global__ void __launch_bounds__(kTmaThreads, 1)
+    quant_tma_kernel(const __grid_constant__ CUtensorMap tm0, const __grid_constant__ CUtensorMap tm1,
+                     const __grid_constant__ CUtensorMap tm2, Geometry g, TmaQuantArgs a) {
+  using namespace sm100;
+  constexpr int VEC = 4;
   constexpr double kMax = FMT == FPSA_E4M3 ? 448.0 : 57344.0;
-  const int32_t u = blockIdx.x, h = blockIdx.y;
+  using V = Vec<__nv_bfloat16, VEC>;
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ uint64_t full[kTmaStages], empty[kTmaStages];
+  __shared__ uint32_t s_peak[2][kTmaConsumerWarps];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double s[VEC];
-  float r[VEC];
-  bool fast = true;
-#pragma unroll
-  for (int i = 0; i < VEC; ++i) {
-    const float peak = __uint_as_float(amax[(int64_t)h * D + lane * VEC + i]);
-    s[i] = scale_of(peak, kMax);
-    r[i] = (float)(1.0 / s[i]);
-    fast &= rcp_ok(r[i]);
-  }
-  if (u == 0 && warp == 0) {
-#pragma unroll
-    for (int i = 0; i < VEC; ++i) scales[(int64_t)h * D + lane * VEC + i] = s[i];
-  }
-  const T* xh = x + (int64_t)h * head_stride + lane * VEC;
-  uint8_t* out = codes + ((int64_t)h * g.M + u) * g.pitch * D + lane * VEC;
-#pragma unroll 4
-  for (int32_t row = warp; row < g.tv; row += kQuantWarps) {
-    float v[VEC];
-    Loader<T, VEC>::load(xh + token_of(g, u, row) * token_stride, v);
-    if constexpr (VEC == 4) {
-      const uint32_t lo = encode2<FMT>(v[0], v[1], s[0], s[1], r[0], r[1], fast);
-      const uint32_t hi = encode2<FMT>(v[2], v[3], s[2], s[3], r[2], r[3], fast);
-      *reinterpret_cast<uint32_t*>(out + (int64_t)row * D) = lo | (hi << 16);
-    } else {
-      *reinterpret_cast<uint16_t*>(out + (int64_t)row * D) =
-          (uint16_t)encode2<FMT>(v[0], v[1], s[0], s[1], r[0], r[1], fast);
+  const int32_t per_job = a.heads * g.M;
+  const int32_t n_items = a.njobs * per_job;
+  const int32_t runs = g.tv / g.sw;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kTmaStages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], kTmaConsumerWarps);
     }
+    fence_barrier_init();
   }
-  for (int32_t row = g.tv + warp; row < g.pitch; row += kQuantWarps) {
-    if constexpr (VEC == 4)
-      *reinterpret_cast<uint32_t*>(out + (int64_t)row * D) = 0u;
-    else
-      *reinterpret_cast<uint16_t*>(out + (int64_t)row * D) = 0;
+  __syncthreads();
+
+  if (warp == kTmaConsumerWarps) {
+    // ------------------------------------------------------------ producer
+    if (lane == 0) {
+      prefetch_tmap(&tm0);
+      prefetch_tmap(&tm1);
+      prefetch_tmap(&tm2);
+      int k = 0;
+      for (int32_t it = blockIdx.x; it < n_items; it += gridDim.x, ++k) {
+        const int st = k % kTmaStages;
+        if (k >= kTmaStages) mbar_wait(&empty[st], ((k / kTmaStages) - 1) & 1);
+        const int32_t z = it / per_job, rem = it - z * per_job, h = rem / g.M, u = rem - h * g.M;
+        const void* tm = z == 0 ? (const void*)&tm0 : (z == 1 ? (const void*)&tm1 : (const void*)&tm2);
+        uint8_t* dst = smem + st * kTmaStageBytes;
+        mbar_arrive_expect_tx(&full[st], (uint32_t)g.tv * kTmaD * 2);
+        const int32_t base = tile_base(g, u);
+        for (int32_t r = 0; r < runs; ++r) {
+          // run r = (lt, lh) of the tile; in tile order runs are consecutive rows
+          const int32_t lt = r / g.sh, lh = r - lt * g.sh;
+          const int32_t tok = g.natural ? base + (lt * g.gh + lh) * g.gw : base + r * g.sw;
+          tma_load_3d(dst + r * g.sw * kTmaD * 2, tm, 0, tok, h, &full[st]);
+        }
+      }
+    }
+    return;
   }
+  // -------------------------------------------------------------- consumers
+  // Ambiguous elements (the bracket straddles a rounding boundary: mostly
+  // exact ties of bf16 data, ~0.4% of elements) are queued in shared memory
+  // and re-encoded exactly by all consumer threads after the tile.
+  __shared__ uint16_t s_queue[2][kTmaQueueCap];
+  __shared__ uint32_t s_count[2];
+  if (threadIdx.x == 0) s_count[0] = 0;
+  named_bar_sync(1, kTmaConsumerWarps * 32);
+  int k = 0;
+  for (int32_t it = blockIdx.x; it < n_items; it += gridDim.x, ++k) {
+    const int st = k % kTmaStages;
+    const int32_t z = it / per_job, rem = it - z * per_job, h = rem / g.M, u = rem - h * g.M;
+    const bool channel = a.channel[z] != 0;
+    uint8_t* out_tile = a.codes[z] + ((int64_t)h * g.M + u) * g.pitch * kTmaD;
+    uint8_t* out = out_tile + lane * VEC;
+    const uint2* tile = reinterpret_cast<const uint2*>(smem + st * kTmaStageBytes) + lane;
+    mbar_wait(&full[st], (k / kTmaStages) & 1);
+    uint32_t m = 0;
+    if (!channel) {
+#pragma unroll 8
+      for (int32_t r = warp; r < g.tv; r += kTmaConsumerWarps) m = absmax_bits<__nv_bfloat16, VEC>(tile[r * 32], m);
+      m = __float_as_uint(bits_to_peak<__nv_bfloat16>(m));
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+      if (lane == 0) s_peak[k & 1][warp] = m;
+    }
+    named_bar_sync(1, kTmaConsumerWarps * 32);
+    if (threadIdx.x == 0) s_count[(k + 1) & 1] = 0;
+    float pk[VEC];
+    Bracket b[VEC];
+    if (!channel) {
+      m = s_peak[k & 1][0];
+#pragma unroll
+      for (int i = 1; i < kTmaConsumerWarps; ++i) m = max(m, s_peak[k & 1][i]);
+      float peak = __uint_as_float(m);
+      if (!(peak <= FLT_MAX)) {
+        if (warp == 0 && lane == 0 && a.err) atomicOr(a.err, 1);
+        peak = 0.0f;
+      }
+      const Bracket bb = bracket_f32<FMT>(peak);
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) {
+        pk[e] = peak;
+        b[e] = bb;
+      }
+      if (warp == 0 && lane == 0) a.scales[z][(int64_t)h * g.M + u] = scale_of(peak, kMax);
+    } else {
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) {
+        const float peak = __uint_as_float(a.amax[(int64_t)h * kTmaD + lane * VEC + e]);
+        pk[e] = peak <= FLT_MAX ? peak : 0.0f;
+        b[e] = bracket_f32<FMT>(pk[e]);
+        if (u == 0 && warp == 0) a.scales[z][(int64_t)h * kTmaD + lane * VEC + e] = scale_of(pk[e], kMax);
+      }
+    }
+    bool fast_ok = true;
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) fast_ok &= b[e].ok;
+    uint32_t* count = &s_count[k & 1];
+    uint16_t* queue = s_queue[k & 1];
+#pragma unroll 4
+    for (int32_t r = warp; r < g.tv; r += kTmaConsumerWarps) {
+      float v[VEC];
+      V::unpack(tile[r * 32], v);
+      uint32_t clo = 0, chi = 0;
+#pragma unroll
+      for (int e = 0; e < VEC; e += 2) {
+        float l0, l1, h0, h1;
+        mul2(v[e], v[e + 1], b[e].lo, b[e + 1].lo, l0, l1);
+        mul2(v[e], v[e + 1], b[e].hi, b[e + 1].hi, h0, h1);
+        clo |= cvt_pair<FMT>(l1, l0) << (8 * e);
+        chi |= cvt_pair<FMT>(h1, h0) << (8 * e);
+      }
+      store_codes<VEC>(out + (int64_t)r * kTmaD, clo);
+      uint32_t diff = fast_ok ? (clo ^ chi) : 0xFFFFFFFFu;
+      while (diff) {  // rare: enqueue each ambiguous byte as (row, column)
+        const int e = (__ffs(diff) - 1) >> 3;
+        diff &= ~(0xFFu << (8 * e));
+        const uint32_t slot = atomicAdd(count, 1u);
+        if (slot < kTmaQueueCap) queue[slot] = (uint16_t)((r << 7) | (lane * VEC + e));
+      }
+    }
+    named_bar_sync(1, kTmaConsumerWarps * 32);
+    const uint32_t n = *count;
+    if (n <= kTmaQueueCap) {
+      for (uint32_t i = threadIdx.x; i < n; i += kTmaConsumerWarps * 32) {
+        const uint32_t rc = queue[i];
+        const int32_t r = rc >> 7, c = rc & 127;
+        const uint16_t bits = reinterpret_cast<const uint16_t*>(smem + st * kTmaStageBytes)[r * kTmaD + c];
+        const float xv = __uint_as_float((uint32_t)bits << 16);
+        const float peak = channel ? __uint_as_float(a.amax[(int64_t)h * kTmaD + c]) : pk[0];
+        out_tile[(int64_t)r * kTmaD + c] = (uint8_t)encode_exact<FMT>(xv, scale_of(peak <= FLT_MAX ? peak : 0.0f, kMax));
+      }
+    } else {
+      // queue overflow (adversarial data): exact pass over the whole tile
+      for (int32_t r = warp; r < g.tv; r += kTmaConsumerWarps) {
+        float v[VEC];
+        V::unpack(tile[r * 32], v);
+        store_codes<VEC>(out + (int64_t)r * kTmaD, encode_slow<FMT, VEC>(v, pk));
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[st]);
+    for (int32_t r = g.tv + warp; r < g.pitch; r += kTmaConsumerWarps) store_codes<VEC>(out + (int64_t)r * kTmaD, 0u);
+  }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  });
+  return fn;
+}
+
+// [heads][L][d] view of a bf16 input with token / head strides (elements).
+bool make_input_map(CUtensorMap* m, const void* x, int64_t L, int32_t heads, int64_t ts, int64_t hs, int32_t sw) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[3] = {(cuuint64_t)kTmaD, (cuuint64_t)L, (cuuint64_t)heads};
+  cuuint64_t strides[2] = {(cuuint64_t)ts * 2, (cuuint64_t)(hs > 0 ? hs : ts) * 2};
+  cuuint32_t box[3] = {(cuuint32_t)kTmaD, (cuuint32_t)sw, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(x), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+int g_num_sms = 0;
+int num_sms() {
+  if (!g_num_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_num_sms <= 0) g_num_sms = 148;
+  }
+  return g_num_sms;
+}
+
+// Launch the TMA quantiser if the request fits it; returns false to fall back.
+bool try_tma_quant(const void* const* xs, int njobs, int dtype, int64_t ts, int64_t hs, int32_t heads,
+                   const Geometry& g, int32_t d, int fmt, const TmaQuantArgs& a, cudaStream_t st) {
+  if (dtype != FPSA_BF16 || d != kTmaD || g.tv > kTmaMaxRows || g.sw > 256 || (ts * 2) % 16 || (hs * 2) % 16)
+    return false;
+  if (heads > 1 && hs == 0) return false;
+  const int64_t L = (int64_t)g.gt * g.gh * g.gw;
+  CUtensorMap tm[3];
+  for (int i = 0; i < 3; ++i)
+    if (!make_input_map(&tm[i], xs[i < njobs ? i : 0], L, heads, ts, hs, g.sw)) return false;
+  const int smem = kTmaStages * kTmaStageBytes;
+  auto kern = fmt == FPSA_E4M3 ? quant_tma_kernel<FPSA_E4M3> : quant_tma_kernel<FPSA_E5M2>;
+  static bool configured[2] = {false, false};
+  if (!configured[fmt]) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) return false;
+    configured[fmt] = true;
+  }
+  const int64_t items = (int64_t)njobs * heads * g.M;
+  const int grid = (int)std::min<int64_t>(items, num_sms());
+  kern<<<grid, kTmaThreads, smem, st>>>(tm[0], tm[1], tm[2], g, a);
+  return true;
 }
 
 int make_geometry(fpsa_dims3 grid, fpsa_dims3 tile, int32_t d, int32_t pitch, int in_order, Geometry* g) {
@@ -278,6 +653,8 @@ int make_geometry(fpsa_dims3 grid, fpsa_dims3 tile, int32_t d, int32_t pitch, in
   if (d != 64 && d != 128) return fail(FPSA_EUNSUPPORTED, "head dim must be 64 or 128, got " + std::to_string(d));
   const int32_t tv = tile.t * tile.h * tile.w;
   if (pitch < tv) return fail(FPSA_EINVAL, "tile_pitch smaller than the tile volume");
+  if (in_order == FPSA_ORDER_NATURAL && tv > kMaxTableRows)
+    return fail(FPSA_EUNSUPPORTED, "tile volume above " + std::to_string(kMaxTableRows) + " tokens");
   if (in_order != FPSA_ORDER_TILE && in_order != FPSA_ORDER_NATURAL) return fail(FPSA_EINVAL, "bad token order");
   *g = Geometry{grid.t, grid.h, grid.w, tile.t, tile.h, tile.w, td.t, td.h, td.w,
                 tv,     td.t * td.h * td.w, pitch, in_order == FPSA_ORDER_NATURAL};
@@ -299,23 +676,21 @@ int cuda_status(const char* where) {
 }
 
 template <typename T, int D, int FMT>
-void launch_qk(const void* x, int64_t ts, int64_t hs, int32_t heads, const Geometry& g, uint8_t* codes,
-               double* scales, int32_t* err, cudaStream_t st) {
-  dim3 grid(g.M, heads);
-  quant_tile_kernel<T, D, FMT><<<grid, kQuantThreads, 0, st>>>(static_cast<const T*>(x), ts, hs, g, codes, scales, err);
+void launch_jobs(const Geometry& g, int32_t heads, const QuantArgs& a, int njobs, cudaStream_t st) {
+  dim3 grid(g.M, heads, njobs);
+  quant_kernel<T, D, FMT><<<grid, kQuantThreads, 0, st>>>(g, a);
 }
 
-template <typename T, int D, int FMT>
-void launch_v(const void* x, int64_t ts, int64_t hs, int32_t heads, const Geometry& g, uint8_t* codes,
-              double* scales, uint32_t* amax, int32_t* err, cudaStream_t st) {
+template <typename T, int D>
+void launch_amax(const void* x, int64_t ts, int64_t hs, int32_t heads, const Geometry& g, uint32_t* amax,
+                 int32_t* err, cudaStream_t st) {
   const int64_t L = (int64_t)g.gt * g.gh * g.gw;
-  const int32_t rows_per_block = 256;
+  const int32_t rows_per_block = 512;
   dim3 ga((unsigned)((L + rows_per_block - 1) / rows_per_block), heads);
   chan_amax_kernel<T, D><<<ga, kQuantThreads, 0, st>>>(static_cast<const T*>(x), ts, hs, L, rows_per_block, amax, err);
-  dim3 gb(g.M, heads);
-  quant_chan_kernel<T, D, FMT><<<gb, kQuantThreads, 0, st>>>(static_cast<const T*>(x), ts, hs, g, amax, codes, scales);
 }
 
+// dtype x d x fmt dispatch of a callable template F<T, D, FMT>::run(args...)
 template <template <typename, int, int> class F, typename... Args>
 void dispatch(int dtype, int32_t d, int fmt, Args&&... args) {
   if (dtype == FPSA_F32) {
@@ -332,16 +707,18 @@ void dispatch(int dtype, int32_t d, int fmt, Args&&... args) {
     }
   }
 }
-
 template <typename T, int D, int FMT>
-struct RunQK {
-  template <typename... A>
-  static void run(A... a) { launch_qk<T, D, FMT>(a...); }
+struct RunJobs {
+  static void run(const Geometry& g, int32_t heads, const QuantArgs& a, int njobs, cudaStream_t st) {
+    launch_jobs<T, D, FMT>(g, heads, a, njobs, st);
+  }
 };
 template <typename T, int D, int FMT>
-struct RunV {
-  template <typename... A>
-  static void run(A... a) { launch_v<T, D, FMT>(a...); }
+struct RunAmax {
+  static void run(const void* x, int64_t ts, int64_t hs, int32_t heads, const Geometry& g, uint32_t* amax,
+                  int32_t* err, cudaStream_t st) {
+    launch_amax<T, D>(x, ts, hs, heads, g, amax, err, st);
+  }
 };
 
 }  // namespace
@@ -356,8 +733,10 @@ extern "C" int fpsa_quantize_qk(const void* x, int dtype, int64_t token_stride, 
   if (int s = check_common(x, dtype, heads, fmt, codes, scales)) return s;
   Geometry g;
   if (int s = make_geometry(grid, tile, d, tile_pitch, in_order, &g)) return s;
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  dispatch<RunQK>(dtype, d, fmt, x, token_stride, head_stride, heads, g, codes, scales, err_flag, st);
+  QuantArgs a{};
+  a.job[0] = QuantJob{x, token_stride, head_stride, codes, scales, 0};
+  a.err = err_flag;
+  dispatch<RunJobs>(dtype, d, fmt, g, heads, a, 1, static_cast<cudaStream_t>(stream));
   return cuda_status("fpsa_quantize_qk");
 }
 
@@ -373,6 +752,51 @@ extern "C" int fpsa_quantize_v(const void* x, int dtype, int64_t token_stride, i
   uint32_t* amax = static_cast<uint32_t*>(workspace);
   if (cudaMemsetAsync(amax, 0, (size_t)heads * d * sizeof(uint32_t), st) != cudaSuccess)
     return cuda_status("fpsa_quantize_v memset");
-  dispatch<RunV>(dtype, d, fmt, x, token_stride, head_stride, heads, g, codes, scales, amax, err_flag, st);
+  dispatch<RunAmax>(dtype, d, fmt, x, token_stride, head_stride, heads, g, amax, err_flag, st);
+  QuantArgs a{};
+  a.job[0] = QuantJob{x, token_stride, head_stride, codes, scales, 1};
+  a.amax = amax;
+  a.err = err_flag;
+  dispatch<RunJobs>(dtype, d, fmt, g, heads, a, 1, st);
   return cuda_status("fpsa_quantize_v");
+}
+
+extern "C" int fpsa_quantize_qkv(const void* q, const void* k, const void* v, int dtype, int64_t token_stride,
+                                 int64_t head_stride, int32_t heads, fpsa_dims3 grid, fpsa_dims3 tile, int32_t d,
+                                 int32_t tile_pitch, int in_order, int fmt, uint8_t* q_codes, uint8_t* k_codes,
+                                 uint8_t* v_codes, double* q_scales, double* k_scales, double* v_scales,
+                                 void* workspace, int32_t* err_flag, void* stream) {
+  clear_error();
+  if (int s = check_common(q, dtype, heads, fmt, q_codes, q_scales)) return s;
+  if (int s = check_common(k, dtype, heads, fmt, k_codes, k_scales)) return s;
+  if (int s = check_common(v, dtype, heads, fmt, v_codes, v_scales)) return s;
+  if (!workspace) return fail(FPSA_EINVAL, "workspace is NULL");
+  Geometry g;
+  if (int s = make_geometry(grid, tile, d, tile_pitch, in_order, &g)) return s;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  uint32_t* amax = static_cast<uint32_t*>(workspace);
+  if (cudaMemsetAsync(amax, 0, (size_t)heads * d * sizeof(uint32_t), st) != cudaSuccess)
+    return cuda_status("fpsa_quantize_qkv memset");
+  dispatch<RunAmax>(dtype, d, fmt, v, token_stride, head_stride, heads, g, amax, err_flag, st);
+  {
+    TmaQuantArgs ta{};
+    ta.codes[0] = q_codes; ta.codes[1] = k_codes; ta.codes[2] = v_codes;
+    ta.scales[0] = q_scales; ta.scales[1] = k_scales; ta.scales[2] = v_scales;
+    ta.channel[2] = 1;
+    ta.njobs = 3;
+    ta.heads = heads;
+    ta.amax = amax;
+    ta.err = err_flag;
+    const void* xs[3] = {q, k, v};
+    if (try_tma_quant(xs, 3, dtype, token_stride, head_stride, heads, g, d, fmt, ta, st))
+      return cuda_status("fpsa_quantize_qkv");
+  }
+  QuantArgs a{};
+  a.job[0] = QuantJob{q, token_stride, head_stride, q_codes, q_scales, 0};
+  a.job[1] = QuantJob{k, token_stride, head_stride, k_codes, k_scales, 0};
+  a.job[2] = QuantJob{v, token_stride, head_stride, v_codes, v_scales, 1};
+  a.amax = amax;
+  a.err = err_flag;
+  dispatch<RunJobs>(dtype, d, fmt, g, heads, a, 3, st);
+  return cuda_status("fpsa_quantize_qkv");
 }

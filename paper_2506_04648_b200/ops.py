@@ -144,6 +144,14 @@ class FpsaPlan:
         order = _lib.ORDER_TILE if tile_order else _lib.ORDER_NATURAL
         g, t = _lib.dims3(self.grid), _lib.dims3(self.tile)
         f = self.fmt.abi_id
+        strides = [self._strides(x, layout) for x in (q, k, v)]
+        if strides[0] == strides[1] == strides[2] and q.dtype == k.dtype == v.dtype:
+            ts, hs = strides[0]
+            _lib.check(L.fpsa_quantize_qkv(
+                _ptr(q), _ptr(k), _ptr(v), _dtype_id(q), ts, hs, self.heads, g, t, self.d, self.pitch, order, f,
+                _ptr(self.q_codes), _ptr(self.k_codes), _ptr(self.v_codes), _ptr(self.q_scales),
+                _ptr(self.k_scales), _ptr(self.v_scales), _ptr(self.workspace), _ptr(self.err), st))
+            return
         for x, codes, scales in ((q, self.q_codes, self.q_scales), (k, self.k_codes, self.k_scales)):
             ts, hs = self._strides(x, layout)
             _lib.check(L.fpsa_quantize_qk(_ptr(x), _dtype_id(x), ts, hs, self.heads, g, t, self.d, self.pitch,

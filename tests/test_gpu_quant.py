@@ -129,3 +129,38 @@ def test_natural_order_multihead_bf16(fpsa, shape):
         vc, vs = O.quantize_v_channelwise(xt)
         assert np.array_equal(plan.v_scales.view(H, d)[h].cpu().numpy(), vs)
         assert np.array_equal(vcodes[h, :, :tv, :].reshape(L, d), vc)
+
+
+@pytest.mark.parametrize("tie_rich", [False, True])
+def test_bf16_exact_ties_natural_order(fpsa, tie_rich):
+    """bf16 data hits exact fp8 midpoints often (e.g. 448*0.796875/4.25 == 84); ties go to even.
+
+    tie_rich draws every value from k/64 with a 4.25 peak per tile, so most
+    quotients are exact midpoints -- exercises the queued exact path and its
+    overflow fallback in the TMA quantiser.
+    """
+    grid, tile, H, d = (6, 10, 32), (3, 5, 16), 2, 128
+    L = grid[0] * grid[1] * grid[2]
+    gen = torch.Generator(device="cuda").manual_seed(7)
+    if tie_rich:
+        k = torch.randint(-255, 256, (L, H, d), generator=gen, device="cuda").float() / 64.0
+        k[0::240, :, 0] = 4.25
+        x = k.to(torch.bfloat16)
+    else:
+        x = torch.randn((L, H, d), generator=gen, device="cuda").to(torch.bfloat16)
+    plan = fpsa.FpsaPlan(grid, tile, (3, 3, 3), H, d)
+    plan.quantize(x, x, x, "lhd")
+    torch.cuda.synchronize()
+    perm = O.tile_perm(grid, tile)
+    tv, M = plan.tv, plan.M
+    qc = plan.q_codes.view(H, M, plan.pitch, d).cpu().numpy()
+    vc = plan.v_codes.view(H, M, plan.pitch, d).cpu().numpy()
+    xs = x.float().cpu().numpy()
+    for h in range(H):
+        xt = xs[perm, h, :]
+        c, s = O.quantize_qk_tilewise(xt, tv)
+        assert np.array_equal(plan.q_scales.view(H, M)[h].cpu().numpy(), s)
+        assert np.array_equal(qc[h, :, :tv, :].reshape(L, d), c)
+        c, s = O.quantize_v_channelwise(xt)
+        assert np.array_equal(plan.v_scales.view(H, d)[h].cpu().numpy(), s)
+        assert np.array_equal(vc[h, :, :tv, :].reshape(L, d), c)
