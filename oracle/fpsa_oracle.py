@@ -332,7 +332,24 @@ def sparse_forward_f32(q, k, v, tv, offs, ids, softmax_scale=None):
                            _softmax_scale(q.shape[1], softmax_scale), quant_p=False)
 
 
-def onepass_forward(codes: dict, tv, offs, ids, fmt: Fmt = E4M3, softmax_scale=None, block=128, tau=0.0):
+def _poly_columns(block: int = 128) -> np.ndarray:
+    """Columns of a key block whose exp2 the GPU kernel evaluates with its polynomial:
+    odd groups of 4 inside each 64-column half (fpsa_attn.cu kPolyGroup)."""
+    c = np.arange(block)
+    return ((c % 64) // 4) % 2 == 1
+
+
+def _exp2_poly(x: np.ndarray) -> np.ndarray:
+    """The kernel's FMA-pipe exp2: x clamped to [-126, 130], j = rint(x), degree-2 minimax on x - j."""
+    x = np.clip(x, -126.0, 130.0)
+    j = np.rint(x)
+    f = x - j
+    y = (np.float32(0.238487109541893) * f + np.float32(0.703453540802002)) * f + np.float32(1.0004364252090454)
+    return np.ldexp(y, j.astype(np.int64))
+
+
+def onepass_forward(codes: dict, tv, offs, ids, fmt: Fmt = E4M3, softmax_scale=None, block=128, tau=0.0,
+                    poly=False):
     """Emulation of the GPU kernel's one-pass schedule (NOT the reference semantics).
 
     Keys are visited per key tile in 128-key blocks (tiles padded to a multiple
@@ -376,7 +393,11 @@ def onepass_forward(codes: dict, tv, offs, ids, fmt: Fmt = E4M3, softmax_scale=N
                 else:
                     m_new = np.maximum(m, mb)
                 alpha = np.where(np.isfinite(m), np.exp2(m - m_new), 0.0)
-                p = np.exp2(s - m_new[:, None] + (math.log2(448.0) - tau))
+                xe = s - m_new[:, None] + (math.log2(448.0) - tau)
+                p = np.exp2(xe)
+                if poly:
+                    pc = _poly_columns(block)[: s.shape[1]]
+                    p[:, pc] = _exp2_poly(xe[:, pc])
                 lsum = lsum * alpha + p.sum(axis=1)
                 pq = grid_round(p.astype(np.float32), E4M3).astype(np.float64)
                 acc = acc * alpha[:, None] + pq @ vb

@@ -43,12 +43,22 @@ namespace {
 
 using namespace sm100;
 
-constexpr int kThreads = 320;
+// 16 softmax warps: for each 128-row query block, warps w and w+4 share the
+// TMEM lane quarter w and split the 128 S columns in two halves (a "pair"),
+// plus a TMA warp and an MMA warp.
+constexpr int kSoftmaxWarps = 16;
+constexpr int kHalf = 64;  // S columns per softmax thread
+constexpr int kTmaWarp = kSoftmaxWarps;
+constexpr int kMmaWarp = kSoftmaxWarps + 1;
+constexpr int kThreads = (kSoftmaxWarps + 2) * 32;
+
 constexpr int kStages = 4;
 constexpr int kBlk = 128;  // rows per query block and keys per key block
 constexpr float kLog2_448 = 8.807354922057604f;
-// Columns [kPolyFrom, 128) of every key block take the FMA-pipe exp2; the rest MUFU ex2.
-constexpr int kPolyFrom = 96;
+// Groups of 4 columns whose exp2 runs on the FMA pipe (polynomial) instead of
+// MUFU ex2: every other group, so both pipes stay busy in the same instruction
+// window (MUFU ex2 alone would bound the kernel at 16 exp/clk/SM).
+__device__ __forceinline__ constexpr bool kPolyGroup(int g) { return (g & 1) == 1; }
 
 struct AttnParams {
   const double* q_scales;
@@ -123,21 +133,43 @@ __device__ __forceinline__ f2 add2(f2 a, f2 b) {
 }
 __device__ __forceinline__ f2 bcast(float v) { return f2{v, v}; }
 
-// 2^x for a pair on the FMA pipe (Cody-Waite split + degree-3 minimax, rel. err 7.5e-5),
-// used for a fraction of the columns so that the MUFU pipe is not the only exp source.
-__device__ __forceinline__ f2 exp2_poly(f2 x) {
-  constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23: x + kMagic rounds x to an integer
-  x.x = fmaxf(x.x, -126.0f);  // keeps the exponent add below in range; 2^-126 -> code 0
-  x.y = fmaxf(x.y, -126.0f);
-  const f2 t = add2(x, bcast(kMagic));
-  const f2 j = add2(t, bcast(-kMagic));
-  const f2 f = add2(x, f2{-j.x, -j.y});
-  f2 y = fma2(bcast(0.055180370807647705f), f, bcast(0.24261191487312317f));
-  y = fma2(y, f, bcast(0.6932594180107117f));
-  y = fma2(y, f, bcast(0.9999279975891113f));
-  // scale by 2^j: add j to the exponent field (t's low mantissa bits hold j)
+// Scalar saturating FMA (there is no .sat for f32x2): clamps to [0, 1].
+__device__ __forceinline__ f2 fma_sat_pair(f2 a, float b, float c) {
+  f2 d;
+  asm("fma.rn.sat.f32 %0, %1, %2, %3;" : "=f"(d.x) : "f"(a.x), "f"(b), "f"(c));
+  asm("fma.rn.sat.f32 %0, %1, %2, %3;" : "=f"(d.y) : "f"(a.y), "f"(b), "f"(c));
+  return d;
+}
+
+// 2^x on the FMA pipe for a pair, x = s * c + noff given as
+//   xs = sat(s * c/256 + (noff + 126)/256)  in [0, 1]   (x clamped to [-126, 130],
+//   so the exponent add below never leaves the float range)
+// Cody-Waite split x = j + f (j = round(x), |f| <= 1/2) with the rounding
+// done by the magic-number add, then a degree-2 minimax for 2^f (rel. err
+// 1.7e-3, far below the 2^-4 step of the e4m3 P it feeds) and j added to the
+// exponent field.  Used for a fraction of the columns so that MUFU ex2 is not
+// the only exp source.
+__device__ __forceinline__ f2 exp2_poly_sat(f2 xs) {
+  constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23
+  const f2 t = fma2(xs, bcast(256.0f), bcast(kMagic - 126.0f));  // kMagic + round(x), x = 256 xs - 126
+  const f2 g = add2(t, bcast(126.0f - kMagic));                   // round(x) + 126
+  const f2 f = fma2(xs, bcast(256.0f), f2{-g.x, -g.y});           // x - round(x)
+  f2 y = fma2(bcast(0.238487109541893f), f, bcast(0.703453540802002f));
+  y = fma2(y, f, bcast(1.0004364252090454f));
   return f2{__uint_as_float(__float_as_uint(y.x) + (__float_as_uint(t.x) << 23)),
             __uint_as_float(__float_as_uint(y.y) + (__float_as_uint(t.y) << 23))};
+}
+
+// Four e4m3 codes in one word (a.x lowest byte).
+__device__ __forceinline__ uint32_t e4m3x4(f2 a, f2 b) {
+  uint32_t r;
+  asm("{\n\t.reg .b16 lo, hi;\n\t"
+      "cvt.rn.satfinite.e4m3x2.f32 lo, %2, %1;\n\t"
+      "cvt.rn.satfinite.e4m3x2.f32 hi, %4, %3;\n\t"
+      "mov.b32 %0, {lo, hi};\n\t}"
+      : "=r"(r)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return r;
 }
 
 __device__ __forceinline__ uint32_t e4m3x2(float hi, float lo) {
@@ -145,6 +177,18 @@ __device__ __forceinline__ uint32_t e4m3x2(float hi, float lo) {
   asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(r) : "f"(hi), "f"(lo));
   return r;
 }
+
+#ifdef FPSA_TRACE
+// Debug builds only: cycle counters accumulated over all CTAs.
+//   [0] softmax: waiting for S   [1] softmax: total loop   [2] MMA: waiting for K/V
+//   [3] MMA: waiting for P       [4] MMA: total loop        [5] softmax: rescale count
+__device__ unsigned long long g_trace[8];
+#define TRACE_T0() const long long _t0 = clock64()
+#define TRACE_ADD(i, v) atomicAdd(&g_trace[i], (unsigned long long)(v))
+#else
+#define TRACE_T0()
+#define TRACE_ADD(i, v)
+#endif
 
 template <int D, int FMT, int OUT>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -158,6 +202,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   __shared__ uint64_t bar_s_full[2], bar_p_ready[2];
   __shared__ uint32_t s_tmem;
   __shared__ float s_vscale[D];
+  __shared__ float s_xchg[2][2][kBlk];       // [query block][half][row] pair exchange
+  __shared__ uint32_t s_flag[2][8][2];       // [j parity][pair][half] overflow verdicts
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int32_t h = p.items[3 * blockIdx.x + 0];
@@ -176,15 +222,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&bar_s_full[i], 1);
-      mbar_init(&bar_p_ready[i], 128);
+      mbar_init(&bar_p_ready[i], 256);
     }
     fence_barrier_init();
   }
-  if (warp == 8) {
+  if (warp == kTmaWarp) {
     tmem_alloc(&s_tmem, 512);
     tmem_relinquish();
   }
-  if (warp == 9) {
+  if (warp == kMmaWarp) {
     for (int i = lane; i < D; i += 32) s_vscale[i] = (float)p.v_scales[(int64_t)h * D + i];
   }
   tc_fence_before();
@@ -194,7 +240,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tm_s[2] = {tmem, tmem + 128};
   const uint32_t tm_o[2] = {tmem + 256, tmem + 256 + D};
 
-  if (warp == 8) {
+  if (warp == kTmaWarp) {
     // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
       prefetch_tmap(&tm_q);
@@ -214,7 +260,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tma_load_2d(smem + S::kV + st * S::kTile, &tm_v, 0, krow, &bar_kv_full[st]);
       }
     }
-  } else if (warp == 9) {
+  } else if (warp == kMmaWarp) {
     // ------------------------------------------------------------ MMA issuer
     if (lane == 0) {
       constexpr uint32_t idesc_qk = idesc_f8(128, 128, FMT, FMT, 0);
@@ -222,10 +268,20 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t sq = smem_u32(smem + S::kQ);
       mbar_wait(&bar_q, 0);
       tc_fence_after();
+#ifdef FPSA_TRACE
+      long long w_kv = 0, w_p = 0;
+      const long long t_loop = clock64();
+#endif
       for (int32_t j = 0; j <= n_kv; ++j) {
         const int st = j % kStages;
         if (j < n_kv) {
+#ifdef FPSA_TRACE
+          const long long ta = clock64();
+#endif
           mbar_wait(&bar_kv_full[st], (j / kStages) & 1);
+#ifdef FPSA_TRACE
+          w_kv += clock64() - ta;
+#endif
           tc_fence_after();
         }
         const int pst = (j + kStages - 1) % kStages;  // stage of block j-1
@@ -233,7 +289,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t sv_prev = smem_u32(smem + S::kV + pst * S::kTile);
         for (int q = 0; q < nqb; ++q) {
           if (j > 0) {
+#ifdef FPSA_TRACE
+            const long long tb = clock64();
+#endif
             mbar_wait(&bar_p_ready[q], (j - 1) & 1);
+#ifdef FPSA_TRACE
+            w_p += clock64() - tb;
+#endif
             tc_fence_after();
 #pragma unroll
             for (int k = 0; k < kBlk / 32; ++k)
@@ -251,97 +313,156 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (j > 0) mma_commit(&bar_kv_empty[pst]);
       }
       mma_commit(&bar_o);
+#ifdef FPSA_TRACE
+      TRACE_ADD(2, w_kv);
+      TRACE_ADD(3, w_p);
+      TRACE_ADD(4, clock64() - t_loop);
+#endif
     }
-  } else if (warp / 4 < nqb) {
-    // ------------------------------------------------------------ softmax (one row per thread)
-    const int q = warp / 4;
-    const int row = threadIdx.x & 127;
+  } else if (warp / 8 < nqb) {
+    // ------------------------------------------------------------ softmax: row x column half
+    const int q = warp / 8;               // query block
+    const int c = (warp / 4) & 1;         // column half of S and O owned by this thread
+    const int pair = warp & 7 & 3 | (q << 2);  // warps (w, w+4) of a query block share TMEM lanes
+    const int row = threadIdx.x & 127;    // TMEM lane = row of the query block
     const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+    const uint32_t s_half = tm_s[q] + lane_off + c * kHalf;
+    const uint32_t p_half = tm_s[q] + lane_off + c * (kHalf / 4);
+    const uint32_t o_half = tm_o[q] + lane_off + c * (D / 2);
     const float cq = (float)p.q_scales[h * p.M + u] * p.scale_log2;
     const float tau = p.tau;
-    float m_ref = -INFINITY, l = 0.0f;
+    auto pair_sync = [&]() { named_bar_sync(1 + pair, 64); };
+    // Rows keep a reference max m_ref; P~ = e4m3(448 * 2^(x - m_ref - tau)).
+    // No per-block max is taken: if both half-row sums of P~ stay <= 448 no
+    // element can have saturated and the block is accepted as computed.  The
+    // first block and blocks with a larger sum (a logit above m_ref + tau, or
+    // a false alarm) take the exact path, which lazily raises m_ref and
+    // rescales the TMEM accumulator; the two halves of a row decide together.
+    float m_ref = 0.0f, l = 0.0f;
+#ifdef FPSA_TRACE
+    long long w_s = 0, n_resc = 0;
+    const long long t_loop = clock64();
+#endif
     for (int32_t j = 0; j < n_kv; ++j) {
       const int32_t kt = j / p.nb, b = j - kt * p.nb;
       const int32_t v = __ldg(p.ids + kt0 + kt);
-      const float c = cq * (float)__ldg(p.k_scales + h * p.M + v);
-      const int valid = min(kBlk, p.tv - b * kBlk);
+      const float cj = cq * (float)__ldg(p.k_scales + h * p.M + v);
+      const int valid = min(kBlk, p.tv - b * kBlk) - c * kHalf;  // valid columns of this half (may be <= 0)
+#ifdef FPSA_TRACE
+      const long long ts0 = clock64();
+#endif
       mbar_wait(&bar_s_full[q], j & 1);
+#ifdef FPSA_TRACE
+      w_s += clock64() - ts0;
+#endif
       tc_fence_after();
-      float s[kBlk];
-      tmem_ld32(tm_s[q] + lane_off + 0, reinterpret_cast<uint32_t*>(s + 0));
-      tmem_ld32(tm_s[q] + lane_off + 32, reinterpret_cast<uint32_t*>(s + 32));
-      tmem_ld32(tm_s[q] + lane_off + 64, reinterpret_cast<uint32_t*>(s + 64));
-      tmem_ld32(tm_s[q] + lane_off + 96, reinterpret_cast<uint32_t*>(s + 96));
-      tmem_wait_ld();
-      // Key columns >= valid are padding (zero K/V rows of a key tile's last
-      // block): set to -inf so they drop out of the max, the sum and P
-      // (valid is a multiple of 8, checked on the host).
-      if (valid < kBlk) {
+      float sv[kHalf];
+      // S stays intact in TMEM until P is written over it: the exact path reloads it.
+      auto load_s = [&]() {
+        tmem_ld32(s_half + 0, reinterpret_cast<uint32_t*>(sv + 0));
+        tmem_ld32(s_half + 32, reinterpret_cast<uint32_t*>(sv + 32));
+        tmem_wait_ld();
+        // key columns >= valid are padding (zero K/V rows of a key tile's last
+        // block): -inf drops them from max, sum and P (valid % 8 == 0, host-checked)
+        if (valid < kHalf) {
 #pragma unroll
-        for (int i = 0; i < kBlk; i += 8) {
-          const bool ok = i < valid;
+          for (int i = 0; i < kHalf; i += 8) {
+            const bool ok = i < valid;
 #pragma unroll
-          for (int k = i; k < i + 8; ++k) s[k] = ok ? s[k] : -INFINITY;
+            for (int k2 = i; k2 < i + 8; ++k2) sv[k2] = ok ? sv[k2] : -INFINITY;
+          }
         }
-      }
-      float mx0 = -INFINITY, mx1 = -INFINITY;
+      };
+      // exact row max over both halves (pair exchange through shared memory)
+      auto row_max = [&]() {
+        float mx0 = -INFINITY, mx1 = -INFINITY;
 #pragma unroll
-      for (int i = 0; i < kBlk; i += 4) {
-        mx0 = max3(mx0, s[i], s[i + 1]);
-        mx1 = max3(mx1, s[i + 2], s[i + 3]);
-      }
-      const float mb = fmaxf(mx0, mx1) * c;
-      if (j == 0) {
-        m_ref = mb;
-      } else if (__any_sync(0xffffffffu, mb > m_ref + tau)) {
-        const float m_new = fmaxf(m_ref, mb);
-        const float alpha = ex2(m_ref - m_new);
-        l *= alpha;
-        m_ref = m_new;
-#pragma unroll 1
-        for (int cc = 0; cc < D; cc += 16) {
-          uint32_t o[16];
-          tmem_ld16(tm_o[q] + lane_off + cc, o);
-          tmem_wait_ld();
-#pragma unroll
-          for (int i = 0; i < 16; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
-          tmem_st16(tm_o[q] + lane_off + cc, o);
+        for (int i = 0; i < kHalf; i += 4) {
+          mx0 = max3(mx0, sv[i], sv[i + 1]);
+          mx1 = max3(mx1, sv[i + 2], sv[i + 3]);
         }
-        tmem_wait_st();
-      }
-      const f2 cc2 = bcast(c), noff = bcast(kLog2_448 - m_ref - tau);
-      f2 lsum0 = bcast(0.0f), lsum1 = bcast(0.0f);
+        s_xchg[q][c][row] = fmaxf(mx0, mx1);
+        pair_sync();
+        const float m = fmaxf(s_xchg[q][0][row], s_xchg[q][1][row]) * cj;
+        pair_sync();  // the exchange slots are reused
+        return m;
+      };
+      uint32_t w[kHalf / 4];
+      auto exp_half = [&](float mref) {
+        const f2 cc2 = bcast(cj), noff = bcast(kLog2_448 - mref - tau);
+        const float cs = cj * (1.0f / 256.0f), ns = (kLog2_448 - mref - tau + 126.0f) * (1.0f / 256.0f);
+        f2 lsum0 = bcast(0.0f), lsum1 = bcast(0.0f);
 #pragma unroll
-      for (int i0 = 0; i0 < kBlk; i0 += 32) {
-        uint32_t w[8];
-#pragma unroll
-        for (int k = i0; k < i0 + 32; k += 4) {
-          f2 pa = fma2(f2{s[k], s[k + 1]}, cc2, noff);
-          f2 pb = fma2(f2{s[k + 2], s[k + 3]}, cc2, noff);
-          if (k >= kPolyFrom) {
-            pa = exp2_poly(pa);
-            pb = exp2_poly(pb);
+        for (int k2 = 0; k2 < kHalf; k2 += 4) {
+          f2 pa, pb;
+          if (kPolyGroup(k2 / 4)) {
+            pa = exp2_poly_sat(fma_sat_pair(f2{sv[k2], sv[k2 + 1]}, cs, ns));
+            pb = exp2_poly_sat(fma_sat_pair(f2{sv[k2 + 2], sv[k2 + 3]}, cs, ns));
           } else {
+            pa = fma2(f2{sv[k2], sv[k2 + 1]}, cc2, noff);
+            pb = fma2(f2{sv[k2 + 2], sv[k2 + 3]}, cc2, noff);
             pa = f2{ex2(pa.x), ex2(pa.y)};
             pb = f2{ex2(pb.x), ex2(pb.y)};
           }
           lsum0 = add2(lsum0, pa);
           lsum1 = add2(lsum1, pb);
-          w[(k - i0) / 4] = e4m3x2(pa.y, pa.x) | (e4m3x2(pb.y, pb.x) << 16);
+          w[k2 / 4] = e4m3x4(pa, pb);
         }
-        tmem_st8(tm_s[q] + lane_off + i0 / 4, w);
+        const f2 ls = add2(lsum0, lsum1);
+        return ls.x + ls.y;
+      };
+      load_s();
+      if (j == 0) m_ref = row_max();
+      float lb = exp_half(m_ref);
+      // half-row sums <= 448 bound every element; the pair agrees on the verdict
+      const uint32_t over = __any_sync(0xffffffffu, lb > 448.0f) ? 1u : 0u;
+      if (lane == 0) s_flag[j & 1][pair][c] = over;
+      pair_sync();
+      if (s_flag[j & 1][pair][0] | s_flag[j & 1][pair][1]) {
+        load_s();
+        const float mb = row_max();
+        if (__any_sync(0xffffffffu, mb > m_ref + tau)) {  // identical in both warps of the pair
+          const float m_new = fmaxf(m_ref, mb);
+          const float alpha = ex2(m_ref - m_new);
+          l *= alpha;
+          m_ref = m_new;
+#ifdef FPSA_TRACE
+          ++n_resc;
+#endif
+#pragma unroll 1
+          for (int cc = 0; cc < D / 2; cc += 16) {
+            uint32_t o[16];
+            tmem_ld16(o_half + cc, o);
+            tmem_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 16; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+            tmem_st16(o_half + cc, o);
+          }
+          tmem_wait_st();
+          lb = exp_half(m_ref);
+        }
       }
-      const f2 lsum = add2(lsum0, lsum1);
-      l += lsum.x + lsum.y;
+      l += lb;
+      tmem_st16(p_half, w);
       tmem_wait_st();
       tc_fence_before();
       mbar_arrive(&bar_p_ready[q]);
     }
+#ifdef FPSA_TRACE
+    if (lane == 0) {
+      TRACE_ADD(0, w_s);
+      TRACE_ADD(1, clock64() - t_loop);
+      TRACE_ADD(5, n_resc);
+      TRACE_ADD(6, n_kv);
+    }
+#endif
     // ------------------------------------------------------------ epilogue
+    s_xchg[q][c][row] = l;
     mbar_wait(&bar_o, 0);
     tc_fence_after();
+    pair_sync();
+    const float inv_l = 1.0f / (s_xchg[q][0][row] + s_xchg[q][1][row]);
     const int32_t r = (qb0 + q) * kBlk + row;  // row inside the tile
-    const float inv_l = 1.0f / l;
     int64_t token;
     if (p.natural) {
       const int32_t ut = u / (p.dh * p.dw), uh = (u / p.dw) % p.dh, uw = u % p.dw;
@@ -350,29 +471,29 @@ __global__ void __launch_bounds__(kThreads, 1)
     } else {
       token = (int64_t)u * p.tv + r;
     }
-    const float* vs = s_vscale;
 #pragma unroll
-    for (int cc = 0; cc < D; cc += 32) {
+    for (int cc = 0; cc < D / 2; cc += 32) {
+      const int col = c * (D / 2) + cc;
       uint32_t o[32];
-      tmem_ld32(tm_o[q] + lane_off + cc, o);
+      tmem_ld32(o_half + cc, o);
       tmem_wait_ld();
       if (r < p.tv) {
         float f[32];
 #pragma unroll
-        for (int i = 0; i < 32; ++i) f[i] = __uint_as_float(o[i]) * inv_l * vs[cc + i];
+        for (int i = 0; i < 32; ++i) f[i] = __uint_as_float(o[i]) * inv_l * s_vscale[col + i];
         if constexpr (OUT == FPSA_F32) {
-          float4* dst = reinterpret_cast<float4*>(static_cast<float*>(p.out) + token * p.out_ts + h * p.out_hs + cc);
+          float4* dst = reinterpret_cast<float4*>(static_cast<float*>(p.out) + token * p.out_ts + h * p.out_hs + col);
 #pragma unroll
           for (int i = 0; i < 8; ++i) dst[i] = make_float4(f[4 * i], f[4 * i + 1], f[4 * i + 2], f[4 * i + 3]);
         } else {
-          uint4* dst = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.out) + token * p.out_ts + h * p.out_hs + cc);
+          uint4* dst = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.out) + token * p.out_ts + h * p.out_hs + col);
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
             uint32_t wv[4];
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              __nv_bfloat162 b2 = __floats2bfloat162_rn(f[8 * i + 2 * k], f[8 * i + 2 * k + 1]);
-              wv[k] = *reinterpret_cast<uint32_t*>(&b2);
+            for (int k2 = 0; k2 < 4; ++k2) {
+              __nv_bfloat162 b2 = __floats2bfloat162_rn(f[8 * i + 2 * k2], f[8 * i + 2 * k2 + 1]);
+              wv[k2] = *reinterpret_cast<uint32_t*>(&b2);
             }
             dst[i] = make_uint4(wv[0], wv[1], wv[2], wv[3]);
           }
@@ -382,7 +503,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 8) tmem_dealloc(tmem, 512);
+  if (warp == kTmaWarp) tmem_dealloc(tmem, 512);
 }
 
 // ---------------------------------------------------------------- host side
@@ -502,3 +623,14 @@ extern "C" int fpsa_attn_fwd(const uint8_t* q_codes, const uint8_t* k_codes, con
   }
 #undef FPSA_LAUNCH
 }
+
+#ifdef FPSA_TRACE
+extern "C" int fpsa_trace_read(unsigned long long* out, int reset) {
+  cudaMemcpyFromSymbol(out, fpsa::g_trace, sizeof(unsigned long long) * 8);
+  if (reset) {
+    unsigned long long z[8] = {0};
+    cudaMemcpyToSymbol(fpsa::g_trace, z, sizeof z);
+  }
+  return 0;
+}
+#endif

@@ -65,7 +65,7 @@ def test_attention_vs_onepass_emulation(fpsa, attn_golden, name):
     offs, ids = O.window_lists(O.tile_grid_dims(c["grid"], c["tile"]), c["window"])
     fmt = O.FORMATS[c["fmt"]]
     _, codes = O.fp8_sparse_forward(q, k, v, tv, offs, ids, fmt)
-    emu = O.onepass_forward(codes, tv, offs, ids, fmt, tau=8.0)
+    emu = O.onepass_forward(codes, tv, offs, ids, fmt, tau=8.0, poly=True)
     cos = O.cosine(out, emu)
     print(f"{name}: cos(emu)={cos:.7f} max-abs={O.max_abs(out, emu):.3e}")
     assert cos >= COS_EMU, cos
