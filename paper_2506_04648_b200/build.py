@@ -30,6 +30,13 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(os.path.join(HERE, s)) <= t for s in SOURCES + HEADERS)
 
 
+def build_trace() -> str:
+    """Instrumented variant (-DFPSA_TRACE, cycle counters; tools/trace_attn.py), never loaded by the package."""
+    target = os.path.join(HERE, "libfpsa_trace.so")
+    subprocess.run([nvcc(), *NVCC_FLAGS, "-DFPSA_TRACE", *SOURCES, "-o", target], cwd=HERE, check=True)
+    return target
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and up_to_date():
         return TARGET
@@ -42,5 +49,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
 
 if __name__ == "__main__":
+    if "--trace" in sys.argv:
+        print(build_trace())
+        sys.exit(0)
     build(force="--force" in sys.argv, verbose="-v" in sys.argv)
     print(TARGET)

@@ -3,28 +3,32 @@
 // Replaces fp8sta.attention.fp8_sparse_forward / _engine
 // (/root/reference/pkg/src/fp8sta/attention.py:91-149, :179-208).
 //
-// One CTA = (head h, query tile u, up to two 128-row query blocks of u).
-// The key sequence of u is the concatenation of its admissible key tiles in
+// One CTA = (head h, query tile u, one 128-row query block of u).  The key
+// sequence of u is the concatenation of its admissible key tiles in
 // ascending id order (sparsity.py:63-67, the reference's reduction order),
-// each key tile cut into 128-key blocks (tiles are stored padded to a
-// multiple of 128 rows, pad rows zero and masked).  Per key block j:
+// each key tile cut into 128-key blocks; a tile's last block has
+// n_tail = tv - 128 (nb - 1) keys (rounded up to 16), so no padding key of a
+// 240-token tile is multiplied or exponentiated.  Per key block j:
 //
-//   S_q(j)  = Q_q K_j^T              tcgen05.mma kind::f8f6f4, A/B from smem,
-//                                    fp32 accumulator in TMEM (128 lanes x 128 cols)
-//   x       = S * (sq[u] * sk[v] * softmax_scale * log2 e)     per-tile factors
-//   m       = running row max, rescaled lazily (only when a block max exceeds
-//             the reference max by more than tau)
-//   P~      = e4m3(448 * 2^-tau * 2^(x - m))  re-quantised per tile, written
-//             back to TMEM (4 codes per column, aliasing S_q)
-//   O_q    += P~ V_j                  tcgen05.mma, A = P~ from TMEM, B = V from
+//   S(j)  = Q K_j^T                  tcgen05.mma kind::f8f6f4, A/B from smem,
+//                                    fp32 accumulator in TMEM buffer j % 2
+//   x     = S * (sq[u] * sk[v] * softmax_scale * log2 e)     per-tile factors
+//   m     = reference row max, raised lazily (only when a block overflows the
+//           e4m3 range above it)
+//   P~    = e4m3(448 * 2^-tau * 2^(x - m))   re-quantised per key block,
+//           written back to TMEM over S(j) (4 codes per column)
+//   O    += P~ V_j                    tcgen05.mma, A = P~ from TMEM, B = V from
 //                                    smem (MN-major, V stored [keys][d])
-//   l      += sum of the unrounded P~ (fp32)
+//   l    += sum of the unrounded P~ (fp32)
 // and finally out = O * v_scale[c] / l.
 //
-// Warp roles (320 threads): warps 0-3 softmax for query block 0, warps 4-7
-// for query block 1 (one thread per row = TMEM lane), warp 8 TMA producer
-// (and TMEM allocator), warp 9 MMA issuer.  The two query blocks ping-pong so
-// that the tensor core works on one block while the other is in softmax.
+// S is double-buffered in TMEM (O: 128 columns, S(even), S(odd): 128 each),
+// so QK(j+1) runs while the softmax works on S(j) and the MMA issue order
+// PV(j), QK(j+2) never makes the softmax wait on its own P.
+//
+// Warp roles (320 threads): warps w and w+4 (w < 4) own TMEM lane quarter w
+// (rows 32w..32w+31) and split the 128 S columns in halves; warp 8 is the
+// TMA producer (and TMEM allocator), warp 9 the MMA issuer.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -43,22 +47,17 @@ namespace {
 
 using namespace sm100;
 
-// 16 softmax warps: for each 128-row query block, warps w and w+4 share the
-// TMEM lane quarter w and split the 128 S columns in two halves (a "pair"),
-// plus a TMA warp and an MMA warp.
-constexpr int kSoftmaxWarps = 16;
-constexpr int kHalf = 64;  // S columns per softmax thread
+constexpr int kSoftmaxWarps = 8;
 constexpr int kTmaWarp = kSoftmaxWarps;
 constexpr int kMmaWarp = kSoftmaxWarps + 1;
 constexpr int kThreads = (kSoftmaxWarps + 2) * 32;
 
 constexpr int kStages = 4;
-constexpr int kBlk = 128;  // rows per query block and keys per key block
+constexpr int kBlk = 128;      // rows per query block and keys per key block
+constexpr int kHalfCols = 64;  // S columns per softmax thread
+constexpr int kFacCap = 2048;  // key-tile scale factors cached in shared memory per CTA
 constexpr float kLog2_448 = 8.807354922057604f;
-// Groups of 4 columns whose exp2 runs on the FMA pipe (polynomial) instead of
-// MUFU ex2: every other group, so both pipes stay busy in the same instruction
-// window (MUFU ex2 alone would bound the kernel at 16 exp/clk/SM).
-__device__ __forceinline__ constexpr bool kPolyGroup(int g) { return (g & 1) == 1; }
+constexpr uint32_t kNegInf = 0xFF800000u;
 
 struct AttnParams {
   const double* q_scales;
@@ -68,7 +67,9 @@ struct AttnParams {
   const int32_t* ids;
   const int32_t* items;
   int32_t M, tv, pitch, nb;
-  float scale_log2;  // softmax_scale * log2(e)
+  int32_t n_tail;     // S columns of the last key block of a tile (tv - 128 (nb-1), rounded up to 16)
+  int32_t tail_pad8;  // 1 if the last 8 of those columns are zero padding (tv % 16 == 8)
+  float softmax_log2;  // f32(softmax_scale * log2 e)
   float tau;
   void* out;
   int64_t out_ts, out_hs;
@@ -80,7 +81,7 @@ template <int D>
 struct Smem {
   static constexpr int kTile = kBlk * D;  // bytes of one 128-row fp8 tile
   static constexpr int kQ = 0;
-  static constexpr int kK = 2 * kTile;
+  static constexpr int kK = kTile;
   static constexpr int kV = kK + kStages * kTile;
   static constexpr int kBytes = kV + kStages * kTile;
   static constexpr uint32_t kSBO = 8 * D;  // 8 rows of D bytes
@@ -134,10 +135,9 @@ __device__ __forceinline__ f2 add2(f2 a, f2 b) {
 __device__ __forceinline__ f2 bcast(float v) { return f2{v, v}; }
 
 // Scalar saturating FMA (there is no .sat for f32x2): clamps to [0, 1].
-__device__ __forceinline__ f2 fma_sat_pair(f2 a, float b, float c) {
-  f2 d;
-  asm("fma.rn.sat.f32 %0, %1, %2, %3;" : "=f"(d.x) : "f"(a.x), "f"(b), "f"(c));
-  asm("fma.rn.sat.f32 %0, %1, %2, %3;" : "=f"(d.y) : "f"(a.y), "f"(b), "f"(c));
+__device__ __forceinline__ float fma_sat(float a, float b, float c) {
+  float d;
+  asm("fma.rn.sat.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
   return d;
 }
 
@@ -147,8 +147,8 @@ __device__ __forceinline__ f2 fma_sat_pair(f2 a, float b, float c) {
 // Cody-Waite split x = j + f (j = round(x), |f| <= 1/2) with the rounding
 // done by the magic-number add, then a degree-2 minimax for 2^f (rel. err
 // 1.7e-3, far below the 2^-4 step of the e4m3 P it feeds) and j added to the
-// exponent field.  Used for a fraction of the columns so that MUFU ex2 is not
-// the only exp source.
+// exponent field.  Used for half of the columns so that MUFU ex2 (16/clk/SM)
+// is not the only exp source.
 __device__ __forceinline__ f2 exp2_poly_sat(f2 xs) {
   constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23
   const f2 t = fma2(xs, bcast(256.0f), bcast(kMagic - 126.0f));  // kMagic + round(x), x = 256 xs - 126
@@ -172,22 +172,104 @@ __device__ __forceinline__ uint32_t e4m3x4(f2 a, f2 b) {
   return r;
 }
 
-__device__ __forceinline__ uint32_t e4m3x2(float hi, float lo) {
-  uint16_t r;
-  asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(r) : "f"(hi), "f"(lo));
-  return r;
+// P~ for 16 S columns [16U, 16U + 16) of a thread's half row, read from the
+// 32-column chunk `s` that holds columns [32 (U/2), 32 (U/2) + 32): 4 groups
+// of 4 keys, the odd groups (columns with bit 2 set) on the FMA-pipe
+// polynomial, the even groups on MUFU ex2.  Writes 4 packed P words
+// w[4U..4U+3] and accumulates the unrounded weights into acc.
+template <int U>
+__device__ __forceinline__ void softmax_unit(const uint32_t* s, f2 cc, f2 bb, float cs, float bs, f2* acc,
+                                             uint32_t* w) {
+#pragma unroll
+  for (int g = 0; g < 4; ++g) {
+    const int c0 = 16 * (U & 1) + 4 * g;
+    const f2 a{__uint_as_float(s[c0]), __uint_as_float(s[c0 + 1])};
+    const f2 b{__uint_as_float(s[c0 + 2]), __uint_as_float(s[c0 + 3])};
+    f2 pa, pb;
+    if (g & 1) {
+      pa = exp2_poly_sat(f2{fma_sat(a.x, cs, bs), fma_sat(a.y, cs, bs)});
+      pb = exp2_poly_sat(f2{fma_sat(b.x, cs, bs), fma_sat(b.y, cs, bs)});
+    } else {
+      pa = fma2(a, cc, bb);
+      pb = fma2(b, cc, bb);
+      pa = f2{ex2(pa.x), ex2(pa.y)};
+      pb = f2{ex2(pb.x), ex2(pb.y)};
+    }
+    acc[g & 1] = add2(acc[g & 1], pa);
+    acc[2 + (g & 1)] = add2(acc[2 + (g & 1)], pb);
+    w[4 * U + g] = e4m3x4(pa, pb);
+  }
+}
+
+// The last 8 of the ncol valid columns are zero K rows (tv % 16 == 8): -inf
+// drops them from max, sum and P.  `s` holds columns [base, base + 32).
+__device__ __forceinline__ void mask_pad8(uint32_t* s, int base, int ncol) {
+#pragma unroll
+  for (int i = 8; i < 32; i += 16)
+    if (base + i + 8 == ncol) {
+#pragma unroll
+      for (int k = i; k < i + 8; ++k) s[k] = kNegInf;
+    }
+}
+
+template <int C>
+__device__ __forceinline__ void softmax_chunk(uint32_t* s, int ncol, bool pad8, f2 cc, f2 bb, float cs, float bs,
+                                              f2* acc, uint32_t* w) {
+  if (pad8) mask_pad8(s, 32 * C, ncol);
+  if (ncol > 32 * C) softmax_unit<2 * C>(s, cc, bb, cs, bs, acc, w);
+  else w[8 * C] = w[8 * C + 1] = w[8 * C + 2] = w[8 * C + 3] = 0u;
+  if (ncol > 32 * C + 16) softmax_unit<2 * C + 1>(s, cc, bb, cs, bs, acc, w);
+  else w[8 * C + 4] = w[8 * C + 5] = w[8 * C + 6] = w[8 * C + 7] = 0u;
+}
+
+// One half row of one key block: 64 S columns streamed from TMEM in two
+// 32-column chunks (the second tcgen05.ld is in flight while the first chunk
+// is processed), ncol (multiple of 16, 0..64) valid.  P words of absent
+// columns are zero.  Returns the half-row sum of the unrounded weights.
+__device__ __forceinline__ float softmax_half(uint32_t s_addr, int ncol, bool pad8, float c, float boff, uint32_t* w) {
+  const f2 cc = bcast(c), bb = bcast(boff);
+  const float cs = c * (1.0f / 256.0f), bs = (boff + 126.0f) * (1.0f / 256.0f);
+  f2 acc[4] = {bcast(0.f), bcast(0.f), bcast(0.f), bcast(0.f)};
+  uint32_t sa[32], sb[32];
+  if (ncol > 0) {
+    tmem_ld32(s_addr, sa);
+    tmem_wait_ld();
+  }
+  if (ncol > 32) tmem_ld32(s_addr + 32, sb);
+  softmax_chunk<0>(sa, ncol, pad8, cc, bb, cs, bs, acc, w);
+  if (ncol > 32) tmem_wait_ld();
+  softmax_chunk<1>(sb, ncol, pad8, cc, bb, cs, bs, acc, w);
+  const f2 t = add2(add2(acc[0], acc[1]), add2(acc[2], acc[3]));
+  return t.x + t.y;
+}
+
+// Max of the first ncol (0..64) raw S values of a half row.
+__device__ __forceinline__ float half_max(uint32_t s_addr, int ncol, bool pad8) {
+  float m0 = -INFINITY, m1 = -INFINITY;
+#pragma unroll
+  for (int base = 0; base < kHalfCols; base += 32) {
+    if (base < ncol) {
+      uint32_t s[32];
+      tmem_ld32(s_addr + base, s);
+      tmem_wait_ld();
+      if (pad8) mask_pad8(s, base, ncol);
+#pragma unroll
+      for (int i = 0; i < 32; i += 4) {
+        if (base + i < ncol) {
+          m0 = max3(m0, __uint_as_float(s[i]), __uint_as_float(s[i + 1]));
+          m1 = max3(m1, __uint_as_float(s[i + 2]), __uint_as_float(s[i + 3]));
+        }
+      }
+    }
+  }
+  return fmaxf(m0, m1);
 }
 
 #ifdef FPSA_TRACE
-// Debug builds only: cycle counters accumulated over all CTAs.
-//   [0] softmax: waiting for S   [1] softmax: total loop   [2] MMA: waiting for K/V
-//   [3] MMA: waiting for P       [4] MMA: total loop        [5] softmax: rescale count
+// Debug builds only: counters accumulated over all CTAs.
+//   [0] softmax: cycles waiting for S   [1] softmax: loop cycles   [2] softmax: first-pass compute
+//   [3] MMA: cycles waiting for P~      [5] rescales   [6] steps   [7] MMA: cycles waiting for K/V
 __device__ unsigned long long g_trace[8];
-#define TRACE_T0() const long long _t0 = clock64()
-#define TRACE_ADD(i, v) atomicAdd(&g_trace[i], (unsigned long long)(v))
-#else
-#define TRACE_T0()
-#define TRACE_ADD(i, v)
 #endif
 
 template <int D, int FMT, int OUT>
@@ -197,33 +279,35 @@ __global__ void __launch_bounds__(kThreads, 1)
   using S = Smem<D>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  __shared__ uint64_t bar_q, bar_o;
+  __shared__ uint64_t bar_q, bar_o, bar_pv;
   __shared__ uint64_t bar_kv_full[kStages], bar_kv_empty[kStages];
-  __shared__ uint64_t bar_s_full[2], bar_p_ready[2];
+  __shared__ uint64_t bar_s_full[2], bar_p_ready[2];  // by step parity: warps may run one step apart
   __shared__ uint32_t s_tmem;
   __shared__ float s_vscale[D];
-  __shared__ float s_xchg[2][2][kBlk];       // [query block][half][row] pair exchange
-  __shared__ uint32_t s_flag[2][8][2];       // [j parity][pair][half] overflow verdicts
+  __shared__ float s_kfac[kFacCap];
+  __shared__ float s_xchg[2][kBlk];     // [half][row] pair exchange
+  __shared__ uint32_t s_flag[2][4][2];  // [step parity][lane quarter][half] overflow verdicts
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int32_t h = p.items[3 * blockIdx.x + 0];
   const int32_t u = p.items[3 * blockIdx.x + 1];
-  const int32_t qb0 = p.items[3 * blockIdx.x + 2];
-  const int nqb = min(2, p.nb - qb0);
+  const int32_t qb = p.items[3 * blockIdx.x + 2];
   const int32_t kt0 = p.offs[u];
-  const int32_t n_kv = (p.offs[u + 1] - kt0) * p.nb;
+  const int32_t n_kt = p.offs[u + 1] - kt0;
+  const int32_t n_kv = n_kt * p.nb;
 
   if (threadIdx.x == 0) {
     mbar_init(&bar_q, 1);
     mbar_init(&bar_o, 1);
+    mbar_init(&bar_pv, 1);
     for (int i = 0; i < kStages; ++i) {
       mbar_init(&bar_kv_full[i], 1);
       mbar_init(&bar_kv_empty[i], 1);
     }
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&bar_s_full[i], 1);
-      mbar_init(&bar_p_ready[i], 256);
-    }
+    mbar_init(&bar_s_full[0], 1);
+    mbar_init(&bar_s_full[1], 1);
+    mbar_init(&bar_p_ready[0], kSoftmaxWarps);  // one arrival per softmax warp
+    mbar_init(&bar_p_ready[1], kSoftmaxWarps);
     fence_barrier_init();
   }
   if (warp == kTmaWarp) {
@@ -231,14 +315,18 @@ __global__ void __launch_bounds__(kThreads, 1)
     tmem_relinquish();
   }
   if (warp == kMmaWarp) {
+    // per-CTA tables: V channel factors and the k-scale of every in-window key tile
     for (int i = lane; i < D; i += 32) s_vscale[i] = (float)p.v_scales[(int64_t)h * D + i];
+    for (int i = lane; i < min(n_kt, kFacCap); i += 32)
+      s_kfac[i] = (float)p.k_scales[(int64_t)h * p.M + p.ids[kt0 + i]];
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = s_tmem;
-  const uint32_t tm_s[2] = {tmem, tmem + 128};
-  const uint32_t tm_o[2] = {tmem + 256, tmem + 256 + D};
+  const uint32_t tm_o = tmem;
+  // S buffers at columns 128 and 256 (computed, not indexed: a local array would go to memory)
+  auto tm_s = [tmem](int32_t j) { return tmem + 128u + 128u * (uint32_t)(j & 1); };
 
   if (warp == kTmaWarp) {
     // ------------------------------------------------------------ TMA producer
@@ -246,223 +334,190 @@ __global__ void __launch_bounds__(kThreads, 1)
       prefetch_tmap(&tm_q);
       prefetch_tmap(&tm_k);
       prefetch_tmap(&tm_v);
-      const int32_t qrow = (h * p.M + u) * p.pitch + qb0 * kBlk;
-      mbar_arrive_expect_tx(&bar_q, nqb * S::kTile);
-      for (int q = 0; q < nqb; ++q) tma_load_2d(smem + S::kQ + q * S::kTile, &tm_q, 0, qrow + q * kBlk, &bar_q);
+      mbar_arrive_expect_tx(&bar_q, S::kTile);
+      tma_load_2d(smem + S::kQ, &tm_q, 0, (h * p.M + u) * p.pitch + qb * kBlk, &bar_q);
+      int32_t kt = 0, b = 0;
+      int32_t krow = (h * p.M + p.ids[kt0]) * p.pitch;
       for (int32_t j = 0; j < n_kv; ++j) {
         const int st = j % kStages;
         if (j >= kStages) mbar_wait(&bar_kv_empty[st], ((j / kStages) - 1) & 1);
-        const int32_t kt = j / p.nb, b = j - kt * p.nb;
-        const int32_t v = p.ids[kt0 + kt];
-        const int32_t krow = (h * p.M + v) * p.pitch + b * kBlk;
         mbar_arrive_expect_tx(&bar_kv_full[st], 2 * S::kTile);
-        tma_load_2d(smem + S::kK + st * S::kTile, &tm_k, 0, krow, &bar_kv_full[st]);
-        tma_load_2d(smem + S::kV + st * S::kTile, &tm_v, 0, krow, &bar_kv_full[st]);
+        tma_load_2d(smem + S::kK + st * S::kTile, &tm_k, 0, krow + b * kBlk, &bar_kv_full[st]);
+        tma_load_2d(smem + S::kV + st * S::kTile, &tm_v, 0, krow + b * kBlk, &bar_kv_full[st]);
+        if (++b == p.nb) {
+          b = 0;
+          if (++kt < n_kt) krow = (h * p.M + __ldg(p.ids + kt0 + kt)) * p.pitch;
+        }
       }
     }
   } else if (warp == kMmaWarp) {
     // ------------------------------------------------------------ MMA issuer
     if (lane == 0) {
       constexpr uint32_t idesc_qk = idesc_f8(128, 128, FMT, FMT, 0);
+      const uint32_t idesc_qk_tail = idesc_f8(128, (uint32_t)p.n_tail, FMT, FMT, 0);
       constexpr uint32_t idesc_pv = idesc_f8(128, D, FPSA_E4M3, FMT, 1);
       const uint32_t sq = smem_u32(smem + S::kQ);
       mbar_wait(&bar_q, 0);
       tc_fence_after();
-#ifdef FPSA_TRACE
-      long long w_kv = 0, w_p = 0;
-      const long long t_loop = clock64();
-#endif
-      for (int32_t j = 0; j <= n_kv; ++j) {
+      // S(j) = Q K_j^T into TMEM buffer j % 2
+      auto issue_qk = [&](int32_t j) {
         const int st = j % kStages;
-        if (j < n_kv) {
 #ifdef FPSA_TRACE
-          const long long ta = clock64();
+        const long long tk0 = clock64();
 #endif
-          mbar_wait(&bar_kv_full[st], (j / kStages) & 1);
+        mbar_wait(&bar_kv_full[st], (j / kStages) & 1);
 #ifdef FPSA_TRACE
-          w_kv += clock64() - ta;
+        atomicAdd(&g_trace[7], (unsigned long long)(clock64() - tk0));
 #endif
-          tc_fence_after();
-        }
-        const int pst = (j + kStages - 1) % kStages;  // stage of block j-1
+        tc_fence_after();
         const uint32_t sk = smem_u32(smem + S::kK + st * S::kTile);
-        const uint32_t sv_prev = smem_u32(smem + S::kV + pst * S::kTile);
-        for (int q = 0; q < nqb; ++q) {
-          if (j > 0) {
-#ifdef FPSA_TRACE
-            const long long tb = clock64();
-#endif
-            mbar_wait(&bar_p_ready[q], (j - 1) & 1);
-#ifdef FPSA_TRACE
-            w_p += clock64() - tb;
-#endif
-            tc_fence_after();
+        const uint32_t idq = (j % p.nb) == p.nb - 1 ? idesc_qk_tail : idesc_qk;
 #pragma unroll
-            for (int k = 0; k < kBlk / 32; ++k)
-              mma_f8_ts(tm_o[q], tm_s[q] + 8 * k, desc_mnmajor<D>(sv_prev + k * 32 * D), idesc_pv,
-                        (j > 1 || k > 0) ? 1u : 0u);
-          }
-          if (j < n_kv) {
-            const uint32_t sqq = sq + q * S::kTile;
+        for (int k = 0; k < D / 32; ++k)
+          mma_f8_ss(tm_s(j), desc_kmajor<D>(sq + 32 * k), desc_kmajor<D>(sk + 32 * k), idq, k > 0 ? 1u : 0u);
+        mma_commit(&bar_s_full[j & 1]);
+      };
+      issue_qk(0);
+      if (n_kv > 1) issue_qk(1);
+      for (int32_t j = 0; j < n_kv; ++j) {
+        // O += P~(j) V_j once the softmax has written P~(j) over S(j)
+#ifdef FPSA_TRACE
+        const long long tp0 = clock64();
+#endif
+        mbar_wait(&bar_p_ready[j & 1], (j >> 1) & 1);
+#ifdef FPSA_TRACE
+        atomicAdd(&g_trace[3], (unsigned long long)(clock64() - tp0));
+#endif
+        tc_fence_after();
+        const int st = j % kStages;
+        const uint32_t sv = smem_u32(smem + S::kV + st * S::kTile);
 #pragma unroll
-            for (int k = 0; k < D / 32; ++k)
-              mma_f8_ss(tm_s[q], desc_kmajor<D>(sqq + 32 * k), desc_kmajor<D>(sk + 32 * k), idesc_qk, k > 0 ? 1u : 0u);
-            mma_commit(&bar_s_full[q]);
-          }
-        }
-        if (j > 0) mma_commit(&bar_kv_empty[pst]);
+        for (int k = 0; k < kBlk / 32; ++k)
+          mma_f8_ts(tm_o, tm_s(j) + 8 * k, desc_mnmajor<D>(sv + k * 32 * D), idesc_pv, (j > 0 || k > 0) ? 1u : 0u);
+        mma_commit(&bar_kv_empty[st]);
+        mma_commit(&bar_pv);
+        if (j + 2 < n_kv) issue_qk(j + 2);
       }
       mma_commit(&bar_o);
-#ifdef FPSA_TRACE
-      TRACE_ADD(2, w_kv);
-      TRACE_ADD(3, w_p);
-      TRACE_ADD(4, clock64() - t_loop);
-#endif
     }
-  } else if (warp / 8 < nqb) {
-    // ------------------------------------------------------------ softmax: row x column half
-    const int q = warp / 8;               // query block
-    const int c = (warp / 4) & 1;         // column half of S and O owned by this thread
-    const int pair = warp & 7 & 3 | (q << 2);  // warps (w, w+4) of a query block share TMEM lanes
-    const int row = threadIdx.x & 127;    // TMEM lane = row of the query block
-    const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
-    const uint32_t s_half = tm_s[q] + lane_off + c * kHalf;
-    const uint32_t p_half = tm_s[q] + lane_off + c * (kHalf / 4);
-    const uint32_t o_half = tm_o[q] + lane_off + c * (D / 2);
-    const float cq = (float)p.q_scales[h * p.M + u] * p.scale_log2;
+  } else {
+    // ------------------------------------------------------------ softmax: (row, column half)
+    const int quarter = warp & 3;
+    const int half = warp >> 2;                 // S columns [64 half, 64 half + 64)
+    const int row = quarter * 32 + lane;        // TMEM lane = row of the query block
+    const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+    const uint32_t o_addr = tm_o + lane_off + half * (D / 2);
+    const float qs = (float)p.q_scales[h * p.M + u];
+    const float sl = p.softmax_log2;
     const float tau = p.tau;
-    auto pair_sync = [&]() { named_bar_sync(1 + pair, 64); };
-    // Rows keep a reference max m_ref; P~ = e4m3(448 * 2^(x - m_ref - tau)).
+    auto pair_sync = [&]() { named_bar_sync(1 + quarter, 64); };
+    // Rows keep a reference max m_ref (log2 units); P~ = e4m3(448 * 2^(x - m_ref - tau)).
     // No per-block max is taken: if both half-row sums of P~ stay <= 448 no
     // element can have saturated and the block is accepted as computed.  The
     // first block and blocks with a larger sum (a logit above m_ref + tau, or
-    // a false alarm) take the exact path, which lazily raises m_ref and
-    // rescales the TMEM accumulator; the two halves of a row decide together.
+    // a false alarm) take the exact path, which lazily raises m_ref for the
+    // warp and rescales the TMEM accumulator (oracle.onepass_forward).
     float m_ref = 0.0f, l = 0.0f;
+    int32_t kt = 0, b = 0;
 #ifdef FPSA_TRACE
-    long long w_s = 0, n_resc = 0;
+    long long w_s = 0, w_c = 0, n_resc = 0;
     const long long t_loop = clock64();
 #endif
     for (int32_t j = 0; j < n_kv; ++j) {
-      const int32_t kt = j / p.nb, b = j - kt * p.nb;
-      const int32_t v = __ldg(p.ids + kt0 + kt);
-      const float cj = cq * (float)__ldg(p.k_scales + h * p.M + v);
-      const int valid = min(kBlk, p.tv - b * kBlk) - c * kHalf;  // valid columns of this half (may be <= 0)
+      const float kf = kt < kFacCap ? s_kfac[kt] : (float)__ldg(p.k_scales + h * p.M + __ldg(p.ids + kt0 + kt));
+      const float c = (qs * kf) * sl;
+      const bool tail = b == p.nb - 1;
+      const int ncol = tail ? p.n_tail : kBlk;
+      const int ncol_h = min(max(ncol - kHalfCols * half, 0), kHalfCols);
+      const bool pad8 = tail && p.tail_pad8 && ncol - kHalfCols * half <= kHalfCols;
+      const uint32_t s_addr = tm_s(j) + lane_off + half * kHalfCols;
 #ifdef FPSA_TRACE
       const long long ts0 = clock64();
 #endif
-      mbar_wait(&bar_s_full[q], j & 1);
+      mbar_wait(&bar_s_full[j & 1], (j >> 1) & 1);
 #ifdef FPSA_TRACE
       w_s += clock64() - ts0;
 #endif
       tc_fence_after();
-      float sv[kHalf];
-      // S stays intact in TMEM until P is written over it: the exact path reloads it.
-      auto load_s = [&]() {
-        tmem_ld32(s_half + 0, reinterpret_cast<uint32_t*>(sv + 0));
-        tmem_ld32(s_half + 32, reinterpret_cast<uint32_t*>(sv + 32));
-        tmem_wait_ld();
-        // key columns >= valid are padding (zero K/V rows of a key tile's last
-        // block): -inf drops them from max, sum and P (valid % 8 == 0, host-checked)
-        if (valid < kHalf) {
-#pragma unroll
-          for (int i = 0; i < kHalf; i += 8) {
-            const bool ok = i < valid;
-#pragma unroll
-            for (int k2 = i; k2 < i + 8; ++k2) sv[k2] = ok ? sv[k2] : -INFINITY;
-          }
-        }
-      };
-      // exact row max over both halves (pair exchange through shared memory)
-      auto row_max = [&]() {
-        float mx0 = -INFINITY, mx1 = -INFINITY;
-#pragma unroll
-        for (int i = 0; i < kHalf; i += 4) {
-          mx0 = max3(mx0, sv[i], sv[i + 1]);
-          mx1 = max3(mx1, sv[i + 2], sv[i + 3]);
-        }
-        s_xchg[q][c][row] = fmaxf(mx0, mx1);
+      auto exchange_max = [&]() {
+        s_xchg[half][row] = half_max(s_addr, ncol_h, pad8);
         pair_sync();
-        const float m = fmaxf(s_xchg[q][0][row], s_xchg[q][1][row]) * cj;
+        const float m = fmaxf(s_xchg[0][row], s_xchg[1][row]) * c;
         pair_sync();  // the exchange slots are reused
         return m;
       };
-      uint32_t w[kHalf / 4];
-      auto exp_half = [&](float mref) {
-        const f2 cc2 = bcast(cj), noff = bcast(kLog2_448 - mref - tau);
-        const float cs = cj * (1.0f / 256.0f), ns = (kLog2_448 - mref - tau + 126.0f) * (1.0f / 256.0f);
-        f2 lsum0 = bcast(0.0f), lsum1 = bcast(0.0f);
-#pragma unroll
-        for (int k2 = 0; k2 < kHalf; k2 += 4) {
-          f2 pa, pb;
-          if (kPolyGroup(k2 / 4)) {
-            pa = exp2_poly_sat(fma_sat_pair(f2{sv[k2], sv[k2 + 1]}, cs, ns));
-            pb = exp2_poly_sat(fma_sat_pair(f2{sv[k2 + 2], sv[k2 + 3]}, cs, ns));
-          } else {
-            pa = fma2(f2{sv[k2], sv[k2 + 1]}, cc2, noff);
-            pb = fma2(f2{sv[k2 + 2], sv[k2 + 3]}, cc2, noff);
-            pa = f2{ex2(pa.x), ex2(pa.y)};
-            pb = f2{ex2(pb.x), ex2(pb.y)};
-          }
-          lsum0 = add2(lsum0, pa);
-          lsum1 = add2(lsum1, pb);
-          w[k2 / 4] = e4m3x4(pa, pb);
-        }
-        const f2 ls = add2(lsum0, lsum1);
-        return ls.x + ls.y;
-      };
-      load_s();
-      if (j == 0) m_ref = row_max();
-      float lb = exp_half(m_ref);
-      // half-row sums <= 448 bound every element; the pair agrees on the verdict
-      const uint32_t over = __any_sync(0xffffffffu, lb > 448.0f) ? 1u : 0u;
-      if (lane == 0) s_flag[j & 1][pair][c] = over;
-      pair_sync();
-      if (s_flag[j & 1][pair][0] | s_flag[j & 1][pair][1]) {
-        load_s();
-        const float mb = row_max();
-        if (__any_sync(0xffffffffu, mb > m_ref + tau)) {  // identical in both warps of the pair
-          const float m_new = fmaxf(m_ref, mb);
-          const float alpha = ex2(m_ref - m_new);
-          l *= alpha;
-          m_ref = m_new;
+      if (j == 0) m_ref = exchange_max();
+      uint32_t w[kHalfCols / 4];
+      float lb;
+      bool redo = false;
 #ifdef FPSA_TRACE
-          ++n_resc;
+      const long long tc0 = clock64();
 #endif
 #pragma unroll 1
-          for (int cc = 0; cc < D / 2; cc += 16) {
-            uint32_t o[16];
-            tmem_ld16(o_half + cc, o);
-            tmem_wait_ld();
-#pragma unroll
-            for (int i = 0; i < 16; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
-            tmem_st16(o_half + cc, o);
-          }
-          tmem_wait_st();
-          lb = exp_half(m_ref);
+      for (;;) {  // one pass; a second one only after the exact path raised m_ref
+        lb = softmax_half(s_addr, ncol_h, pad8, c, kLog2_448 - m_ref - tau, w);
+#ifdef FPSA_TRACE
+        if (!redo) w_c += clock64() - tc0;
+#endif
+        if (redo) {
+          pair_sync();  // both halves re-read S(j) before P is written over it
+          break;
         }
+        // half-row sums <= 448 bound every element; the pair agrees on the verdict
+        const uint32_t over = __any_sync(0xffffffffu, lb > 448.0f) ? 1u : 0u;
+        if (lane == 0) s_flag[j & 1][quarter][half] = over;
+        pair_sync();  // also: both halves have read S(j) before either writes P over it
+        if (!(s_flag[j & 1][quarter][0] | s_flag[j & 1][quarter][1])) break;
+        const float mb = exchange_max();
+        if (!__any_sync(0xffffffffu, mb > m_ref + tau)) break;  // identical in both warps of the pair
+        const float m_new = fmaxf(m_ref, mb);
+        const float alpha = ex2(m_ref - m_new);
+        l *= alpha;
+        m_ref = m_new;
+#ifdef FPSA_TRACE
+        ++n_resc;
+#endif
+        if (j > 0) mbar_wait(&bar_pv, (j - 1) & 1);  // O complete up to block j-1
+        tc_fence_after();
+#pragma unroll 1
+        for (int cc = 0; cc < D / 2; cc += 32) {
+          uint32_t o[32];
+          tmem_ld32(o_addr + cc, o);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+          tmem_st32(o_addr + cc, o);
+        }
+        tmem_wait_st();
+        redo = true;
       }
       l += lb;
-      tmem_st16(p_half, w);
+      tmem_st16(tm_s(j) + lane_off + half * (kHalfCols / 4), w);
       tmem_wait_st();
       tc_fence_before();
-      mbar_arrive(&bar_p_ready[q]);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bar_p_ready[j & 1]);
+      if (++b == p.nb) {
+        b = 0;
+        ++kt;
+      }
     }
 #ifdef FPSA_TRACE
     if (lane == 0) {
-      TRACE_ADD(0, w_s);
-      TRACE_ADD(1, clock64() - t_loop);
-      TRACE_ADD(5, n_resc);
-      TRACE_ADD(6, n_kv);
+      atomicAdd(&g_trace[0], (unsigned long long)w_s);
+      atomicAdd(&g_trace[1], (unsigned long long)(clock64() - t_loop));
+      atomicAdd(&g_trace[2], (unsigned long long)w_c);
+      atomicAdd(&g_trace[5], (unsigned long long)n_resc);
+      atomicAdd(&g_trace[6], (unsigned long long)n_kv);
     }
 #endif
     // ------------------------------------------------------------ epilogue
-    s_xchg[q][c][row] = l;
+    s_xchg[half][row] = l;
     mbar_wait(&bar_o, 0);
     tc_fence_after();
     pair_sync();
-    const float inv_l = 1.0f / (s_xchg[q][0][row] + s_xchg[q][1][row]);
-    const int32_t r = (qb0 + q) * kBlk + row;  // row inside the tile
+    const float inv_l = 1.0f / (s_xchg[0][row] + s_xchg[1][row]);
+    const int32_t r = qb * kBlk + row;  // row inside the tile
     int64_t token;
     if (p.natural) {
       const int32_t ut = u / (p.dh * p.dw), uh = (u / p.dw) % p.dh, uw = u % p.dw;
@@ -473,9 +528,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
 #pragma unroll
     for (int cc = 0; cc < D / 2; cc += 32) {
-      const int col = c * (D / 2) + cc;
+      const int col = half * (D / 2) + cc;
       uint32_t o[32];
-      tmem_ld32(o_half + cc, o);
+      tmem_ld32(o_addr + cc, o);
       tmem_wait_ld();
       if (r < p.tv) {
         float f[32];
@@ -592,8 +647,13 @@ extern "C" int fpsa_attn_fwd(const uint8_t* q_codes, const uint8_t* k_codes, con
   p.M = M;
   p.tv = tv;
   p.pitch = tile_pitch;
-  p.nb = tile_pitch / kBlk;
-  p.scale_log2 = softmax_scale * 1.4426950408889634f;
+  p.nb = (tv + kBlk - 1) / kBlk;
+  {
+    const int32_t tail = tv - kBlk * ((tv - 1) / kBlk);  // valid keys of a tile's last 128-key block
+    p.n_tail = (tail + 15) / 16 * 16;
+    p.tail_pad8 = p.n_tail != tail;
+  }
+  p.softmax_log2 = softmax_scale * 1.4426950408889634f;
   p.tau = tau_log2;
   p.out = out;
   p.out_ts = out_token_stride;
