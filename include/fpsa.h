@@ -112,11 +112,10 @@ int fpsa_quantize_qkv(const void* q, const void* k, const void* v, int dtype, in
                       uint8_t* v_codes, double* q_scales, double* k_scales, double* v_scales, void* workspace,
                       int32_t* err_flag, void* stream);
 
-/* Work list for fpsa_attn_fwd: one entry per (head, query tile, 128-row
- * query block), tiles with the most key tiles first within each head, the
- * query blocks of a tile adjacent (they stream the same K/V).  Host-side;
- * n_items returns the count, items (capacity `cap`, 3 int32 each: head,
- * tile, query block). */
+/* Work list for fpsa_attn_fwd: one entry per (head, query tile, pair of
+ * 128-row query blocks), tiles with the most key tiles first within each
+ * head.  Host-side; n_items returns the count, items (capacity `cap`, 3 int32
+ * each: head, tile, first query block of the pair). */
 int fpsa_attn_worklist(int32_t heads, fpsa_dims3 tile_dims, int32_t tile_volume, const int32_t* offs_host,
                        int32_t* items, int64_t cap, int64_t* n_items);
 

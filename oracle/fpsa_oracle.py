@@ -348,12 +348,12 @@ def _exp2_poly(x: np.ndarray) -> np.ndarray:
     return np.ldexp(y, j.astype(np.int64))
 
 
-def onepass_forward(codes: dict, tv, offs, ids, fmt: Fmt = E4M3, softmax_scale=None, block=128, tau=0.0,
+def onepass_forward(codes: dict, tv, offs, ids, fmt: Fmt = E4M3, softmax_scale=None, block=64, tau=0.0,
                     poly=False):
     """Emulation of the GPU kernel's one-pass schedule (NOT the reference semantics).
 
-    Keys are visited per key tile in 128-key blocks (tiles padded to a multiple
-    of 128); the running row max m is updated per block, the unnormalised
+    Keys are visited per key tile in `block`-key blocks (the last block of a
+    tile is shorter); the running row max m is updated per block, the unnormalised
     weights 448*exp(x - m) are rounded to E4M3 before the PV product, the
     denominator sums the unrounded weights.  Used to check the CUDA kernel
     tightly; the reference-facing check is against ``fp8_sparse_forward``.

@@ -3,32 +3,34 @@
 // Replaces fp8sta.attention.fp8_sparse_forward / _engine
 // (/root/reference/pkg/src/fp8sta/attention.py:91-149, :179-208).
 //
-// One CTA = (head h, query tile u, one 128-row query block of u).  The key
+// One CTA = (head h, query tile u, two 128-row query blocks of u).  The key
 // sequence of u is the concatenation of its admissible key tiles in
 // ascending id order (sparsity.py:63-67, the reference's reduction order),
-// each key tile cut into 128-key blocks; a tile's last block has
-// n_tail = tv - 128 (nb - 1) keys (rounded up to 16), so no padding key of a
-// 240-token tile is multiplied or exponentiated.  Per key block j:
+// each key tile cut into 64-key blocks; a tile's last block has
+// n_tail = tv - 64 (nb - 1) keys (rounded up to 16), so no padding key of a
+// 240-token tile is multiplied or exponentiated.  Per key block j and query
+// block q:
 //
-//   S(j)  = Q K_j^T                  tcgen05.mma kind::f8f6f4, A/B from smem,
-//                                    fp32 accumulator in TMEM buffer j % 2
-//   x     = S * (sq[u] * sk[v] * softmax_scale * log2 e)     per-tile factors
-//   m     = reference row max, raised lazily (only when a block overflows the
-//           e4m3 range above it)
-//   P~    = e4m3(448 * 2^-tau * 2^(x - m))   re-quantised per key block,
-//           written back to TMEM over S(j) (4 codes per column)
-//   O    += P~ V_j                    tcgen05.mma, A = P~ from TMEM, B = V from
+//   S(q,j) = Q_q K_j^T               tcgen05.mma kind::f8f6f4 M128 N64, A/B from
+//                                    smem, fp32 accumulator in TMEM buffer (q, j % 2)
+//   x      = S * (sq[u] * sk[v] * softmax_scale * log2 e)     per-tile factors
+//   m      = reference row max, raised lazily (only when a block overflows the
+//            e4m3 range above it)
+//   P~     = e4m3(448 * 2^-tau * 2^(x - m))   re-quantised per key block,
+//            written back to TMEM over S(q,j) (4 codes per column)
+//   O_q   += P~ V_j                  tcgen05.mma, A = P~ from TMEM, B = V from
 //                                    smem (MN-major, V stored [keys][d])
-//   l    += sum of the unrounded P~ (fp32)
+//   l      += sum of the unrounded P~ (fp32)
 // and finally out = O * v_scale[c] / l.
 //
-// S is double-buffered in TMEM (O: 128 columns, S(even), S(odd): 128 each),
-// so QK(j+1) runs while the softmax works on S(j) and the MMA issue order
-// PV(j), QK(j+2) never makes the softmax wait on its own P.
+// TMEM (512 columns): O_0, O_1 (128 each), S(0, even/odd), S(1, even/odd)
+// (64 each).  With S double-buffered, QK(q, j+1) runs while the softmax
+// works on S(q, j), and the MMA issue order PV(q, j), QK(q, j+2) never makes
+// the softmax wait on its own P.
 //
-// Warp roles (320 threads): warps w and w+4 (w < 4) own TMEM lane quarter w
-// (rows 32w..32w+31) and split the 128 S columns in halves; warp 8 is the
-// TMA producer (and TMEM allocator), warp 9 the MMA issuer.
+// Warp roles (320 threads): warps 0-3 own the 128 rows (TMEM lanes) of query
+// block 0, warps 4-7 those of query block 1, one thread per row; warp 8 is
+// the TMA producer (and TMEM allocator), warp 9 the MMA issuer.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -52,9 +54,9 @@ constexpr int kTmaWarp = kSoftmaxWarps;
 constexpr int kMmaWarp = kSoftmaxWarps + 1;
 constexpr int kThreads = (kSoftmaxWarps + 2) * 32;
 
-constexpr int kStages = 4;
-constexpr int kBlk = 128;      // rows per query block and keys per key block
-constexpr int kHalfCols = 64;  // S columns per softmax thread
+constexpr int kStages = 8;    // K/V ring depth (64-key blocks)
+constexpr int kBlk = 128;     // rows per query block
+constexpr int kKeys = 64;     // keys per key block = S columns per softmax thread
 constexpr int kFacCap = 2048;  // key-tile scale factors cached in shared memory per CTA
 constexpr float kLog2_448 = 8.807354922057604f;
 constexpr uint32_t kNegInf = 0xFF800000u;
@@ -66,8 +68,8 @@ struct AttnParams {
   const int32_t* offs;
   const int32_t* ids;
   const int32_t* items;
-  int32_t M, tv, pitch, nb;
-  int32_t n_tail;     // S columns of the last key block of a tile (tv - 128 (nb-1), rounded up to 16)
+  int32_t M, tv, pitch, nb, nqb;  // nb: 64-key blocks per tile; nqb: 128-row query blocks per tile
+  int32_t n_tail;     // S columns of the last key block of a tile (tv - 64 (nb-1), rounded up to 16)
   int32_t tail_pad8;  // 1 if the last 8 of those columns are zero padding (tv % 16 == 8)
   float softmax_log2;  // f32(softmax_scale * log2 e)
   float tau;
@@ -79,11 +81,12 @@ struct AttnParams {
 
 template <int D>
 struct Smem {
-  static constexpr int kTile = kBlk * D;  // bytes of one 128-row fp8 tile
+  static constexpr int kQTile = kBlk * D;   // bytes of one 128-row fp8 query block
+  static constexpr int kKTile = kKeys * D;  // bytes of one 64-key fp8 K or V block
   static constexpr int kQ = 0;
-  static constexpr int kK = kTile;
-  static constexpr int kV = kK + kStages * kTile;
-  static constexpr int kBytes = kV + kStages * kTile;
+  static constexpr int kK = 2 * kQTile;
+  static constexpr int kV = kK + kStages * kKTile;
+  static constexpr int kBytes = kV + kStages * kKTile;
   static constexpr uint32_t kSBO = 8 * D;  // 8 rows of D bytes
 };
 
@@ -222,11 +225,11 @@ __device__ __forceinline__ void softmax_chunk(uint32_t* s, int ncol, bool pad8, 
   else w[8 * C + 4] = w[8 * C + 5] = w[8 * C + 6] = w[8 * C + 7] = 0u;
 }
 
-// One half row of one key block: 64 S columns streamed from TMEM in two
-// 32-column chunks (the second tcgen05.ld is in flight while the first chunk
-// is processed), ncol (multiple of 16, 0..64) valid.  P words of absent
-// columns are zero.  Returns the half-row sum of the unrounded weights.
-__device__ __forceinline__ float softmax_half(uint32_t s_addr, int ncol, bool pad8, float c, float boff, uint32_t* w) {
+// One row of one key block: 64 S columns streamed from TMEM in two 32-column
+// chunks (the second tcgen05.ld is in flight while the first chunk is
+// processed), ncol (multiple of 16, 16..64) valid.  P words of absent
+// columns are zero.  Returns the row sum of the unrounded weights.
+__device__ __forceinline__ float softmax_block(uint32_t s_addr, int ncol, bool pad8, float c, float boff, uint32_t* w) {
   const f2 cc = bcast(c), bb = bcast(boff);
   const float cs = c * (1.0f / 256.0f), bs = (boff + 126.0f) * (1.0f / 256.0f);
   f2 acc[4] = {bcast(0.f), bcast(0.f), bcast(0.f), bcast(0.f)};
@@ -243,11 +246,11 @@ __device__ __forceinline__ float softmax_half(uint32_t s_addr, int ncol, bool pa
   return t.x + t.y;
 }
 
-// Max of the first ncol (0..64) raw S values of a half row.
-__device__ __forceinline__ float half_max(uint32_t s_addr, int ncol, bool pad8) {
+// Max of the first ncol (16..64) raw S values of a row.
+__device__ __forceinline__ float block_max(uint32_t s_addr, int ncol, bool pad8) {
   float m0 = -INFINITY, m1 = -INFINITY;
 #pragma unroll
-  for (int base = 0; base < kHalfCols; base += 32) {
+  for (int base = 0; base < kKeys; base += 32) {
     if (base < ncol) {
       uint32_t s[32];
       tmem_ld32(s_addr + base, s);
@@ -279,19 +282,20 @@ __global__ void __launch_bounds__(kThreads, 1)
   using S = Smem<D>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  __shared__ uint64_t bar_q, bar_o, bar_pv;
+  __shared__ uint64_t bar_q, bar_o;
   __shared__ uint64_t bar_kv_full[kStages], bar_kv_empty[kStages];
-  __shared__ uint64_t bar_s_full[2], bar_p_ready[2];  // by step parity: warps may run one step apart
+  __shared__ uint64_t bar_s_full[2][2];   // [query block][S buffer]
+  __shared__ uint64_t bar_p_ready[2][2];  // [query block][step parity]: a block's warps may run one step apart
+  __shared__ uint64_t bar_pv[2];          // [query block]: PV(q, j) complete
   __shared__ uint32_t s_tmem;
   __shared__ float s_vscale[D];
   __shared__ float s_kfac[kFacCap];
-  __shared__ float s_xchg[2][kBlk];     // [half][row] pair exchange
-  __shared__ uint32_t s_flag[2][4][2];  // [step parity][lane quarter][half] overflow verdicts
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int32_t h = p.items[3 * blockIdx.x + 0];
   const int32_t u = p.items[3 * blockIdx.x + 1];
-  const int32_t qb = p.items[3 * blockIdx.x + 2];
+  const int32_t qb0 = p.items[3 * blockIdx.x + 2];
+  const int nqb = min(2, p.nqb - qb0);
   const int32_t kt0 = p.offs[u];
   const int32_t n_kt = p.offs[u + 1] - kt0;
   const int32_t n_kv = n_kt * p.nb;
@@ -299,15 +303,17 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (threadIdx.x == 0) {
     mbar_init(&bar_q, 1);
     mbar_init(&bar_o, 1);
-    mbar_init(&bar_pv, 1);
     for (int i = 0; i < kStages; ++i) {
       mbar_init(&bar_kv_full[i], 1);
       mbar_init(&bar_kv_empty[i], 1);
     }
-    mbar_init(&bar_s_full[0], 1);
-    mbar_init(&bar_s_full[1], 1);
-    mbar_init(&bar_p_ready[0], kSoftmaxWarps);  // one arrival per softmax warp
-    mbar_init(&bar_p_ready[1], kSoftmaxWarps);
+    for (int q = 0; q < 2; ++q) {
+      mbar_init(&bar_s_full[q][0], 1);
+      mbar_init(&bar_s_full[q][1], 1);
+      mbar_init(&bar_p_ready[q][0], 4);  // one arrival per softmax warp of the block
+      mbar_init(&bar_p_ready[q][1], 4);
+      mbar_init(&bar_pv[q], 1);
+    }
     fence_barrier_init();
   }
   if (warp == kTmaWarp) {
@@ -324,98 +330,124 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = s_tmem;
-  const uint32_t tm_o = tmem;
-  // S buffers at columns 128 and 256 (computed, not indexed: a local array would go to memory)
-  auto tm_s = [tmem](int32_t j) { return tmem + 128u + 128u * (uint32_t)(j & 1); };
+  // O_q at column 128 q; S(q, buffer) at 256 + 128 q + 64 buffer (computed, not
+  // indexed: a local array would live in memory)
+  auto tm_o = [tmem](int q) { return tmem + 128u * (uint32_t)q; };
+  auto tm_s = [tmem](int q, int32_t j) { return tmem + 256u + 128u * (uint32_t)q + 64u * (uint32_t)(j & 1); };
 
   if (warp == kTmaWarp) {
-    // ------------------------------------------------------------ TMA producer
+    // ------------------------------------------------------------ TMA producer (warp-uniform, one elected lane issues)
     if (lane == 0) {
       prefetch_tmap(&tm_q);
       prefetch_tmap(&tm_k);
       prefetch_tmap(&tm_v);
-      mbar_arrive_expect_tx(&bar_q, S::kTile);
-      tma_load_2d(smem + S::kQ, &tm_q, 0, (h * p.M + u) * p.pitch + qb * kBlk, &bar_q);
-      int32_t kt = 0, b = 0;
-      int32_t krow = (h * p.M + p.ids[kt0]) * p.pitch;
-      for (int32_t j = 0; j < n_kv; ++j) {
-        const int st = j % kStages;
-        if (j >= kStages) mbar_wait(&bar_kv_empty[st], ((j / kStages) - 1) & 1);
-        mbar_arrive_expect_tx(&bar_kv_full[st], 2 * S::kTile);
-        tma_load_2d(smem + S::kK + st * S::kTile, &tm_k, 0, krow + b * kBlk, &bar_kv_full[st]);
-        tma_load_2d(smem + S::kV + st * S::kTile, &tm_v, 0, krow + b * kBlk, &bar_kv_full[st]);
-        if (++b == p.nb) {
-          b = 0;
-          if (++kt < n_kt) krow = (h * p.M + __ldg(p.ids + kt0 + kt)) * p.pitch;
-        }
+    }
+    __syncwarp();
+    const int32_t qrow = (h * p.M + u) * p.pitch + qb0 * kBlk;
+    mbar_arrive_expect_tx_w(&bar_q, nqb * S::kQTile);
+    for (int q = 0; q < nqb; ++q) tma_load_2d_w(smem + S::kQ + q * S::kQTile, &tm_q, 0, qrow + q * kBlk, &bar_q);
+    int32_t kt = 0, b = 0, st = 0;
+    uint32_t ph = 0;
+    int32_t krow = (h * p.M + p.ids[kt0]) * p.pitch;
+    for (int32_t j = 0; j < n_kv; ++j) {
+      if (j >= kStages) mbar_wait(&bar_kv_empty[st], ph ^ 1);
+      mbar_arrive_expect_tx_w(&bar_kv_full[st], 2 * S::kKTile);
+      tma_load_2d_w(smem + S::kK + st * S::kKTile, &tm_k, 0, krow + b * kKeys, &bar_kv_full[st]);
+      tma_load_2d_w(smem + S::kV + st * S::kKTile, &tm_v, 0, krow + b * kKeys, &bar_kv_full[st]);
+      if (++b == p.nb) {
+        b = 0;
+        if (++kt < n_kt) krow = (h * p.M + __ldg(p.ids + kt0 + kt)) * p.pitch;
+      }
+      if (++st == kStages) {
+        st = 0;
+        ph ^= 1;
       }
     }
   } else if (warp == kMmaWarp) {
-    // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
-      constexpr uint32_t idesc_qk = idesc_f8(128, 128, FMT, FMT, 0);
-      const uint32_t idesc_qk_tail = idesc_f8(128, (uint32_t)p.n_tail, FMT, FMT, 0);
-      constexpr uint32_t idesc_pv = idesc_f8(128, D, FPSA_E4M3, FMT, 1);
-      const uint32_t sq = smem_u32(smem + S::kQ);
-      mbar_wait(&bar_q, 0);
+    // ------------------------------------------------------------ MMA issuer (warp-uniform, one elected lane issues)
+    constexpr uint32_t idesc_qk = idesc_f8(128, kKeys, FMT, FMT, 0);
+    const uint32_t idesc_qk_tail = idesc_f8(128, (uint32_t)p.n_tail, FMT, FMT, 0);
+    constexpr uint32_t idesc_pv = idesc_f8(128, D, FPSA_E4M3, FMT, 1);
+    const uint32_t sq = smem_u32(smem + S::kQ);
+    const uint32_t sk0 = smem_u32(smem + S::kK), sv0 = smem_u32(smem + S::kV);
+    mbar_wait(&bar_q, 0);
+    tc_fence_after();
+    // S(q, j) = Q_q K_j^T into TMEM buffer (q, j % 2); (st, b) = stage and in-tile block of j
+    auto issue_qk = [&](int q, int32_t j, int st, bool tail) {
+      const uint32_t sk = sk0 + st * S::kKTile;
+      const uint32_t idq = tail ? idesc_qk_tail : idesc_qk;
+      const uint32_t sqq = sq + q * S::kQTile;
+#pragma unroll
+      for (int k = 0; k < D / 32; ++k)
+        mma_f8_ss_w(tm_s(q, j), desc_kmajor<D>(sqq + 32 * k), desc_kmajor<D>(sk + 32 * k), idq, k > 0 ? 1u : 0u);
+      mma_commit_w(&bar_s_full[q][j & 1]);
+    };
+    // (st2, b2): stage / in-tile block of step j + 2, with the full-barrier phase
+    int st2 = 0, b2 = 0;
+    uint32_t ph2 = 0;
+    auto advance2 = [&]() {
+      if (++b2 == p.nb) b2 = 0;
+      if (++st2 == kStages) {
+        st2 = 0;
+        ph2 ^= 1;
+      }
+    };
+    for (int32_t j = 0; j < min(n_kv, 2); ++j) {
+      mbar_wait(&bar_kv_full[st2], ph2);
       tc_fence_after();
-      // S(j) = Q K_j^T into TMEM buffer j % 2
-      auto issue_qk = [&](int32_t j) {
-        const int st = j % kStages;
+      for (int q = 0; q < nqb; ++q) issue_qk(q, j, st2, b2 == p.nb - 1);
+      advance2();
+    }
+    int st = 0;
+    for (int32_t j = 0; j < n_kv; ++j) {
+      const uint32_t sv = sv0 + st * S::kKTile;
+      const bool more = j + 2 < n_kv;
+      if (more) {
 #ifdef FPSA_TRACE
         const long long tk0 = clock64();
 #endif
-        mbar_wait(&bar_kv_full[st], (j / kStages) & 1);
+        mbar_wait(&bar_kv_full[st2], ph2);
 #ifdef FPSA_TRACE
-        atomicAdd(&g_trace[7], (unsigned long long)(clock64() - tk0));
+        if (lane == 0) atomicAdd(&g_trace[7], (unsigned long long)(clock64() - tk0));
 #endif
         tc_fence_after();
-        const uint32_t sk = smem_u32(smem + S::kK + st * S::kTile);
-        const uint32_t idq = (j % p.nb) == p.nb - 1 ? idesc_qk_tail : idesc_qk;
-#pragma unroll
-        for (int k = 0; k < D / 32; ++k)
-          mma_f8_ss(tm_s(j), desc_kmajor<D>(sq + 32 * k), desc_kmajor<D>(sk + 32 * k), idq, k > 0 ? 1u : 0u);
-        mma_commit(&bar_s_full[j & 1]);
-      };
-      issue_qk(0);
-      if (n_kv > 1) issue_qk(1);
-      for (int32_t j = 0; j < n_kv; ++j) {
-        // O += P~(j) V_j once the softmax has written P~(j) over S(j)
+      }
+      for (int q = 0; q < nqb; ++q) {
+        // O_q += P~(q, j) V_j once the softmax has written P~ over S(q, j)
 #ifdef FPSA_TRACE
         const long long tp0 = clock64();
 #endif
-        mbar_wait(&bar_p_ready[j & 1], (j >> 1) & 1);
+        mbar_wait(&bar_p_ready[q][j & 1], (j >> 1) & 1);
 #ifdef FPSA_TRACE
-        atomicAdd(&g_trace[3], (unsigned long long)(clock64() - tp0));
+        if (lane == 0) atomicAdd(&g_trace[3], (unsigned long long)(clock64() - tp0));
 #endif
         tc_fence_after();
-        const int st = j % kStages;
-        const uint32_t sv = smem_u32(smem + S::kV + st * S::kTile);
 #pragma unroll
-        for (int k = 0; k < kBlk / 32; ++k)
-          mma_f8_ts(tm_o, tm_s(j) + 8 * k, desc_mnmajor<D>(sv + k * 32 * D), idesc_pv, (j > 0 || k > 0) ? 1u : 0u);
-        mma_commit(&bar_kv_empty[st]);
-        mma_commit(&bar_pv);
-        if (j + 2 < n_kv) issue_qk(j + 2);
+        for (int k = 0; k < kKeys / 32; ++k)
+          mma_f8_ts_w(tm_o(q), tm_s(q, j) + 8 * k, desc_mnmajor<D>(sv + k * 32 * D), idesc_pv,
+                      (j > 0 || k > 0) ? 1u : 0u);
+        mma_commit_w(&bar_pv[q]);
+        if (more) issue_qk(q, j + 2, st2, b2 == p.nb - 1);
       }
-      mma_commit(&bar_o);
+      mma_commit_w(&bar_kv_empty[st]);
+      if (more) advance2();
+      if (++st == kStages) st = 0;
     }
-  } else {
-    // ------------------------------------------------------------ softmax: (row, column half)
-    const int quarter = warp & 3;
-    const int half = warp >> 2;                 // S columns [64 half, 64 half + 64)
-    const int row = quarter * 32 + lane;        // TMEM lane = row of the query block
-    const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
-    const uint32_t o_addr = tm_o + lane_off + half * (D / 2);
+    mma_commit_w(&bar_o);
+  } else if (warp / 4 < nqb) {
+    // ------------------------------------------------------------ softmax: one thread per row
+    const int q = warp / 4;                     // query block
+    const int row = (warp & 3) * 32 + lane;     // TMEM lane = row of the query block
+    const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+    const uint32_t o_addr = tm_o(q) + lane_off;
     const float qs = (float)p.q_scales[h * p.M + u];
     const float sl = p.softmax_log2;
     const float tau = p.tau;
-    auto pair_sync = [&]() { named_bar_sync(1 + quarter, 64); };
     // Rows keep a reference max m_ref (log2 units); P~ = e4m3(448 * 2^(x - m_ref - tau)).
-    // No per-block max is taken: if both half-row sums of P~ stay <= 448 no
-    // element can have saturated and the block is accepted as computed.  The
-    // first block and blocks with a larger sum (a logit above m_ref + tau, or
-    // a false alarm) take the exact path, which lazily raises m_ref for the
+    // No per-block max is taken: if the row sum of P~ stays <= 448 no element
+    // can have saturated and the block is accepted as computed.  The first
+    // block and blocks with a larger sum (a logit above m_ref + tau, or a
+    // false alarm) take the exact path, which lazily raises m_ref for the
     // warp and rescales the TMEM accumulator (oracle.onepass_forward).
     float m_ref = 0.0f, l = 0.0f;
     int32_t kt = 0, b = 0;
@@ -427,49 +459,32 @@ __global__ void __launch_bounds__(kThreads, 1)
       const float kf = kt < kFacCap ? s_kfac[kt] : (float)__ldg(p.k_scales + h * p.M + __ldg(p.ids + kt0 + kt));
       const float c = (qs * kf) * sl;
       const bool tail = b == p.nb - 1;
-      const int ncol = tail ? p.n_tail : kBlk;
-      const int ncol_h = min(max(ncol - kHalfCols * half, 0), kHalfCols);
-      const bool pad8 = tail && p.tail_pad8 && ncol - kHalfCols * half <= kHalfCols;
-      const uint32_t s_addr = tm_s(j) + lane_off + half * kHalfCols;
+      const int ncol = tail ? p.n_tail : kKeys;
+      const bool pad8 = tail && p.tail_pad8;
+      const uint32_t s_addr = tm_s(q, j) + lane_off;
 #ifdef FPSA_TRACE
       const long long ts0 = clock64();
 #endif
-      mbar_wait(&bar_s_full[j & 1], (j >> 1) & 1);
+      mbar_wait(&bar_s_full[q][j & 1], (j >> 1) & 1);
 #ifdef FPSA_TRACE
       w_s += clock64() - ts0;
-#endif
-      tc_fence_after();
-      auto exchange_max = [&]() {
-        s_xchg[half][row] = half_max(s_addr, ncol_h, pad8);
-        pair_sync();
-        const float m = fmaxf(s_xchg[0][row], s_xchg[1][row]) * c;
-        pair_sync();  // the exchange slots are reused
-        return m;
-      };
-      if (j == 0) m_ref = exchange_max();
-      uint32_t w[kHalfCols / 4];
-      float lb;
-      bool redo = false;
-#ifdef FPSA_TRACE
       const long long tc0 = clock64();
 #endif
+      tc_fence_after();
+      if (j == 0) m_ref = block_max(s_addr, ncol, pad8) * c;
+      uint32_t w[kKeys / 4];
+      float lb;
+      bool redo = false;
 #pragma unroll 1
       for (;;) {  // one pass; a second one only after the exact path raised m_ref
-        lb = softmax_half(s_addr, ncol_h, pad8, c, kLog2_448 - m_ref - tau, w);
+        lb = softmax_block(s_addr, ncol, pad8, c, kLog2_448 - m_ref - tau, w);
 #ifdef FPSA_TRACE
         if (!redo) w_c += clock64() - tc0;
 #endif
-        if (redo) {
-          pair_sync();  // both halves re-read S(j) before P is written over it
-          break;
-        }
-        // half-row sums <= 448 bound every element; the pair agrees on the verdict
-        const uint32_t over = __any_sync(0xffffffffu, lb > 448.0f) ? 1u : 0u;
-        if (lane == 0) s_flag[j & 1][quarter][half] = over;
-        pair_sync();  // also: both halves have read S(j) before either writes P over it
-        if (!(s_flag[j & 1][quarter][0] | s_flag[j & 1][quarter][1])) break;
-        const float mb = exchange_max();
-        if (!__any_sync(0xffffffffu, mb > m_ref + tau)) break;  // identical in both warps of the pair
+        // a row sum <= 448 bounds every element
+        if (redo || !__any_sync(0xffffffffu, lb > 448.0f)) break;
+        const float mb = block_max(s_addr, ncol, pad8) * c;
+        if (!__any_sync(0xffffffffu, mb > m_ref + tau)) break;
         const float m_new = fmaxf(m_ref, mb);
         const float alpha = ex2(m_ref - m_new);
         l *= alpha;
@@ -477,10 +492,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 #ifdef FPSA_TRACE
         ++n_resc;
 #endif
-        if (j > 0) mbar_wait(&bar_pv, (j - 1) & 1);  // O complete up to block j-1
+        if (j > 0) mbar_wait(&bar_pv[q], (j - 1) & 1);  // O complete up to block j-1
         tc_fence_after();
 #pragma unroll 1
-        for (int cc = 0; cc < D / 2; cc += 32) {
+        for (int cc = 0; cc < D; cc += 32) {
           uint32_t o[32];
           tmem_ld32(o_addr + cc, o);
           tmem_wait_ld();
@@ -492,11 +507,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         redo = true;
       }
       l += lb;
-      tmem_st16(tm_s(j) + lane_off + half * (kHalfCols / 4), w);
+      tmem_st16(s_addr, w);
       tmem_wait_st();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&bar_p_ready[j & 1]);
+      if (lane == 0) mbar_arrive(&bar_p_ready[q][j & 1]);
       if (++b == p.nb) {
         b = 0;
         ++kt;
@@ -512,12 +527,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
 #endif
     // ------------------------------------------------------------ epilogue
-    s_xchg[half][row] = l;
     mbar_wait(&bar_o, 0);
     tc_fence_after();
-    pair_sync();
-    const float inv_l = 1.0f / (s_xchg[0][row] + s_xchg[1][row]);
-    const int32_t r = qb * kBlk + row;  // row inside the tile
+    const float inv_l = 1.0f / l;
+    const int32_t r = (qb0 + q) * kBlk + row;  // row inside the tile
     int64_t token;
     if (p.natural) {
       const int32_t ut = u / (p.dh * p.dw), uh = (u / p.dw) % p.dh, uw = u % p.dw;
@@ -526,11 +539,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     } else {
       token = (int64_t)u * p.tv + r;
     }
-#pragma unroll
-    for (int cc = 0; cc < D / 2; cc += 32) {
-      const int col = half * (D / 2) + cc;
+#pragma unroll 1
+    for (int col = 0; col < D; col += 32) {
       uint32_t o[32];
-      tmem_ld32(o_addr + cc, o);
+      tmem_ld32(o_addr + col, o);
       tmem_wait_ld();
       if (r < p.tv) {
         float f[32];
@@ -575,12 +587,12 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-int make_code_map(CUtensorMap* m, const uint8_t* base, int64_t rows, int32_t d) {
+int make_code_map(CUtensorMap* m, const uint8_t* base, int64_t rows, int32_t d, int32_t box_rows) {
   auto fn = encode_fn();
   if (!fn) return fail(FPSA_ECUDA, "cuTensorMapEncodeTiled unavailable");
   cuuint64_t dims[2] = {(cuuint64_t)d, (cuuint64_t)rows};
   cuuint64_t strides[1] = {(cuuint64_t)d};
-  cuuint32_t box[2] = {(cuuint32_t)d, (cuuint32_t)kBlk};
+  cuuint32_t box[2] = {(cuuint32_t)d, (cuuint32_t)box_rows};
   cuuint32_t es[2] = {1, 1};
   CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(base), dims, strides, box, es,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, d == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
@@ -634,9 +646,9 @@ extern "C" int fpsa_attn_fwd(const uint8_t* q_codes, const uint8_t* k_codes, con
   const int32_t M = td.t * td.h * td.w;
   const int64_t rows = (int64_t)heads * M * tile_pitch;
   CUtensorMap tq, tk, tvm;
-  if (int s = make_code_map(&tq, q_codes, rows, d)) return s;
-  if (int s = make_code_map(&tk, k_codes, rows, d)) return s;
-  if (int s = make_code_map(&tvm, v_codes, rows, d)) return s;
+  if (int s = make_code_map(&tq, q_codes, rows, d, kBlk)) return s;
+  if (int s = make_code_map(&tk, k_codes, rows, d, kKeys)) return s;
+  if (int s = make_code_map(&tvm, v_codes, rows, d, kKeys)) return s;
   AttnParams p{};
   p.q_scales = q_scales;
   p.k_scales = k_scales;
@@ -647,9 +659,10 @@ extern "C" int fpsa_attn_fwd(const uint8_t* q_codes, const uint8_t* k_codes, con
   p.M = M;
   p.tv = tv;
   p.pitch = tile_pitch;
-  p.nb = (tv + kBlk - 1) / kBlk;
+  p.nb = (tv + kKeys - 1) / kKeys;
+  p.nqb = (tv + kBlk - 1) / kBlk;
   {
-    const int32_t tail = tv - kBlk * ((tv - 1) / kBlk);  // valid keys of a tile's last 128-key block
+    const int32_t tail = tv - kKeys * (p.nb - 1);  // valid keys of a tile's last 64-key block
     p.n_tail = (tail + 15) / 16 * 16;
     p.tail_pad8 = p.n_tail != tail;
   }
