@@ -112,27 +112,38 @@ int fpsa_quantize_qkv(const void* q, const void* k, const void* v, int dtype, in
                       uint8_t* v_codes, double* q_scales, double* k_scales, double* v_scales, void* workspace,
                       int32_t* err_flag, void* stream);
 
-/* Work list for fpsa_attn_fwd: one entry per (head, query tile, pair of
- * 128-row query blocks), tiles with the most key tiles first within each
- * head.  Host-side; n_items returns the count, items (capacity `cap`, 3 int32
- * each: head, tile, first query block of the pair). */
+/* Work list for fpsa_attn_fwd: one entry per (head, query tile, 128-row
+ * query block), tiles with the most key tiles first within each head, the
+ * query blocks of a tile adjacent (they stream the same K/V from L2).
+ * Host-side; n_items returns the count, items (capacity `cap`, 3 int32 each:
+ * head, tile, query block). */
 int fpsa_attn_worklist(int32_t heads, fpsa_dims3 tile_dims, int32_t tile_volume, const int32_t* offs_host,
                        int32_t* items, int64_t cap, int64_t* n_items);
 
+/* Bytes of device workspace fpsa_attn_fwd needs for n_items work items (the
+ * list of items recomputed in exact mode, see below). */
+int fpsa_attn_workspace_bytes(int32_t n_items, int64_t* bytes);
+
 /* Sliding-tile sparse FP8 attention forward over quantised codes.
+ * Persistent kernel over the work list; items whose one-pass softmax may have
+ * saturated e4m3 (a logit more than tau_log2 above the first key block's row
+ * max) are recomputed by a second, exact-max launch on the same stream.
  *   q/k/v codes: tile-major padded (fpsa_quantize_*), tile_pitch a multiple of 128
  *   q/k scales: f64 [heads*M]; v scales f64 [heads*d]
  *   offs/ids: device CSR from fpsa_window_csr; items/n_items: device work list
  *   softmax_scale > 0 (the reference default is f32(1/sqrt(d)))
  *   out: element (token, head, c) at out + token*out_token_stride +
  *        head*out_head_stride + c, tokens in out_order, dtype out_dtype
- *   tau_log2: lazy-rescale headroom of the one-pass softmax (0..8)
+ *   tau_log2: headroom of the one-pass softmax above the first block's row max (0..8)
+ *   workspace: device, >= fpsa_attn_workspace_bytes(n_items); word 0 = number of
+ *              items recomputed exactly by this call (readable after the stream syncs)
  * Replaces fp8_sparse_forward / _engine (fp8sta/attention.py:91-149, :179-208). */
 int fpsa_attn_fwd(const uint8_t* q_codes, const uint8_t* k_codes, const uint8_t* v_codes, const double* q_scales,
                   const double* k_scales, const double* v_scales, int32_t heads, fpsa_dims3 grid, fpsa_dims3 tile,
                   int32_t d, int32_t tile_pitch, const int32_t* offs, const int32_t* ids, const int32_t* items,
                   int32_t n_items, float softmax_scale, int fmt, float tau_log2, void* out, int out_dtype,
-                  int64_t out_token_stride, int64_t out_head_stride, int out_order, void* stream);
+                  int64_t out_token_stride, int64_t out_head_stride, int out_order, void* workspace,
+                  int64_t workspace_bytes, void* stream);
 
 #ifdef __cplusplus
 }

@@ -334,7 +334,7 @@ def sparse_forward_f32(q, k, v, tv, offs, ids, softmax_scale=None):
 
 def _poly_columns(block: int = 128) -> np.ndarray:
     """Columns of a key block whose exp2 the GPU kernel evaluates with its polynomial:
-    odd groups of 4 inside each 64-column half (fpsa_attn.cu kPolyGroup)."""
+    odd groups of 4 (fpsa_attn.cu softmax_unit, groups with bit 2 of the column set)."""
     c = np.arange(block)
     return ((c % 64) // 4) % 2 == 1
 
@@ -348,15 +348,19 @@ def _exp2_poly(x: np.ndarray) -> np.ndarray:
     return np.ldexp(y, j.astype(np.int64))
 
 
-def onepass_forward(codes: dict, tv, offs, ids, fmt: Fmt = E4M3, softmax_scale=None, block=64, tau=0.0,
-                    poly=False):
-    """Emulation of the GPU kernel's one-pass schedule (NOT the reference semantics).
+def onepass_forward(codes: dict, tv, offs, ids, fmt: Fmt = E4M3, softmax_scale=None, block=128, tau=0.0,
+                    poly=False, return_redo=False):
+    """Emulation of the GPU kernel's schedule (NOT the reference semantics).
 
-    Keys are visited per key tile in `block`-key blocks (the last block of a
-    tile is shorter); the running row max m is updated per block, the unnormalised
-    weights 448*exp(x - m) are rounded to E4M3 before the PV product, the
-    denominator sums the unrounded weights.  Used to check the CUDA kernel
-    tightly; the reference-facing check is against ``fp8_sparse_forward``.
+    Work item = 128 query rows of a tile.  Keys are visited per key tile in
+    `block`-key blocks (the last block of a tile is shorter).  The reference
+    max m of a row is the max of its first key block; the unnormalised weights
+    448 * 2^(x - m - tau) are rounded to E4M3 before the PV product and the
+    denominator sums the unrounded weights.  If any 64-column half-row sum of
+    an item exceeds 448 (possible saturation), the item is recomputed with the
+    exact row max and tau = 0 (the kernel's redo launch).  Used to check the
+    CUDA kernel tightly; the reference-facing check is against
+    ``fp8_sparse_forward``.
     """
     qv = decode(codes["q_codes"], fmt).astype(np.float64)
     kv = decode(codes["k_codes"], fmt).astype(np.float64)
@@ -365,45 +369,48 @@ def onepass_forward(codes: dict, tv, offs, ids, fmt: Fmt = E4M3, softmax_scale=N
     L, d = qv.shape
     M = L // tv
     scale = float(_softmax_scale(d, softmax_scale))
-    log2e = 1.0 / math.log(2.0)
+    sl = float(np.float32(scale / math.log(2.0)))
     out = np.empty((L, d), dtype=np.float64)
+    redo = []
+    pc_all = _poly_columns(block)
     for u in range(M):
-        qrows = qv[u * tv:(u + 1) * tv]
-        m = np.full(tv, -np.inf)
-        lsum = np.zeros(tv)
-        acc = np.zeros((tv, d))
-        for vt in ids[offs[u]:offs[u + 1]]:
-            c = float(np.float32(np.float32(qs[u]) * np.float32(ks[vt]) * np.float32(scale * log2e)))
-            for b0 in range(0, tv, block):
-                b1 = min(b0 + block, tv)
-                kb = kv[vt * tv + b0: vt * tv + b1]
-                vb = vv[vt * tv + b0: vt * tv + b1]
-                s = (qrows @ kb.T) * c
-                mb = s.max(axis=1)
-                if not np.isfinite(m).any():
-                    m_new = mb
-                elif tau > 0.0:
-                    # lazy rescale per 32-row warp: the kernel keeps the reference
-                    # max unless some row of the warp exceeds it by more than tau
-                    m_new = m.copy()
-                    for w0 in range(0, tv, 32):
-                        sl = slice(w0, min(w0 + 32, tv))
-                        if np.any(mb[sl] > m[sl] + tau):
-                            m_new[sl] = np.maximum(m[sl], mb[sl])
-                else:
-                    m_new = np.maximum(m, mb)
-                alpha = np.where(np.isfinite(m), np.exp2(m - m_new), 0.0)
-                xe = s - m_new[:, None] + (math.log2(448.0) - tau)
-                p = np.exp2(xe)
-                if poly:
-                    pc = _poly_columns(block)[: s.shape[1]]
-                    p[:, pc] = _exp2_poly(xe[:, pc])
-                lsum = lsum * alpha + p.sum(axis=1)
-                pq = grid_round(p.astype(np.float32), E4M3).astype(np.float64)
-                acc = acc * alpha[:, None] + pq @ vb
-                m = m_new
-        out[u * tv:(u + 1) * tv] = acc / lsum[:, None] * vs[None, :]
-    return out.astype(np.float32)
+        for r0 in range(0, tv, 128):
+            rows = slice(u * tv + r0, u * tv + min(r0 + 128, tv))
+            qrows = qv[rows]
+            blocks = []
+            for vt in ids[offs[u]:offs[u + 1]]:
+                c = float(np.float32(np.float32(np.float32(qs[u]) * np.float32(ks[vt])) * np.float32(sl)))
+                for b0 in range(0, tv, block):
+                    b1 = min(b0 + block, tv)
+                    blocks.append((c, vt * tv + b0, vt * tv + b1))
+
+            def run(m, t):
+                lsum = np.zeros(qrows.shape[0])
+                acc = np.zeros((qrows.shape[0], d))
+                over = False
+                for c, k0, k1 in blocks:
+                    x = (qrows @ kv[k0:k1].T) * c
+                    xe = x - m[:, None] + (math.log2(448.0) - t)
+                    p = np.exp2(xe)
+                    if poly:
+                        pc = pc_all[: x.shape[1]]
+                        p[:, pc] = _exp2_poly(xe[:, pc])
+                    for h0 in range(0, x.shape[1], 64):
+                        over |= bool(np.any(p[:, h0:h0 + 64].sum(axis=1) > 448.0))
+                    lsum += p.sum(axis=1)
+                    pq = grid_round(p.astype(np.float32), E4M3).astype(np.float64)
+                    acc += pq @ vv[k0:k1]
+                return acc / lsum[:, None] * vs[None, :], over
+
+            c0, k0, k1 = blocks[0]
+            o, over = run((qrows @ kv[k0:k1].T).max(axis=1) * c0, tau)
+            if over:
+                m = np.max([((qrows @ kv[a:b].T) * c).max(axis=1) for c, a, b in blocks], axis=0)
+                o, _ = run(m, 0.0)
+                redo.append((u, r0 // 128))
+            out[rows] = o
+    res = out.astype(np.float32)
+    return (res, redo) if return_redo else res
 
 
 # --------------------------------------------------------------------------

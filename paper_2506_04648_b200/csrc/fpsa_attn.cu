@@ -3,34 +3,40 @@
 // Replaces fp8sta.attention.fp8_sparse_forward / _engine
 // (/root/reference/pkg/src/fp8sta/attention.py:91-149, :179-208).
 //
-// One CTA = (head h, query tile u, two 128-row query blocks of u).  The key
-// sequence of u is the concatenation of its admissible key tiles in
-// ascending id order (sparsity.py:63-67, the reference's reduction order),
-// each key tile cut into 64-key blocks; a tile's last block has
-// n_tail = tv - 64 (nb - 1) keys (rounded up to 16), so no padding key of a
-// 240-token tile is multiplied or exponentiated.  Per key block j and query
-// block q:
+// Persistent kernel: one CTA per SM walks a list of work items, one item =
+// (head h, query tile u, one 128-row query block of u).  The key sequence of
+// u is the concatenation of its admissible key tiles in ascending id order
+// (sparsity.py:63-67, the reference's reduction order), each key tile cut
+// into 128-key blocks; a tile's last block has n_tail = tv - 128 (nb - 1)
+// keys (rounded up to 16), so no padding key of a 240-token tile is
+// multiplied or exponentiated.  Per key block j:
 //
-//   S(q,j) = Q_q K_j^T               tcgen05.mma kind::f8f6f4 M128 N64, A/B from
-//                                    smem, fp32 accumulator in TMEM buffer (q, j % 2)
-//   x      = S * (sq[u] * sk[v] * softmax_scale * log2 e)     per-tile factors
-//   m      = reference row max, raised lazily (only when a block overflows the
-//            e4m3 range above it)
-//   P~     = e4m3(448 * 2^-tau * 2^(x - m))   re-quantised per key block,
-//            written back to TMEM over S(q,j) (4 codes per column)
-//   O_q   += P~ V_j                  tcgen05.mma, A = P~ from TMEM, B = V from
+//   S(j)  = Q K_j^T                  tcgen05.mma kind::f8f6f4 M128 N128, A/B from
+//                                    smem, fp32 accumulator in TMEM buffer j % 2
+//   x     = S * (sq[u] * sk[v] * softmax_scale * log2 e)     per-tile factors
+//   m     = row max of the first key block (fixed for the item)
+//   P~    = e4m3(448 * 2^-tau * 2^(x - m))   re-quantised per key block,
+//           written back to TMEM over S(j) (4 codes per column)
+//   O    += P~ V_j                    tcgen05.mma, A = P~ from TMEM, B = V from
 //                                    smem (MN-major, V stored [keys][d])
-//   l      += sum of the unrounded P~ (fp32)
+//   l    += sum of the unrounded P~ (fp32)
 // and finally out = O * v_scale[c] / l.
 //
-// TMEM (512 columns): O_0, O_1 (128 each), S(0, even/odd), S(1, even/odd)
-// (64 each).  With S double-buffered, QK(q, j+1) runs while the softmax
-// works on S(q, j), and the MMA issue order PV(q, j), QK(q, j+2) never makes
-// the softmax wait on its own P.
+// Overflow: a thread whose half-row sum of P~ exceeds 448 may have hit the
+// e4m3 saturation (a logit more than tau above m).  Its item is appended to
+// a redo list and recomputed by a second launch of the same kernel in exact
+// mode: a first pass over the keys takes the exact row max, a second pass
+// uses it with tau = 0.
 //
-// Warp roles (320 threads): warps 0-3 own the 128 rows (TMEM lanes) of query
-// block 0, warps 4-7 those of query block 1, one thread per row; warp 8 is
-// the TMA producer (and TMEM allocator), warp 9 the MMA issuer.
+// TMEM: O (D columns), S(even) at column 128, S(odd) at 256.  With S
+// double-buffered, QK(j+1) runs while the softmax works on S(j), and the MMA
+// issue order PV(j), QK(j+2) never makes the softmax wait on its own P.
+//
+// Warp roles (320 threads): warps w and w+4 (w < 4) own TMEM lane quarter w
+// (rows 32w..32w+31), warp w the S columns 0-63, warp w+4 the columns
+// 64-127; each writes the P~ of its 64 keys into the first 16 columns of its
+// own half, so the halves never wait for each other.  Warp 8 is the TMA
+// producer (and TMEM allocator), warp 9 the MMA issuer.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -54,12 +60,12 @@ constexpr int kTmaWarp = kSoftmaxWarps;
 constexpr int kMmaWarp = kSoftmaxWarps + 1;
 constexpr int kThreads = (kSoftmaxWarps + 2) * 32;
 
-constexpr int kStages = 8;    // K/V ring depth (64-key blocks)
-constexpr int kBlk = 128;     // rows per query block
-constexpr int kKeys = 64;     // keys per key block = S columns per softmax thread
-constexpr int kFacCap = 2048;  // key-tile scale factors cached in shared memory per CTA
+constexpr int kStages = 4;     // K/V ring depth (128-key blocks)
+constexpr int kBlk = 128;      // rows per query block = keys per key block
+constexpr int kHalf = 64;      // S columns per softmax thread
 constexpr float kLog2_448 = 8.807354922057604f;
 constexpr uint32_t kNegInf = 0xFF800000u;
+constexpr int kRedoHeader = 4;  // int32 words before the redo items in the workspace
 
 struct AttnParams {
   const double* q_scales;
@@ -67,9 +73,12 @@ struct AttnParams {
   const double* v_scales;
   const int32_t* offs;
   const int32_t* ids;
-  const int32_t* items;
-  int32_t M, tv, pitch, nb, nqb;  // nb: 64-key blocks per tile; nqb: 128-row query blocks per tile
-  int32_t n_tail;     // S columns of the last key block of a tile (tv - 64 (nb-1), rounded up to 16)
+  const int32_t* items;  // (head, tile, query block) triples
+  int32_t n_items;
+  int32_t* redo;         // [0]: count, [kRedoHeader..]: triples of items to recompute exactly
+  int32_t exact;         // 1: this launch recomputes the redo list with the exact row max
+  int32_t M, tv, pitch, nb;  // nb: 128-key blocks per tile
+  int32_t n_tail;     // S columns of the last key block of a tile (tv - 128 (nb-1), rounded up to 16)
   int32_t tail_pad8;  // 1 if the last 8 of those columns are zero padding (tv % 16 == 8)
   float softmax_log2;  // f32(softmax_scale * log2 e)
   float tau;
@@ -81,12 +90,11 @@ struct AttnParams {
 
 template <int D>
 struct Smem {
-  static constexpr int kQTile = kBlk * D;   // bytes of one 128-row fp8 query block
-  static constexpr int kKTile = kKeys * D;  // bytes of one 64-key fp8 K or V block
-  static constexpr int kQ = 0;
-  static constexpr int kK = 2 * kQTile;
-  static constexpr int kV = kK + kStages * kKTile;
-  static constexpr int kBytes = kV + kStages * kKTile;
+  static constexpr int kTile = kBlk * D;  // bytes of one 128-row fp8 tile
+  static constexpr int kQ = 0;            // two query-block buffers (next item prefetched)
+  static constexpr int kK = 2 * kTile;
+  static constexpr int kV = kK + kStages * kTile;
+  static constexpr int kBytes = kV + kStages * kTile;
   static constexpr uint32_t kSBO = 8 * D;  // 8 rows of D bytes
 };
 
@@ -225,10 +233,10 @@ __device__ __forceinline__ void softmax_chunk(uint32_t* s, int ncol, bool pad8, 
   else w[8 * C + 4] = w[8 * C + 5] = w[8 * C + 6] = w[8 * C + 7] = 0u;
 }
 
-// One row of one key block: 64 S columns streamed from TMEM in two 32-column
-// chunks (the second tcgen05.ld is in flight while the first chunk is
-// processed), ncol (multiple of 16, 16..64) valid.  P words of absent
-// columns are zero.  Returns the row sum of the unrounded weights.
+// One half row of one key block: 64 S columns streamed from TMEM in two
+// 32-column chunks (the second tcgen05.ld is in flight while the first chunk
+// is processed), ncol (multiple of 16, 0..64) valid.  P words of absent
+// columns are zero.  Returns the half-row sum of the unrounded weights.
 __device__ __forceinline__ float softmax_block(uint32_t s_addr, int ncol, bool pad8, float c, float boff, uint32_t* w) {
   const f2 cc = bcast(c), bb = bcast(boff);
   const float cs = c * (1.0f / 256.0f), bs = (boff + 126.0f) * (1.0f / 256.0f);
@@ -246,11 +254,11 @@ __device__ __forceinline__ float softmax_block(uint32_t s_addr, int ncol, bool p
   return t.x + t.y;
 }
 
-// Max of the first ncol (16..64) raw S values of a row.
+// Max of the first ncol (0..64) raw S values of a half row (-inf if none).
 __device__ __forceinline__ float block_max(uint32_t s_addr, int ncol, bool pad8) {
   float m0 = -INFINITY, m1 = -INFINITY;
 #pragma unroll
-  for (int base = 0; base < kKeys; base += 32) {
+  for (int base = 0; base < kHalf; base += 32) {
     if (base < ncol) {
       uint32_t s[32];
       tmem_ld32(s_addr + base, s);
@@ -270,8 +278,9 @@ __device__ __forceinline__ float block_max(uint32_t s_addr, int ncol, bool pad8)
 
 #ifdef FPSA_TRACE
 // Debug builds only: counters accumulated over all CTAs.
-//   [0] softmax: cycles waiting for S   [1] softmax: loop cycles   [2] softmax: first-pass compute
-//   [3] MMA: cycles waiting for P~      [5] rescales   [6] steps   [7] MMA: cycles waiting for K/V
+//   [0] softmax: cycles waiting for S   [1] softmax: step-loop cycles   [2] softmax: first-pass compute
+//   [3] MMA: cycles waiting for P~      [5] redo items                  [6] softmax warp-steps
+//   [7] MMA: cycles waiting for K/V
 __device__ unsigned long long g_trace[8];
 #endif
 
@@ -282,58 +291,47 @@ __global__ void __launch_bounds__(kThreads, 1)
   using S = Smem<D>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  __shared__ uint64_t bar_q, bar_o;
+  __shared__ uint64_t bar_q[2], bar_qfree[2];  // query-block buffer (item parity): loaded / no longer read
+  __shared__ uint64_t bar_o, bar_ofree;        // O complete for the item / epilogue has read O
   __shared__ uint64_t bar_kv_full[kStages], bar_kv_empty[kStages];
-  __shared__ uint64_t bar_s_full[2][2];   // [query block][S buffer]
-  __shared__ uint64_t bar_p_ready[2][2];  // [query block][step parity]: a block's warps may run one step apart
-  __shared__ uint64_t bar_pv[2];          // [query block]: PV(q, j) complete
+  __shared__ uint64_t bar_s_full[2], bar_p_ready[2];  // by S buffer / step parity
   __shared__ uint32_t s_tmem;
-  __shared__ float s_vscale[D];
-  __shared__ float s_kfac[kFacCap];
+  __shared__ float s_xchg[2][kBlk];  // [half][row] pair exchange
+  __shared__ uint32_t s_ovf[2];      // per item parity: some row overflowed
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int32_t h = p.items[3 * blockIdx.x + 0];
-  const int32_t u = p.items[3 * blockIdx.x + 1];
-  const int32_t qb0 = p.items[3 * blockIdx.x + 2];
-  const int nqb = min(2, p.nqb - qb0);
-  const int32_t kt0 = p.offs[u];
-  const int32_t n_kt = p.offs[u + 1] - kt0;
-  const int32_t n_kv = n_kt * p.nb;
+  const int32_t* items = p.exact ? p.redo + kRedoHeader : p.items;
+  const int32_t count = p.exact ? *reinterpret_cast<volatile int32_t*>(p.redo) : p.n_items;
+  if ((int32_t)blockIdx.x >= count) return;
 
   if (threadIdx.x == 0) {
-    mbar_init(&bar_q, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&bar_q[i], 1);
+      mbar_init(&bar_qfree[i], 1);
+      mbar_init(&bar_s_full[i], 1);
+      mbar_init(&bar_p_ready[i], kSoftmaxWarps);  // one arrival per softmax warp
+    }
     mbar_init(&bar_o, 1);
+    mbar_init(&bar_ofree, kSoftmaxWarps);
     for (int i = 0; i < kStages; ++i) {
       mbar_init(&bar_kv_full[i], 1);
       mbar_init(&bar_kv_empty[i], 1);
     }
-    for (int q = 0; q < 2; ++q) {
-      mbar_init(&bar_s_full[q][0], 1);
-      mbar_init(&bar_s_full[q][1], 1);
-      mbar_init(&bar_p_ready[q][0], 4);  // one arrival per softmax warp of the block
-      mbar_init(&bar_p_ready[q][1], 4);
-      mbar_init(&bar_pv[q], 1);
-    }
+    s_ovf[0] = s_ovf[1] = 0;
     fence_barrier_init();
   }
   if (warp == kTmaWarp) {
     tmem_alloc(&s_tmem, 512);
     tmem_relinquish();
   }
-  if (warp == kMmaWarp) {
-    // per-CTA tables: V channel factors and the k-scale of every in-window key tile
-    for (int i = lane; i < D; i += 32) s_vscale[i] = (float)p.v_scales[(int64_t)h * D + i];
-    for (int i = lane; i < min(n_kt, kFacCap); i += 32)
-      s_kfac[i] = (float)p.k_scales[(int64_t)h * p.M + p.ids[kt0 + i]];
-  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = s_tmem;
-  // O_q at column 128 q; S(q, buffer) at 256 + 128 q + 64 buffer (computed, not
-  // indexed: a local array would live in memory)
-  auto tm_o = [tmem](int q) { return tmem + 128u * (uint32_t)q; };
-  auto tm_s = [tmem](int q, int32_t j) { return tmem + 256u + 128u * (uint32_t)q + 64u * (uint32_t)(j & 1); };
+  const uint32_t tm_o = tmem;
+  // S buffers at columns 128 and 256 (computed, not indexed: a local array would live in memory)
+  auto tm_s = [tmem](uint32_t g) { return tmem + 128u + 128u * (g & 1u); };
+  const float tau = p.exact ? 0.0f : p.tau;
 
   if (warp == kTmaWarp) {
     // ------------------------------------------------------------ TMA producer (warp-uniform, one elected lane issues)
@@ -343,230 +341,265 @@ __global__ void __launch_bounds__(kThreads, 1)
       prefetch_tmap(&tm_v);
     }
     __syncwarp();
-    const int32_t qrow = (h * p.M + u) * p.pitch + qb0 * kBlk;
-    mbar_arrive_expect_tx_w(&bar_q, nqb * S::kQTile);
-    for (int q = 0; q < nqb; ++q) tma_load_2d_w(smem + S::kQ + q * S::kQTile, &tm_q, 0, qrow + q * kBlk, &bar_q);
-    int32_t kt = 0, b = 0, st = 0;
-    uint32_t ph = 0;
-    int32_t krow = (h * p.M + p.ids[kt0]) * p.pitch;
-    for (int32_t j = 0; j < n_kv; ++j) {
-      if (j >= kStages) mbar_wait(&bar_kv_empty[st], ph ^ 1);
-      mbar_arrive_expect_tx_w(&bar_kv_full[st], 2 * S::kKTile);
-      tma_load_2d_w(smem + S::kK + st * S::kKTile, &tm_k, 0, krow + b * kKeys, &bar_kv_full[st]);
-      tma_load_2d_w(smem + S::kV + st * S::kKTile, &tm_v, 0, krow + b * kKeys, &bar_kv_full[st]);
-      if (++b == p.nb) {
-        b = 0;
-        if (++kt < n_kt) krow = (h * p.M + __ldg(p.ids + kt0 + kt)) * p.pitch;
-      }
-      if (++st == kStages) {
-        st = 0;
-        ph ^= 1;
+    uint32_t g = 0;  // K/V block counter over all items of this CTA
+    int32_t iter = 0;
+    for (int32_t it = blockIdx.x; it < count; it += gridDim.x, ++iter) {
+      const int32_t h = items[3 * it], u = items[3 * it + 1], qb = items[3 * it + 2];
+      const int32_t kt0 = __ldg(p.offs + u), n_kt = __ldg(p.offs + u + 1) - kt0;
+      const int32_t n_kv = n_kt * p.nb, steps = p.exact ? 2 * n_kv : n_kv;
+      const int qbuf = iter & 1;
+      if (iter >= 2) mbar_wait(&bar_qfree[qbuf], ((iter >> 1) - 1) & 1);
+      mbar_arrive_expect_tx_w(&bar_q[qbuf], S::kTile);
+      tma_load_2d_w(smem + S::kQ + qbuf * S::kTile, &tm_q, 0, (h * p.M + u) * p.pitch + qb * kBlk, &bar_q[qbuf]);
+      int32_t kt = 0, b = 0;
+      int32_t krow = (h * p.M + __ldg(p.ids + kt0)) * p.pitch;
+      for (int32_t s = 0; s < steps; ++s, ++g) {
+        const uint32_t st = g % kStages;
+        if (g >= (uint32_t)kStages) mbar_wait(&bar_kv_empty[st], ((g / kStages) - 1) & 1);
+        mbar_arrive_expect_tx_w(&bar_kv_full[st], 2 * S::kTile);
+        tma_load_2d_w(smem + S::kK + st * S::kTile, &tm_k, 0, krow + b * kBlk, &bar_kv_full[st]);
+        tma_load_2d_w(smem + S::kV + st * S::kTile, &tm_v, 0, krow + b * kBlk, &bar_kv_full[st]);
+        if (++b == p.nb) {
+          b = 0;
+          if (++kt == n_kt) kt = 0;  // exact mode streams the keys twice
+          krow = (h * p.M + __ldg(p.ids + kt0 + kt)) * p.pitch;
+        }
       }
     }
   } else if (warp == kMmaWarp) {
     // ------------------------------------------------------------ MMA issuer (warp-uniform, one elected lane issues)
-    constexpr uint32_t idesc_qk = idesc_f8(128, kKeys, FMT, FMT, 0);
+    constexpr uint32_t idesc_qk = idesc_f8(128, 128, FMT, FMT, 0);
     const uint32_t idesc_qk_tail = idesc_f8(128, (uint32_t)p.n_tail, FMT, FMT, 0);
     constexpr uint32_t idesc_pv = idesc_f8(128, D, FPSA_E4M3, FMT, 1);
-    const uint32_t sq = smem_u32(smem + S::kQ);
     const uint32_t sk0 = smem_u32(smem + S::kK), sv0 = smem_u32(smem + S::kV);
-    mbar_wait(&bar_q, 0);
-    tc_fence_after();
-    // S(q, j) = Q_q K_j^T into TMEM buffer (q, j % 2); (st, b) = stage and in-tile block of j
-    auto issue_qk = [&](int q, int32_t j, int st, bool tail) {
-      const uint32_t sk = sk0 + st * S::kKTile;
-      const uint32_t idq = tail ? idesc_qk_tail : idesc_qk;
-      const uint32_t sqq = sq + q * S::kQTile;
-#pragma unroll
-      for (int k = 0; k < D / 32; ++k)
-        mma_f8_ss_w(tm_s(q, j), desc_kmajor<D>(sqq + 32 * k), desc_kmajor<D>(sk + 32 * k), idq, k > 0 ? 1u : 0u);
-      mma_commit_w(&bar_s_full[q][j & 1]);
-    };
-    // (st2, b2): stage / in-tile block of step j + 2, with the full-barrier phase
-    int st2 = 0, b2 = 0;
-    uint32_t ph2 = 0;
-    auto advance2 = [&]() {
-      if (++b2 == p.nb) b2 = 0;
-      if (++st2 == kStages) {
-        st2 = 0;
-        ph2 ^= 1;
-      }
-    };
-    for (int32_t j = 0; j < min(n_kv, 2); ++j) {
-      mbar_wait(&bar_kv_full[st2], ph2);
+    uint32_t g = 0;
+    int32_t iter = 0;
+    for (int32_t it = blockIdx.x; it < count; it += gridDim.x, ++iter) {
+      const int32_t u = items[3 * it + 1];
+      const int32_t n_kt = __ldg(p.offs + u + 1) - __ldg(p.offs + u);
+      const int32_t n_kv = n_kt * p.nb, steps = p.exact ? 2 * n_kv : n_kv;
+      const int32_t pv0 = p.exact ? n_kv : 0;  // first step with a PV
+      const int qbuf = iter & 1;
+      const uint32_t sq = smem_u32(smem + S::kQ + qbuf * S::kTile);
+      mbar_wait(&bar_q[qbuf], (iter >> 1) & 1);
       tc_fence_after();
-      for (int q = 0; q < nqb; ++q) issue_qk(q, j, st2, b2 == p.nb - 1);
-      advance2();
-    }
-    int st = 0;
-    for (int32_t j = 0; j < n_kv; ++j) {
-      const uint32_t sv = sv0 + st * S::kKTile;
-      const bool more = j + 2 < n_kv;
-      if (more) {
-#ifdef FPSA_TRACE
-        const long long tk0 = clock64();
-#endif
-        mbar_wait(&bar_kv_full[st2], ph2);
-#ifdef FPSA_TRACE
-        if (lane == 0) atomicAdd(&g_trace[7], (unsigned long long)(clock64() - tk0));
-#endif
+      // S(step) = Q K^T into TMEM buffer g % 2; b = in-tile block of the step
+      auto issue_qk = [&](uint32_t gg, int32_t b) {
+        const uint32_t st = gg % kStages;
+        mbar_wait(&bar_kv_full[st], (gg / kStages) & 1);
         tc_fence_after();
+        const uint32_t sk = sk0 + st * S::kTile;
+        const uint32_t idq = b == p.nb - 1 ? idesc_qk_tail : idesc_qk;
+#pragma unroll
+        for (int k = 0; k < D / 32; ++k)
+          mma_f8_ss_w(tm_s(gg), desc_kmajor<D>(sq + 32 * k), desc_kmajor<D>(sk + 32 * k), idq, k > 0 ? 1u : 0u);
+        mma_commit_w(&bar_s_full[gg & 1]);
+      };
+      int32_t b2 = 0;  // in-tile block of step s + 2
+      for (int32_t s = 0; s < min(steps, 2); ++s) {
+        issue_qk(g + s, b2);
+        if (++b2 == p.nb) b2 = 0;
       }
-      for (int q = 0; q < nqb; ++q) {
-        // O_q += P~(q, j) V_j once the softmax has written P~ over S(q, j)
+      if (steps <= 2) mma_commit_w(&bar_qfree[qbuf]);
+      for (int32_t s = 0; s < steps; ++s) {
+        const uint32_t gs = g + s;
+        const uint32_t st = gs % kStages;
 #ifdef FPSA_TRACE
         const long long tp0 = clock64();
 #endif
-        mbar_wait(&bar_p_ready[q][j & 1], (j >> 1) & 1);
+        mbar_wait(&bar_p_ready[gs & 1], (gs >> 1) & 1);
 #ifdef FPSA_TRACE
         if (lane == 0) atomicAdd(&g_trace[3], (unsigned long long)(clock64() - tp0));
 #endif
         tc_fence_after();
+        if (s >= pv0) {
+          // O += P~ V: P~ of keys 64c..64c+63 sits in the first 16 columns of S half c
+          if (s == pv0 && iter > 0) {
+            mbar_wait(&bar_ofree, (iter - 1) & 1);  // the previous item's epilogue has read O
+            tc_fence_after();
+          }
+          const uint32_t sv = sv0 + st * S::kTile;
 #pragma unroll
-        for (int k = 0; k < kKeys / 32; ++k)
-          mma_f8_ts_w(tm_o(q), tm_s(q, j) + 8 * k, desc_mnmajor<D>(sv + k * 32 * D), idesc_pv,
-                      (j > 0 || k > 0) ? 1u : 0u);
-        mma_commit_w(&bar_pv[q]);
-        if (more) issue_qk(q, j + 2, st2, b2 == p.nb - 1);
-      }
-      mma_commit_w(&bar_kv_empty[st]);
-      if (more) advance2();
-      if (++st == kStages) st = 0;
-    }
-    mma_commit_w(&bar_o);
-  } else if (warp / 4 < nqb) {
-    // ------------------------------------------------------------ softmax: one thread per row
-    const int q = warp / 4;                     // query block
-    const int row = (warp & 3) * 32 + lane;     // TMEM lane = row of the query block
-    const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
-    const uint32_t o_addr = tm_o(q) + lane_off;
-    const float qs = (float)p.q_scales[h * p.M + u];
-    const float sl = p.softmax_log2;
-    const float tau = p.tau;
-    // Rows keep a reference max m_ref (log2 units); P~ = e4m3(448 * 2^(x - m_ref - tau)).
-    // No per-block max is taken: if the row sum of P~ stays <= 448 no element
-    // can have saturated and the block is accepted as computed.  The first
-    // block and blocks with a larger sum (a logit above m_ref + tau, or a
-    // false alarm) take the exact path, which lazily raises m_ref for the
-    // warp and rescales the TMEM accumulator (oracle.onepass_forward).
-    float m_ref = 0.0f, l = 0.0f;
-    int32_t kt = 0, b = 0;
-#ifdef FPSA_TRACE
-    long long w_s = 0, w_c = 0, n_resc = 0;
-    const long long t_loop = clock64();
-#endif
-    for (int32_t j = 0; j < n_kv; ++j) {
-      const float kf = kt < kFacCap ? s_kfac[kt] : (float)__ldg(p.k_scales + h * p.M + __ldg(p.ids + kt0 + kt));
-      const float c = (qs * kf) * sl;
-      const bool tail = b == p.nb - 1;
-      const int ncol = tail ? p.n_tail : kKeys;
-      const bool pad8 = tail && p.tail_pad8;
-      const uint32_t s_addr = tm_s(q, j) + lane_off;
-#ifdef FPSA_TRACE
-      const long long ts0 = clock64();
-#endif
-      mbar_wait(&bar_s_full[q][j & 1], (j >> 1) & 1);
-#ifdef FPSA_TRACE
-      w_s += clock64() - ts0;
-      const long long tc0 = clock64();
-#endif
-      tc_fence_after();
-      if (j == 0) m_ref = block_max(s_addr, ncol, pad8) * c;
-      uint32_t w[kKeys / 4];
-      float lb;
-      bool redo = false;
-#pragma unroll 1
-      for (;;) {  // one pass; a second one only after the exact path raised m_ref
-        lb = softmax_block(s_addr, ncol, pad8, c, kLog2_448 - m_ref - tau, w);
-#ifdef FPSA_TRACE
-        if (!redo) w_c += clock64() - tc0;
-#endif
-        // a row sum <= 448 bounds every element
-        if (redo || !__any_sync(0xffffffffu, lb > 448.0f)) break;
-        const float mb = block_max(s_addr, ncol, pad8) * c;
-        if (!__any_sync(0xffffffffu, mb > m_ref + tau)) break;
-        const float m_new = fmaxf(m_ref, mb);
-        const float alpha = ex2(m_ref - m_new);
-        l *= alpha;
-        m_ref = m_new;
-#ifdef FPSA_TRACE
-        ++n_resc;
-#endif
-        if (j > 0) mbar_wait(&bar_pv[q], (j - 1) & 1);  // O complete up to block j-1
-        tc_fence_after();
-#pragma unroll 1
-        for (int cc = 0; cc < D; cc += 32) {
-          uint32_t o[32];
-          tmem_ld32(o_addr + cc, o);
-          tmem_wait_ld();
-#pragma unroll
-          for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
-          tmem_st32(o_addr + cc, o);
+          for (int k = 0; k < kBlk / 32; ++k)
+            mma_f8_ts_w(tm_o, tm_s(gs) + 64 * (k >> 1) + 8 * (k & 1), desc_mnmajor<D>(sv + k * 32 * D), idesc_pv,
+                        (s > pv0 || k > 0) ? 1u : 0u);
         }
-        tmem_wait_st();
-        redo = true;
+        mma_commit_w(&bar_kv_empty[st]);
+        if (s + 2 < steps) {
+          issue_qk(gs + 2, b2);
+          if (++b2 == p.nb) b2 = 0;
+          if (s + 3 == steps) mma_commit_w(&bar_qfree[qbuf]);
+        }
       }
-      l += lb;
-      tmem_st16(s_addr, w);
-      tmem_wait_st();
+      mma_commit_w(&bar_o);
+      g += steps;
+    }
+  } else {
+    // ------------------------------------------------------------ softmax: (row, column half)
+    const int quarter = warp & 3;
+    const int half = warp >> 2;              // S columns [64 half, 64 half + 64)
+    const int row = quarter * 32 + lane;     // TMEM lane = row of the query block
+    const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+    const uint32_t o_addr = tm_o + lane_off + half * (D / 2);
+    const float sl = p.softmax_log2;
+    auto pair_sync = [&]() { named_bar_sync(1 + quarter, 64); };
+    auto pair_max = [&](float m) {  // max over both halves of the row
+      s_xchg[half][row] = m;
+      pair_sync();
+      const float r = fmaxf(s_xchg[0][row], s_xchg[1][row]);
+      pair_sync();  // the exchange slots are reused
+      return r;
+    };
+    uint32_t g = 0;
+    int32_t iter = 0;
+#ifdef FPSA_TRACE
+    long long w_s = 0, w_c = 0, t_loop = 0;
+    int64_t n_steps = 0;
+#endif
+    for (int32_t it = blockIdx.x; it < count; it += gridDim.x, ++iter) {
+      const int32_t h = items[3 * it], u = items[3 * it + 1], qb = items[3 * it + 2];
+      const int32_t kt0 = __ldg(p.offs + u), n_kt = __ldg(p.offs + u + 1) - kt0;
+      const int32_t n_kv = n_kt * p.nb;
+      const float qs = (float)__ldg(p.q_scales + h * p.M + u);
+      const double* ks = p.k_scales + (int64_t)h * p.M;
+      // c(kt) = f32(f32(sq) * f32(sk)) * f32(scale log2 e), the oracle's factor order
+      auto factor = [&](int32_t kt) { return (qs * (float)__ldg(ks + __ldg(p.ids + kt0 + kt))) * sl; };
+      float m_ref = 0.0f, l = 0.0f;
+      bool ovf = false;
+#ifdef FPSA_TRACE
+      const long long tl0 = clock64();
+#endif
+      for (int pass = p.exact ? 0 : 1; pass < 2; ++pass) {
+        // pass 0 (exact mode only): running max of x over all key blocks
+        float m_acc = -INFINITY;
+        int32_t kt = 0, b = 0;
+        float c = factor(0);
+        for (int32_t j = 0; j < n_kv; ++j, ++g) {
+          const bool tail = b == p.nb - 1;
+          const int ncol = (tail ? p.n_tail : kBlk) - kHalf * half;
+          const int ncol_h = min(max(ncol, 0), kHalf);
+          const bool pad8 = tail && p.tail_pad8 && ncol > 0 && ncol <= kHalf;
+          const uint32_t s_addr = tm_s(g) + lane_off + half * kHalf;
+          // next step's factor, loaded while this step waits / computes
+          const int32_t kt_next = tail ? kt + 1 : kt;
+          const float c_next = (tail && kt_next < n_kt) ? factor(kt_next) : c;
+#ifdef FPSA_TRACE
+          const long long ts0 = clock64();
+#endif
+          mbar_wait(&bar_s_full[g & 1], (g >> 1) & 1);
+#ifdef FPSA_TRACE
+          w_s += clock64() - ts0;
+          const long long tc0 = clock64();
+          ++n_steps;
+#endif
+          tc_fence_after();
+          if (pass == 0) {
+            m_acc = fmaxf(m_acc, block_max(s_addr, ncol_h, pad8) * c);
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&bar_p_ready[g & 1]);  // S consumed
+          } else {
+            if (j == 0 && !p.exact) m_ref = pair_max(block_max(s_addr, ncol_h, pad8)) * c;
+            uint32_t w[kHalf / 4];
+            const float lb = softmax_block(s_addr, ncol_h, pad8, c, kLog2_448 - m_ref - tau, w);
+#ifdef FPSA_TRACE
+            w_c += clock64() - tc0;
+#endif
+            ovf |= lb > 448.0f;  // a half-row sum <= 448 bounds every element
+            l += lb;
+            tmem_st16(s_addr, w);
+            tmem_wait_st();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&bar_p_ready[g & 1]);
+          }
+          c = c_next;
+          if (tail) {
+            b = 0;
+            ++kt;
+          } else {
+            ++b;
+          }
+        }
+        if (pass == 0) m_ref = pair_max(m_acc);
+      }
+#ifdef FPSA_TRACE
+      t_loop += clock64() - tl0;
+#endif
+      // ---------------------------------------------------------- epilogue
+      s_xchg[half][row] = l;
+      mbar_wait(&bar_o, iter & 1);
+      tc_fence_after();
+      pair_sync();
+      const float inv_l = 1.0f / (s_xchg[0][row] + s_xchg[1][row]);
+      const int32_t r = qb * kBlk + row;  // row inside the tile
+      int64_t token;
+      if (p.natural) {
+        const int32_t ut = u / (p.dh * p.dw), uh = (u / p.dw) % p.dh, uw = u % p.dw;
+        const int32_t lt = r / (p.sh * p.sw), lh = (r / p.sw) % p.sh, lw = r % p.sw;
+        token = ((int64_t)(ut * p.st + lt) * p.gh + (uh * p.sh + lh)) * p.gw + (uw * p.sw + lw);
+      } else {
+        token = (int64_t)u * p.tv + r;
+      }
+      const double* vs = p.v_scales + (int64_t)h * D;
+#pragma unroll
+      for (int cc = 0; cc < D / 2; cc += 32) {
+        const int col = half * (D / 2) + cc;
+        uint32_t o[32];
+        tmem_ld32(o_addr + cc, o);
+        tmem_wait_ld();
+        if (r < p.tv) {
+          float f[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) f[i] = __uint_as_float(o[i]) * inv_l * (float)__ldg(vs + col + i);
+          if constexpr (OUT == FPSA_F32) {
+            float4* dst =
+                reinterpret_cast<float4*>(static_cast<float*>(p.out) + token * p.out_ts + h * p.out_hs + col);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) dst[i] = make_float4(f[4 * i], f[4 * i + 1], f[4 * i + 2], f[4 * i + 3]);
+          } else {
+            uint4* dst = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.out) + token * p.out_ts +
+                                                  h * p.out_hs + col);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              uint32_t wv[4];
+#pragma unroll
+              for (int k2 = 0; k2 < 4; ++k2) {
+                __nv_bfloat162 b2 = __floats2bfloat162_rn(f[8 * i + 2 * k2], f[8 * i + 2 * k2 + 1]);
+                wv[k2] = *reinterpret_cast<uint32_t*>(&b2);
+              }
+              dst[i] = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+            }
+          }
+        }
+      }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&bar_p_ready[q][j & 1]);
-      if (++b == p.nb) {
-        b = 0;
-        ++kt;
+      if (lane == 0) mbar_arrive(&bar_ofree);
+      if (!p.exact) {
+        // items with a possibly saturated P~ are recomputed exactly by the redo launch
+        if (__any_sync(0xffffffffu, ovf) && lane == 0) atomicOr(&s_ovf[iter & 1], 1u);
+        named_bar_sync(5, kSoftmaxWarps * 32);
+        if (threadIdx.x == 0 && s_ovf[iter & 1]) {
+          s_ovf[iter & 1] = 0;
+          const int32_t slot = atomicAdd(p.redo, 1);
+          p.redo[kRedoHeader + 3 * slot] = h;
+          p.redo[kRedoHeader + 3 * slot + 1] = u;
+          p.redo[kRedoHeader + 3 * slot + 2] = qb;
+#ifdef FPSA_TRACE
+          atomicAdd(&g_trace[5], 1ull);
+#endif
+        }
       }
     }
 #ifdef FPSA_TRACE
     if (lane == 0) {
       atomicAdd(&g_trace[0], (unsigned long long)w_s);
-      atomicAdd(&g_trace[1], (unsigned long long)(clock64() - t_loop));
+      atomicAdd(&g_trace[1], (unsigned long long)t_loop);
       atomicAdd(&g_trace[2], (unsigned long long)w_c);
-      atomicAdd(&g_trace[5], (unsigned long long)n_resc);
-      atomicAdd(&g_trace[6], (unsigned long long)n_kv);
+      atomicAdd(&g_trace[6], (unsigned long long)n_steps);
     }
 #endif
-    // ------------------------------------------------------------ epilogue
-    mbar_wait(&bar_o, 0);
-    tc_fence_after();
-    const float inv_l = 1.0f / l;
-    const int32_t r = (qb0 + q) * kBlk + row;  // row inside the tile
-    int64_t token;
-    if (p.natural) {
-      const int32_t ut = u / (p.dh * p.dw), uh = (u / p.dw) % p.dh, uw = u % p.dw;
-      const int32_t lt = r / (p.sh * p.sw), lh = (r / p.sw) % p.sh, lw = r % p.sw;
-      token = ((int64_t)(ut * p.st + lt) * p.gh + (uh * p.sh + lh)) * p.gw + (uw * p.sw + lw);
-    } else {
-      token = (int64_t)u * p.tv + r;
-    }
-#pragma unroll 1
-    for (int col = 0; col < D; col += 32) {
-      uint32_t o[32];
-      tmem_ld32(o_addr + col, o);
-      tmem_wait_ld();
-      if (r < p.tv) {
-        float f[32];
-#pragma unroll
-        for (int i = 0; i < 32; ++i) f[i] = __uint_as_float(o[i]) * inv_l * s_vscale[col + i];
-        if constexpr (OUT == FPSA_F32) {
-          float4* dst = reinterpret_cast<float4*>(static_cast<float*>(p.out) + token * p.out_ts + h * p.out_hs + col);
-#pragma unroll
-          for (int i = 0; i < 8; ++i) dst[i] = make_float4(f[4 * i], f[4 * i + 1], f[4 * i + 2], f[4 * i + 3]);
-        } else {
-          uint4* dst = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.out) + token * p.out_ts + h * p.out_hs + col);
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            uint32_t wv[4];
-#pragma unroll
-            for (int k2 = 0; k2 < 4; ++k2) {
-              __nv_bfloat162 b2 = __floats2bfloat162_rn(f[8 * i + 2 * k2], f[8 * i + 2 * k2 + 1]);
-              wv[k2] = *reinterpret_cast<uint32_t*>(&b2);
-            }
-            dst[i] = make_uint4(wv[0], wv[1], wv[2], wv[3]);
-          }
-        }
-      }
-    }
   }
   tc_fence_before();
   __syncthreads();
@@ -601,9 +634,21 @@ int make_code_map(CUtensorMap* m, const uint8_t* base, int64_t rows, int32_t d, 
   return FPSA_OK;
 }
 
+int g_num_sms = 0;
+int num_sms() {
+  if (!g_num_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_num_sms <= 0) g_num_sms = 148;
+  }
+  return g_num_sms;
+}
+
+// Main persistent launch, then the exact-mode launch over the redo list
+// (its CTAs exit at once when the list is empty).
 template <int D, int FMT, int OUT>
-int launch(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, const AttnParams& p, int32_t n_items,
-           cudaStream_t st) {
+int launch(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, AttnParams p, cudaStream_t st) {
   auto kern = fpsa_attn_kernel<D, FMT, OUT>;
   constexpr int smem = Smem<D>::kBytes + 1024;
   static bool configured = false;
@@ -612,7 +657,12 @@ int launch(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, 
       return fail(FPSA_ECUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(cudaGetLastError()));
     configured = true;
   }
-  kern<<<n_items, kThreads, smem, st>>>(tq, tk, tv, p);
+  if (cudaMemsetAsync(p.redo, 0, sizeof(int32_t), st) != cudaSuccess)
+    return fail(FPSA_ECUDA, std::string("fpsa_attn_fwd redo reset: ") + cudaGetErrorString(cudaGetLastError()));
+  p.exact = 0;
+  kern<<<std::min(p.n_items, num_sms()), kThreads, smem, st>>>(tq, tk, tv, p);
+  p.exact = 1;
+  kern<<<std::min(p.n_items, num_sms()), kThreads, smem, st>>>(tq, tk, tv, p);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(FPSA_ECUDA, std::string("fpsa_attn_fwd launch: ") + cudaGetErrorString(e));
   return FPSA_OK;
@@ -628,7 +678,8 @@ extern "C" int fpsa_attn_fwd(const uint8_t* q_codes, const uint8_t* k_codes, con
                              fpsa_dims3 grid, fpsa_dims3 tile, int32_t d, int32_t tile_pitch, const int32_t* offs,
                              const int32_t* ids, const int32_t* items, int32_t n_items, float softmax_scale, int fmt,
                              float tau_log2, void* out, int out_dtype, int64_t out_token_stride,
-                             int64_t out_head_stride, int out_order, void* stream) {
+                             int64_t out_head_stride, int out_order, void* workspace, int64_t workspace_bytes,
+                             void* stream) {
   clear_error();
   fpsa_dims3 td;
   if (int s = fpsa_tile_grid(grid, tile, &td)) return s;
@@ -643,12 +694,16 @@ extern "C" int fpsa_attn_fwd(const uint8_t* q_codes, const uint8_t* k_codes, con
   if (out_dtype != FPSA_F32 && out_dtype != FPSA_BF16) return fail(FPSA_EUNSUPPORTED, "out dtype must be f32 or bf16");
   if (!(tau_log2 >= 0.0f && tau_log2 <= 8.0f)) return fail(FPSA_EINVAL, "tau_log2 must be in [0, 8]");
   if (heads < 1 || n_items < 1) return fail(FPSA_EINVAL, "empty problem");
+  int64_t need = 0;
+  fpsa_attn_workspace_bytes(n_items, &need);
+  if (!workspace || workspace_bytes < need)
+    return fail(FPSA_ECAPACITY, "attention workspace must hold " + std::to_string(need) + " bytes");
   const int32_t M = td.t * td.h * td.w;
   const int64_t rows = (int64_t)heads * M * tile_pitch;
   CUtensorMap tq, tk, tvm;
   if (int s = make_code_map(&tq, q_codes, rows, d, kBlk)) return s;
-  if (int s = make_code_map(&tk, k_codes, rows, d, kKeys)) return s;
-  if (int s = make_code_map(&tvm, v_codes, rows, d, kKeys)) return s;
+  if (int s = make_code_map(&tk, k_codes, rows, d, kBlk)) return s;
+  if (int s = make_code_map(&tvm, v_codes, rows, d, kBlk)) return s;
   AttnParams p{};
   p.q_scales = q_scales;
   p.k_scales = k_scales;
@@ -656,13 +711,14 @@ extern "C" int fpsa_attn_fwd(const uint8_t* q_codes, const uint8_t* k_codes, con
   p.offs = offs;
   p.ids = ids;
   p.items = items;
+  p.n_items = n_items;
+  p.redo = static_cast<int32_t*>(workspace);
   p.M = M;
   p.tv = tv;
   p.pitch = tile_pitch;
-  p.nb = (tv + kKeys - 1) / kKeys;
-  p.nqb = (tv + kBlk - 1) / kBlk;
+  p.nb = (tv + kBlk - 1) / kBlk;
   {
-    const int32_t tail = tv - kKeys * (p.nb - 1);  // valid keys of a tile's last 64-key block
+    const int32_t tail = tv - kBlk * (p.nb - 1);  // valid keys of a tile's last 128-key block
     p.n_tail = (tail + 15) / 16 * 16;
     p.tail_pad8 = p.n_tail != tail;
   }
@@ -680,7 +736,7 @@ extern "C" int fpsa_attn_fwd(const uint8_t* q_codes, const uint8_t* k_codes, con
   p.dh = td.h;
   p.dw = td.w;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-#define FPSA_LAUNCH(D_, F_, O_) return launch<D_, F_, O_>(tq, tk, tvm, p, n_items, st)
+#define FPSA_LAUNCH(D_, F_, O_) return launch<D_, F_, O_>(tq, tk, tvm, p, st)
   if (d == 128) {
     if (fmt == FPSA_E4M3) {
       if (out_dtype == FPSA_F32) FPSA_LAUNCH(128, FPSA_E4M3, FPSA_F32); else FPSA_LAUNCH(128, FPSA_E4M3, FPSA_BF16);
@@ -695,6 +751,12 @@ extern "C" int fpsa_attn_fwd(const uint8_t* q_codes, const uint8_t* k_codes, con
     }
   }
 #undef FPSA_LAUNCH
+}
+
+extern "C" int fpsa_attn_workspace_bytes(int32_t n_items, int64_t* bytes) {
+  if (!bytes || n_items < 0) return fail(FPSA_EINVAL, "bad arguments");
+  *bytes = (int64_t)(kRedoHeader + 3 * (int64_t)n_items) * (int64_t)sizeof(int32_t);
+  return FPSA_OK;
 }
 
 #ifdef FPSA_TRACE

@@ -166,24 +166,23 @@ extern "C" int fpsa_attn_worklist(int32_t heads, fpsa_dims3 td, int32_t tile_vol
   if (heads < 1 || tile_volume < 1 || !offs) return fail(FPSA_EINVAL, "bad worklist arguments");
   const int32_t M = td.t * td.h * td.w;
   const int32_t nqb = (tile_volume + 127) / 128;  // 128-row query blocks per tile
-  const int32_t pairs = (nqb + 1) / 2;             // a CTA owns two of them
   // Longest-processing-time first inside each head; heads in order so that the
   // K/V codes of the heads in flight stay L2 resident.
   std::vector<int32_t> order(M);
   std::iota(order.begin(), order.end(), 0);
   std::stable_sort(order.begin(), order.end(),
                    [&](int32_t a, int32_t b) { return offs[a + 1] - offs[a] > offs[b + 1] - offs[b]; });
-  const int64_t total = (int64_t)heads * M * pairs;
+  const int64_t total = (int64_t)heads * M * nqb;
   if (n_items) *n_items = total;
   if (!items) return FPSA_OK;
   if (cap < total) return fail(FPSA_ECAPACITY, "work list capacity too small");
   int64_t pos = 0;
   for (int32_t h = 0; h < heads; ++h)
     for (int32_t i = 0; i < M; ++i)
-      for (int32_t pr = 0; pr < pairs; ++pr) {
+      for (int32_t qb = 0; qb < nqb; ++qb) {
         items[3 * pos + 0] = h;
         items[3 * pos + 1] = order[i];
-        items[3 * pos + 2] = 2 * pr;
+        items[3 * pos + 2] = qb;
         ++pos;
       }
   return FPSA_OK;

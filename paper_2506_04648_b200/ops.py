@@ -50,7 +50,7 @@ def tile_pitch(tile_volume: int) -> int:
 
 
 def worklist(heads: int, mask: BlockMask, tile_volume: int) -> np.ndarray:
-    """(head, query tile, first q-block) items, longest first within each head."""
+    """(head, query tile, query block) items, longest first within each head."""
     L = _lib.lib()
     n = ctypes.c_int64(0)
     td = _lib.dims3(mask.tile_grid_dims)
@@ -104,6 +104,9 @@ class FpsaPlan:
         self.k_scales = torch.empty_like(self.q_scales)
         self.v_scales = torch.empty(self.heads * self.d, dtype=torch.float64, device=dev)
         self.workspace = torch.empty(self.heads * self.d, dtype=torch.int32, device=dev)
+        need = ctypes.c_int64(0)
+        _lib.check(_lib.lib().fpsa_attn_workspace_bytes(self.n_items, ctypes.byref(need)))
+        self.attn_ws = torch.zeros(-(-need.value // 4), dtype=torch.int32, device=dev)
         self.err = torch.zeros(1, dtype=torch.int32, device=dev)
 
     # ------------------------------------------------------------------ accounting
@@ -177,7 +180,12 @@ class FpsaPlan:
             _ptr(self.q_codes), _ptr(self.k_codes), _ptr(self.v_codes), _ptr(self.q_scales), _ptr(self.k_scales),
             _ptr(self.v_scales), self.heads, _lib.dims3(self.grid), _lib.dims3(self.tile), self.d, self.pitch,
             _ptr(self.offs), _ptr(self.ids), _ptr(self.items), self.n_items, float(scale), self.fmt.abi_id,
-            self.tau, _ptr(out), odt, ts, hs, _lib.ORDER_TILE if tile_order else _lib.ORDER_NATURAL, st))
+            self.tau, _ptr(out), odt, ts, hs, _lib.ORDER_TILE if tile_order else _lib.ORDER_NATURAL,
+            _ptr(self.attn_ws), self.attn_ws.numel() * 4, st))
+
+    def redo_count(self) -> int:
+        """Work items the last attention call recomputed in exact mode (synchronises)."""
+        return int(self.attn_ws[0].item())
 
     def check_finite(self) -> None:
         """Raise ValueError if a quantised input held a non-finite value (synchronises)."""

@@ -211,13 +211,19 @@ def test_worklist_covers_every_query_block(fpsa):
         H = 3
         items = worklist(H, m, tv).reshape(-1, 3)
         nqb = -(-tv // 128)
-        seen = {(h, u, b) for h, u, b0 in items.tolist() for b in (b0, b0 + 1) if b < nqb}
-        assert len(seen) == H * m.tiles_total * nqb
+        seen = {(h, u, b) for h, u, b in items.tolist()}
+        assert len(seen) == len(items) == H * m.tiles_total * nqb
         counts = np.diff(m.offsets)
         # longest first within each head
         for h in range(H):
             c = counts[items[items[:, 0] == h][:, 1]]
             assert np.all(c[:-1] >= c[1:])
+
+
+def test_attn_workspace_size(lib):
+    n = ctypes.c_int64(0)
+    assert lib.fpsa_attn_workspace_bytes(25200, ctypes.byref(n)) == 0
+    assert n.value >= 4 * (3 * 25200 + 1)
 
 
 def test_flops_accounting(fpsa):
@@ -241,6 +247,6 @@ def test_device_calls_reject_bad_arguments_before_cuda(lib):
                               None, None, None, None)
     assert st in (_lib.FPSA_EINVAL, _lib.FPSA_EINDIVISIBLE)
     st = lib.fpsa_attn_fwd(None, None, None, None, None, None, 1, g, t, 64, 128, None, None, None, 1, 0.125, 0, 8.0,
-                           None, _lib.F32, 64, 0, _lib.ORDER_TILE, None)
+                           None, _lib.F32, 64, 0, _lib.ORDER_TILE, None, 0, None)
     assert st == _lib.FPSA_EINVAL
     assert lib.fpsa_last_error()

@@ -21,9 +21,8 @@ t = list(buf)
 n_sm_warps = t[6]  # sum over softmax warps of n_kv
 print(f"attention {s.elapsed_time(e):.3f} ms (traced build)")
 n = max(1, t[6])  # softmax warp-steps
-ctas = n / 8 / max(1, t[6] / 8 / max(1, plan.n_items)) if False else None
 print(f"softmax per warp-step: loop {t[1]/n:.0f} clk, wait-for-S {t[0]/n:.0f}, first-pass compute {t[2]/n:.0f}, "
-      f"rest (sync/flags/store/setup) {(t[1]-t[0]-t[2])/n:.0f}")
+      f"rest (setup/store/arrive) {(t[1]-t[0]-t[2])/n:.0f}")
 steps = n / 8
 print(f"MMA per step: wait P {t[3]/steps:.0f} clk, wait K/V {t[7]/steps:.0f} clk")
-print(f"rescales per (warp, block): {t[5]/max(1,t[6]):.4f}")
+print(f"redo items: {t[5]} of {plan.n_items}")
