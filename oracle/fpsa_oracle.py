@@ -356,8 +356,9 @@ def onepass_forward(codes: dict, tv, offs, ids, fmt: Fmt = E4M3, softmax_scale=N
     `block`-key blocks (the last block of a tile is shorter).  The reference
     max m of a row is the max of its first key block; the unnormalised weights
     448 * 2^(x - m - tau) are rounded to E4M3 before the PV product and the
-    denominator sums the unrounded weights.  If any 64-column half-row sum of
-    an item exceeds 448 (possible saturation), the item is recomputed with the
+    denominator is the sum of the rounded weights (the kernel accumulates it
+    with the PV MMA through a column of ones).  If any rounded weight of an
+    item reaches 448 (possible saturation), the item is recomputed with the
     exact row max and tau = 0 (the kernel's redo launch).  Used to check the
     CUDA kernel tightly; the reference-facing check is against
     ``fp8_sparse_forward``.
@@ -395,10 +396,9 @@ def onepass_forward(codes: dict, tv, offs, ids, fmt: Fmt = E4M3, softmax_scale=N
                     if poly:
                         pc = pc_all[: x.shape[1]]
                         p[:, pc] = _exp2_poly(xe[:, pc])
-                    for h0 in range(0, x.shape[1], 64):
-                        over |= bool(np.any(p[:, h0:h0 + 64].sum(axis=1) > 448.0))
-                    lsum += p.sum(axis=1)
                     pq = grid_round(p.astype(np.float32), E4M3).astype(np.float64)
+                    over |= bool(np.any(pq >= 448.0))
+                    lsum += pq.sum(axis=1)
                     acc += pq @ vv[k0:k1]
                 return acc / lsum[:, None] * vs[None, :], over
 

@@ -17,18 +17,19 @@
 //   m     = row max of the first key block (fixed for the item)
 //   P~    = e4m3(448 * 2^-tau * 2^(x - m))   re-quantised per key block,
 //           written back to TMEM over S(j) (4 codes per column)
-//   O    += P~ V_j                    tcgen05.mma, A = P~ from TMEM, B = V from
-//                                    smem (MN-major, V stored [keys][d])
-//   l    += sum of the unrounded P~ (fp32)
+//   [O|l] += P~ [V_j | 1]             tcgen05.mma N = D + 16, A = P~ from TMEM,
+//                                    B = V from smem (MN-major, V stored [keys][d])
+//                                    plus a constant "ones" MN atom: the extra
+//                                    columns accumulate the row sum l of P~
 // and finally out = O * v_scale[c] / l.
 //
-// Overflow: a thread whose half-row sum of P~ exceeds 448 may have hit the
-// e4m3 saturation (a logit more than tau above m).  Its item is appended to
-// a redo list and recomputed by a second launch of the same kernel in exact
-// mode: a first pass over the keys takes the exact row max, a second pass
-// uses it with tau = 0.
+// Overflow: a P~ code equal to 0x7E (448) may be a saturated weight (a logit
+// more than tau above m).  Its item is appended to a redo list and recomputed
+// by a second launch of the same kernel in exact mode: a first pass over the
+// keys takes the exact row max, a second pass uses it with tau = 0
+// (DESIGN.md).
 //
-// TMEM: O (D columns), S(even) at column 128, S(odd) at 256.  With S
+// TMEM: [O|l] (D + 16 columns), S(even) at column 256, S(odd) at 384.  With S
 // double-buffered, QK(j+1) runs while the softmax works on S(j), and the MMA
 // issue order PV(j), QK(j+2) never makes the softmax wait on its own P.
 //
@@ -49,6 +50,7 @@
 #include "../../include/fpsa.h"
 #include "fpsa_internal.h"
 #include "sm100.cuh"
+#include "softmax.cuh"
 
 namespace fpsa {
 namespace {
@@ -62,9 +64,7 @@ constexpr int kThreads = (kSoftmaxWarps + 2) * 32;
 
 constexpr int kStages = 4;     // K/V ring depth (128-key blocks)
 constexpr int kBlk = 128;      // rows per query block = keys per key block
-constexpr int kHalf = 64;      // S columns per softmax thread
 constexpr float kLog2_448 = 8.807354922057604f;
-constexpr uint32_t kNegInf = 0xFF800000u;
 constexpr int kRedoHeader = 4;  // int32 words before the redo items in the workspace
 
 struct AttnParams {
@@ -94,7 +94,8 @@ struct Smem {
   static constexpr int kQ = 0;            // two query-block buffers (next item prefetched)
   static constexpr int kK = 2 * kTile;
   static constexpr int kV = kK + kStages * kTile;
-  static constexpr int kBytes = kV + kStages * kTile;
+  static constexpr int kOnes = kV + kStages * kTile;  // 128 rows x D bytes of e4m3 1.0 (the "ones" MN atom)
+  static constexpr int kBytes = kOnes + kTile;
   static constexpr uint32_t kSBO = 8 * D;  // 8 rows of D bytes
 };
 
@@ -104,6 +105,14 @@ __device__ __forceinline__ uint64_t desc_kmajor(uint32_t addr) {
   if constexpr (D == 64) d = (d & ~((uint64_t)7 << 61)) | ((uint64_t)4 << 61);  // SWIZZLE_64B
   return d;
 }
+// MN-major V block whose second MN atom (columns D..D+15 of B) is the ones
+// region at byte offset `lbo` (leading byte offset field, 16-byte units).
+template <int D>
+__device__ __forceinline__ uint64_t desc_mnmajor_ones(uint32_t addr, uint32_t lbo) {
+  uint64_t d = smem_desc_sw128(addr, lbo, Smem<D>::kSBO);
+  if constexpr (D == 64) d = (d & ~((uint64_t)7 << 61)) | ((uint64_t)4 << 61);
+  return d;
+}
 template <int D>
 __device__ __forceinline__ uint64_t desc_mnmajor(uint32_t addr) {
   uint64_t d = smem_desc_sw128(addr, 16384, Smem<D>::kSBO);
@@ -111,177 +120,11 @@ __device__ __forceinline__ uint64_t desc_mnmajor(uint32_t addr) {
   return d;
 }
 
-__device__ __forceinline__ float ex2(float x) {
-  float y;
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
-__device__ __forceinline__ float max3(float a, float b, float c) {
-  float y;
-  asm("max.f32 %0, %1, %2, %3;" : "=f"(y) : "f"(a), "f"(b), "f"(c));
-  return y;
-}
-// ---- packed f32x2 arithmetic (sm_100 FFMA2 / FADD2): two lanes per instruction
-struct f2 {
-  float x, y;
-};
-__device__ __forceinline__ f2 fma2(f2 a, f2 b, f2 c) {
-  f2 d;
-  asm("{\n\t.reg .b64 ra, rb, rc, rd;\n\t"
-      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\tmov.b64 rc, {%6, %7};\n\t"
-      "fma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;\n\t}"
-      : "=f"(d.x), "=f"(d.y)
-      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
-  return d;
-}
-__device__ __forceinline__ f2 add2(f2 a, f2 b) {
-  f2 d;
-  asm("{\n\t.reg .b64 ra, rb, rd;\n\t"
-      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
-      "add.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;\n\t}"
-      : "=f"(d.x), "=f"(d.y)
-      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
-  return d;
-}
-__device__ __forceinline__ f2 bcast(float v) { return f2{v, v}; }
-
-// Scalar saturating FMA (there is no .sat for f32x2): clamps to [0, 1].
-__device__ __forceinline__ float fma_sat(float a, float b, float c) {
-  float d;
-  asm("fma.rn.sat.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
-  return d;
-}
-
-// 2^x on the FMA pipe for a pair, x = s * c + noff given as
-//   xs = sat(s * c/256 + (noff + 126)/256)  in [0, 1]   (x clamped to [-126, 130],
-//   so the exponent add below never leaves the float range)
-// Cody-Waite split x = j + f (j = round(x), |f| <= 1/2) with the rounding
-// done by the magic-number add, then a degree-2 minimax for 2^f (rel. err
-// 1.7e-3, far below the 2^-4 step of the e4m3 P it feeds) and j added to the
-// exponent field.  Used for half of the columns so that MUFU ex2 (16/clk/SM)
-// is not the only exp source.
-__device__ __forceinline__ f2 exp2_poly_sat(f2 xs) {
-  constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23
-  const f2 t = fma2(xs, bcast(256.0f), bcast(kMagic - 126.0f));  // kMagic + round(x), x = 256 xs - 126
-  const f2 g = add2(t, bcast(126.0f - kMagic));                   // round(x) + 126
-  const f2 f = fma2(xs, bcast(256.0f), f2{-g.x, -g.y});           // x - round(x)
-  f2 y = fma2(bcast(0.238487109541893f), f, bcast(0.703453540802002f));
-  y = fma2(y, f, bcast(1.0004364252090454f));
-  return f2{__uint_as_float(__float_as_uint(y.x) + (__float_as_uint(t.x) << 23)),
-            __uint_as_float(__float_as_uint(y.y) + (__float_as_uint(t.y) << 23))};
-}
-
-// Four e4m3 codes in one word (a.x lowest byte).
-__device__ __forceinline__ uint32_t e4m3x4(f2 a, f2 b) {
-  uint32_t r;
-  asm("{\n\t.reg .b16 lo, hi;\n\t"
-      "cvt.rn.satfinite.e4m3x2.f32 lo, %2, %1;\n\t"
-      "cvt.rn.satfinite.e4m3x2.f32 hi, %4, %3;\n\t"
-      "mov.b32 %0, {lo, hi};\n\t}"
-      : "=r"(r)
-      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
-  return r;
-}
-
-// P~ for 16 S columns [16U, 16U + 16) of a thread's half row, read from the
-// 32-column chunk `s` that holds columns [32 (U/2), 32 (U/2) + 32): 4 groups
-// of 4 keys, the odd groups (columns with bit 2 set) on the FMA-pipe
-// polynomial, the even groups on MUFU ex2.  Writes 4 packed P words
-// w[4U..4U+3] and accumulates the unrounded weights into acc.
-template <int U>
-__device__ __forceinline__ void softmax_unit(const uint32_t* s, f2 cc, f2 bb, float cs, float bs, f2* acc,
-                                             uint32_t* w) {
-#pragma unroll
-  for (int g = 0; g < 4; ++g) {
-    const int c0 = 16 * (U & 1) + 4 * g;
-    const f2 a{__uint_as_float(s[c0]), __uint_as_float(s[c0 + 1])};
-    const f2 b{__uint_as_float(s[c0 + 2]), __uint_as_float(s[c0 + 3])};
-    f2 pa, pb;
-    if (g & 1) {
-      pa = exp2_poly_sat(f2{fma_sat(a.x, cs, bs), fma_sat(a.y, cs, bs)});
-      pb = exp2_poly_sat(f2{fma_sat(b.x, cs, bs), fma_sat(b.y, cs, bs)});
-    } else {
-      pa = fma2(a, cc, bb);
-      pb = fma2(b, cc, bb);
-      pa = f2{ex2(pa.x), ex2(pa.y)};
-      pb = f2{ex2(pb.x), ex2(pb.y)};
-    }
-    acc[g & 1] = add2(acc[g & 1], pa);
-    acc[2 + (g & 1)] = add2(acc[2 + (g & 1)], pb);
-    w[4 * U + g] = e4m3x4(pa, pb);
-  }
-}
-
-// The last 8 of the ncol valid columns are zero K rows (tv % 16 == 8): -inf
-// drops them from max, sum and P.  `s` holds columns [base, base + 32).
-__device__ __forceinline__ void mask_pad8(uint32_t* s, int base, int ncol) {
-#pragma unroll
-  for (int i = 8; i < 32; i += 16)
-    if (base + i + 8 == ncol) {
-#pragma unroll
-      for (int k = i; k < i + 8; ++k) s[k] = kNegInf;
-    }
-}
-
-template <int C>
-__device__ __forceinline__ void softmax_chunk(uint32_t* s, int ncol, bool pad8, f2 cc, f2 bb, float cs, float bs,
-                                              f2* acc, uint32_t* w) {
-  if (pad8) mask_pad8(s, 32 * C, ncol);
-  if (ncol > 32 * C) softmax_unit<2 * C>(s, cc, bb, cs, bs, acc, w);
-  else w[8 * C] = w[8 * C + 1] = w[8 * C + 2] = w[8 * C + 3] = 0u;
-  if (ncol > 32 * C + 16) softmax_unit<2 * C + 1>(s, cc, bb, cs, bs, acc, w);
-  else w[8 * C + 4] = w[8 * C + 5] = w[8 * C + 6] = w[8 * C + 7] = 0u;
-}
-
-// One half row of one key block: 64 S columns streamed from TMEM in two
-// 32-column chunks (the second tcgen05.ld is in flight while the first chunk
-// is processed), ncol (multiple of 16, 0..64) valid.  P words of absent
-// columns are zero.  Returns the half-row sum of the unrounded weights.
-__device__ __forceinline__ float softmax_block(uint32_t s_addr, int ncol, bool pad8, float c, float boff, uint32_t* w) {
-  const f2 cc = bcast(c), bb = bcast(boff);
-  const float cs = c * (1.0f / 256.0f), bs = (boff + 126.0f) * (1.0f / 256.0f);
-  f2 acc[4] = {bcast(0.f), bcast(0.f), bcast(0.f), bcast(0.f)};
-  uint32_t sa[32], sb[32];
-  if (ncol > 0) {
-    tmem_ld32(s_addr, sa);
-    tmem_wait_ld();
-  }
-  if (ncol > 32) tmem_ld32(s_addr + 32, sb);
-  softmax_chunk<0>(sa, ncol, pad8, cc, bb, cs, bs, acc, w);
-  if (ncol > 32) tmem_wait_ld();
-  softmax_chunk<1>(sb, ncol, pad8, cc, bb, cs, bs, acc, w);
-  const f2 t = add2(add2(acc[0], acc[1]), add2(acc[2], acc[3]));
-  return t.x + t.y;
-}
-
-// Max of the first ncol (0..64) raw S values of a half row (-inf if none).
-__device__ __forceinline__ float block_max(uint32_t s_addr, int ncol, bool pad8) {
-  float m0 = -INFINITY, m1 = -INFINITY;
-#pragma unroll
-  for (int base = 0; base < kHalf; base += 32) {
-    if (base < ncol) {
-      uint32_t s[32];
-      tmem_ld32(s_addr + base, s);
-      tmem_wait_ld();
-      if (pad8) mask_pad8(s, base, ncol);
-#pragma unroll
-      for (int i = 0; i < 32; i += 4) {
-        if (base + i < ncol) {
-          m0 = max3(m0, __uint_as_float(s[i]), __uint_as_float(s[i + 1]));
-          m1 = max3(m1, __uint_as_float(s[i + 2]), __uint_as_float(s[i + 3]));
-        }
-      }
-    }
-  }
-  return fmaxf(m0, m1);
-}
-
 #ifdef FPSA_TRACE
 // Debug builds only: counters accumulated over all CTAs.
 //   [0] softmax: cycles waiting for S   [1] softmax: step-loop cycles   [2] softmax: first-pass compute
 //   [3] MMA: cycles waiting for P~      [5] redo items                  [6] softmax warp-steps
-//   [7] MMA: cycles waiting for K/V
-__device__ unsigned long long g_trace[8];
+//   [4] softmax: S load (tcgen05.ld + wait) cycles   [7] MMA: cycles waiting for K/V
 #endif
 
 template <int D, int FMT, int OUT>
@@ -324,13 +167,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     tmem_alloc(&s_tmem, 512);
     tmem_relinquish();
   }
+  for (int i = threadIdx.x; i < S::kTile / 4; i += kThreads)  // 1.0 in V's format
+    reinterpret_cast<uint32_t*>(smem + S::kOnes)[i] = FMT == FPSA_E4M3 ? 0x38383838u : 0x3C3C3C3Cu;
+  fence_proxy_async_smem();  // generic-proxy writes read by the tensor core
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = s_tmem;
-  const uint32_t tm_o = tmem;
-  // S buffers at columns 128 and 256 (computed, not indexed: a local array would live in memory)
-  auto tm_s = [tmem](uint32_t g) { return tmem + 128u + 128u * (g & 1u); };
+  const uint32_t tm_o = tmem;  // O: columns 0..D-1, row sums of P~: D..D+15
+  // S buffers at columns 256 and 384 (computed, not indexed: a local array would live in memory)
+  auto tm_s = [tmem](uint32_t g) { return tmem + 256u + 128u * (g & 1u); };
   const float tau = p.exact ? 0.0f : p.tau;
 
   if (warp == kTmaWarp) {
@@ -370,8 +216,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ------------------------------------------------------------ MMA issuer (warp-uniform, one elected lane issues)
     constexpr uint32_t idesc_qk = idesc_f8(128, 128, FMT, FMT, 0);
     const uint32_t idesc_qk_tail = idesc_f8(128, (uint32_t)p.n_tail, FMT, FMT, 0);
-    constexpr uint32_t idesc_pv = idesc_f8(128, D, FPSA_E4M3, FMT, 1);
+    constexpr uint32_t idesc_pv = idesc_f8(128, D + 16, FPSA_E4M3, FMT, 1);
     const uint32_t sk0 = smem_u32(smem + S::kK), sv0 = smem_u32(smem + S::kV);
+    const uint32_t sones = smem_u32(smem + S::kOnes);
     uint32_t g = 0;
     int32_t iter = 0;
     for (int32_t it = blockIdx.x; it < count; it += gridDim.x, ++iter) {
@@ -407,13 +254,16 @@ __global__ void __launch_bounds__(kThreads, 1)
 #ifdef FPSA_TRACE
         const long long tp0 = clock64();
 #endif
+        FPSA_TL(9, 0, gs);
         mbar_wait(&bar_p_ready[gs & 1], (gs >> 1) & 1);
+        FPSA_TL(9, 1, gs);
 #ifdef FPSA_TRACE
         if (lane == 0) atomicAdd(&g_trace[3], (unsigned long long)(clock64() - tp0));
 #endif
         tc_fence_after();
         if (s >= pv0) {
-          // O += P~ V: P~ of keys 64c..64c+63 sits in the first 16 columns of S half c
+          // [O|l] += P~ [V|1]: P~ of keys 64c..64c+63 sits in the first 16 columns of S half c;
+          // the B descriptor's leading byte offset points from V at the ones atom
           if (s == pv0 && iter > 0) {
             mbar_wait(&bar_ofree, (iter - 1) & 1);  // the previous item's epilogue has read O
             tc_fence_after();
@@ -421,12 +271,14 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t sv = sv0 + st * S::kTile;
 #pragma unroll
           for (int k = 0; k < kBlk / 32; ++k)
-            mma_f8_ts_w(tm_o, tm_s(gs) + 64 * (k >> 1) + 8 * (k & 1), desc_mnmajor<D>(sv + k * 32 * D), idesc_pv,
-                        (s > pv0 || k > 0) ? 1u : 0u);
+            mma_f8_ts_w(tm_o, tm_s(gs) + 64 * (k >> 1) + 8 * (k & 1), desc_mnmajor_ones<D>(sv + k * 32 * D, sones - sv),
+                        idesc_pv, (s > pv0 || k > 0) ? 1u : 0u);
         }
         mma_commit_w(&bar_kv_empty[st]);
+        FPSA_TL(9, 2, gs);
         if (s + 2 < steps) {
           issue_qk(gs + 2, b2);
+          FPSA_TL(9, 3, gs);
           if (++b2 == p.nb) b2 = 0;
           if (s + 3 == steps) mma_commit_w(&bar_qfree[qbuf]);
         }
@@ -464,8 +316,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       const double* ks = p.k_scales + (int64_t)h * p.M;
       // c(kt) = f32(f32(sq) * f32(sk)) * f32(scale log2 e), the oracle's factor order
       auto factor = [&](int32_t kt) { return (qs * (float)__ldg(ks + __ldg(p.ids + kt0 + kt))) * sl; };
-      float m_ref = 0.0f, l = 0.0f;
-      bool ovf = false;
+      float m_ref = 0.0f;
+      uint32_t sat = 0u;
 #ifdef FPSA_TRACE
       const long long tl0 = clock64();
 #endif
@@ -486,7 +338,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 #ifdef FPSA_TRACE
           const long long ts0 = clock64();
 #endif
+          FPSA_TL(warp, 0, g);
           mbar_wait(&bar_s_full[g & 1], (g >> 1) & 1);
+          FPSA_TL(warp, 1, g);
 #ifdef FPSA_TRACE
           w_s += clock64() - ts0;
           const long long tc0 = clock64();
@@ -501,17 +355,17 @@ __global__ void __launch_bounds__(kThreads, 1)
           } else {
             if (j == 0 && !p.exact) m_ref = pair_max(block_max(s_addr, ncol_h, pad8)) * c;
             uint32_t w[kHalf / 4];
-            const float lb = softmax_block(s_addr, ncol_h, pad8, c, kLog2_448 - m_ref - tau, w);
+            sat |= softmax_block(s_addr, ncol_h, pad8, c, kLog2_448 - m_ref - tau, w);
 #ifdef FPSA_TRACE
             w_c += clock64() - tc0;
 #endif
-            ovf |= lb > 448.0f;  // a half-row sum <= 448 bounds every element
-            l += lb;
+            FPSA_TL(warp, 2, g);
             tmem_st16(s_addr, w);
             tmem_wait_st();
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&bar_p_ready[g & 1]);
+            FPSA_TL(warp, 3, g);
           }
           c = c_next;
           if (tail) {
@@ -527,11 +381,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       t_loop += clock64() - tl0;
 #endif
       // ---------------------------------------------------------- epilogue
-      s_xchg[half][row] = l;
       mbar_wait(&bar_o, iter & 1);
       tc_fence_after();
-      pair_sync();
-      const float inv_l = 1.0f / (s_xchg[0][row] + s_xchg[1][row]);
+      float inv_l;
+      {
+        uint32_t lw[16];
+        tmem_ld16(tm_o + lane_off + D, lw);  // row sum of P~ (the ones columns, all equal)
+        tmem_wait_ld();
+        inv_l = 1.0f / __uint_as_float(lw[0]);
+      }
       const int32_t r = qb * kBlk + row;  // row inside the tile
       int64_t token;
       if (p.natural) {
@@ -578,7 +436,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (lane == 0) mbar_arrive(&bar_ofree);
       if (!p.exact) {
         // items with a possibly saturated P~ are recomputed exactly by the redo launch
-        if (__any_sync(0xffffffffu, ovf) && lane == 0) atomicOr(&s_ovf[iter & 1], 1u);
+        if (__any_sync(0xffffffffu, sat != 0u) && lane == 0) atomicOr(&s_ovf[iter & 1], 1u);
         named_bar_sync(5, kSoftmaxWarps * 32);
         if (threadIdx.x == 0 && s_ovf[iter & 1]) {
           s_ovf[iter & 1] = 0;
@@ -760,6 +618,10 @@ extern "C" int fpsa_attn_workspace_bytes(int32_t n_items, int64_t* bytes) {
 }
 
 #ifdef FPSA_TRACE
+extern "C" int fpsa_trace_timeline(long long* out) {
+  cudaMemcpyFromSymbol(out, fpsa::g_tl, sizeof(fpsa::g_tl));
+  return (int)(sizeof(fpsa::g_tl) / sizeof(long long));
+}
 extern "C" int fpsa_trace_read(unsigned long long* out, int reset) {
   cudaMemcpyFromSymbol(out, fpsa::g_trace, sizeof(unsigned long long) * 8);
   if (reset) {

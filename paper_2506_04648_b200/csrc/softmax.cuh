@@ -1,0 +1,261 @@
+// Per-row softmax building blocks of the attention kernel (fpsa_attn.cu):
+// packed f32x2 arithmetic, the FMA-pipe exp2 polynomial, e4m3 packing, and
+// the 64-column half-row pass that turns S (TMEM) into P~ words.
+// Shared with tools/probes/softmax_rate.cu, which times them in isolation.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "sm100.cuh"
+
+namespace fpsa {
+namespace {
+
+using namespace sm100;
+
+constexpr int kHalf = 64;  // S columns per softmax thread
+
+#ifdef FPSA_TRACE
+__device__ unsigned long long g_trace[8];  // debug builds only, see fpsa_attn.cu
+// per-step timeline of CTA 0 (clock64): softmax warps 0..7 x 4 events, MMA warp 4 events
+constexpr int kTlSteps = 256;
+__device__ long long g_tl[kTlSteps][10][4];
+#define FPSA_TL(slot, ev, step)                                                        \
+  do {                                                                                 \
+    if (blockIdx.x == 0 && (threadIdx.x & 31) == 0 && (step) < kTlSteps)               \
+      g_tl[(step)][(slot)][(ev)] = clock64();                                          \
+  } while (0)
+#else
+#define FPSA_TL(slot, ev, step) \
+  do {                          \
+  } while (0)
+#endif
+constexpr uint32_t kNegInf = 0xFF800000u;
+
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float max3(float a, float b, float c) {
+  float y;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(y) : "f"(a), "f"(b), "f"(c));
+  return y;
+}
+// ---- packed f32x2 arithmetic (sm_100 FFMA2 / FADD2): two lanes per instruction
+struct f2 {
+  float x, y;
+};
+__device__ __forceinline__ f2 fma2(f2 a, f2 b, f2 c) {
+  f2 d;
+  asm("{\n\t.reg .b64 ra, rb, rc, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\tmov.b64 rc, {%6, %7};\n\t"
+      "fma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return d;
+}
+__device__ __forceinline__ f2 add2(f2 a, f2 b) {
+  f2 d;
+  asm("{\n\t.reg .b64 ra, rb, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+      "add.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
+__device__ __forceinline__ f2 bcast(float v) { return f2{v, v}; }
+
+// Scalar saturating FMA (there is no .sat for f32x2): clamps to [0, 1].
+__device__ __forceinline__ float fma_sat(float a, float b, float c) {
+  float d;
+  asm("fma.rn.sat.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+
+// 2^x on the FMA pipe for a pair, x = s * c + noff given as
+//   xs = sat(s * c/256 + (noff + 126)/256)  in [0, 1]   (x clamped to [-126, 130],
+//   so the exponent add below never leaves the float range)
+// Cody-Waite split x = j + f (j = round(x), |f| <= 1/2) with the rounding
+// done by the magic-number add, then a degree-2 minimax for 2^f (rel. err
+// 1.7e-3, far below the 2^-4 step of the e4m3 P it feeds) and j added to the
+// exponent field.  Used for half of the columns so that MUFU ex2 (16/clk/SM)
+// is not the only exp source.
+__device__ __forceinline__ f2 exp2_poly_sat(f2 xs) {
+  constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23
+  const f2 t = fma2(xs, bcast(256.0f), bcast(kMagic - 126.0f));  // kMagic + round(x), x = 256 xs - 126
+  const f2 g = add2(t, bcast(126.0f - kMagic));                   // round(x) + 126
+  const f2 f = fma2(xs, bcast(256.0f), f2{-g.x, -g.y});           // x - round(x)
+  f2 y = fma2(bcast(0.238487109541893f), f, bcast(0.703453540802002f));
+  y = fma2(y, f, bcast(1.0004364252090454f));
+  return f2{__uint_as_float(__float_as_uint(y.x) + (__float_as_uint(t.x) << 23)),
+            __uint_as_float(__float_as_uint(y.y) + (__float_as_uint(t.y) << 23))};
+}
+
+// Four e4m3 codes in one word (a.x lowest byte).
+__device__ __forceinline__ uint32_t e4m3x4(f2 a, f2 b) {
+  uint32_t r;
+  asm("{\n\t.reg .b16 lo, hi;\n\t"
+      "cvt.rn.satfinite.e4m3x2.f32 lo, %2, %1;\n\t"
+      "cvt.rn.satfinite.e4m3x2.f32 hi, %4, %3;\n\t"
+      "mov.b32 %0, {lo, hi};\n\t}"
+      : "=r"(r)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return r;
+}
+
+// Which groups of 4 columns of a 32-column chunk take the FMA-pipe
+// polynomial (bit g set -> columns 4g..4g+3) instead of MUFU ex2; the odd
+// groups by default (half of the columns, balancing MUFU and the FMA pipe).
+#ifndef FPSA_POLY_MASK
+#define FPSA_POLY_MASK 0xAA
+#endif
+
+// P~ for 16 S columns [16U, 16U + 16) of a thread's half row, read from the
+// 32-column chunk `s` that holds columns [32 (U/2), 32 (U/2) + 32): 4 groups
+// of 4 keys, polynomial or MUFU per FPSA_POLY_MASK.  Writes 4 packed P words
+// w[4U..4U+3] and (SUM) accumulates the unrounded weights into acc.
+template <int U, int MASK = FPSA_POLY_MASK, bool SUM = true>
+__device__ __forceinline__ void softmax_unit(const uint32_t* s, f2 cc, f2 bb, float cs, float bs, f2* acc,
+                                             uint32_t* w) {
+#pragma unroll
+  for (int g = 0; g < 4; ++g) {
+    const int c0 = 16 * (U & 1) + 4 * g;
+    const f2 a{__uint_as_float(s[c0]), __uint_as_float(s[c0 + 1])};
+    const f2 b{__uint_as_float(s[c0 + 2]), __uint_as_float(s[c0 + 3])};
+    f2 pa, pb;
+    if ((MASK >> (4 * (U & 1) + g)) & 1) {
+      pa = exp2_poly_sat(f2{fma_sat(a.x, cs, bs), fma_sat(a.y, cs, bs)});
+      pb = exp2_poly_sat(f2{fma_sat(b.x, cs, bs), fma_sat(b.y, cs, bs)});
+    } else {
+      pa = fma2(a, cc, bb);
+      pb = fma2(b, cc, bb);
+      pa = f2{ex2(pa.x), ex2(pa.y)};
+      pb = f2{ex2(pb.x), ex2(pb.y)};
+    }
+    if constexpr (SUM) {
+      acc[g & 1] = add2(acc[g & 1], pa);
+      acc[2 + (g & 1)] = add2(acc[2 + (g & 1)], pb);
+    }
+    w[4 * U + g] = e4m3x4(pa, pb);
+  }
+}
+
+// All 32 columns of chunk C (P words w[8C..8C+7]) in phases: every MUFU
+// argument and every polynomial argument is formed first, then the MUFU ops
+// are issued, then the polynomials, then the packing.  Keeping all MUFU
+// arguments live at once gives each MUFU its own source register; with a
+// reused register, the next FFMA2 would wait (WAR) until the XU queue has
+// read the previous MUFU's operand.
+template <int C, int MASK = FPSA_POLY_MASK>
+__device__ __forceinline__ void softmax_chunk32(const uint32_t* s, f2 cc, f2 bb, float cs, float bs, uint32_t* w) {
+  f2 x[16];  // per column pair: MUFU argument or clamped polynomial argument
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const f2 v{__uint_as_float(s[2 * i]), __uint_as_float(s[2 * i + 1])};
+    if ((MASK >> (i / 2)) & 1) x[i] = f2{fma_sat(v.x, cs, bs), fma_sat(v.y, cs, bs)};
+    else x[i] = fma2(v, cc, bb);
+  }
+#pragma unroll
+  for (int i = 0; i < 16; ++i)
+    if (!((MASK >> (i / 2)) & 1)) x[i] = f2{ex2(x[i].x), ex2(x[i].y)};
+#pragma unroll
+  for (int i = 0; i < 16; ++i)
+    if ((MASK >> (i / 2)) & 1) x[i] = exp2_poly_sat(x[i]);
+#pragma unroll
+  for (int g = 0; g < 8; ++g) w[8 * C + g] = e4m3x4(x[2 * g], x[2 * g + 1]);
+}
+
+// The last 8 of the ncol valid columns are zero K rows (tv % 16 == 8): -inf
+// drops them from max, sum and P.  `s` holds columns [base, base + 32).
+__device__ __forceinline__ void mask_pad8(uint32_t* s, int base, int ncol) {
+#pragma unroll
+  for (int i = 8; i < 32; i += 16)
+    if (base + i + 8 == ncol) {
+#pragma unroll
+      for (int k = i; k < i + 8; ++k) s[k] = kNegInf;
+    }
+}
+
+template <int C>
+__device__ __forceinline__ void softmax_chunk(uint32_t* s, int ncol, bool pad8, f2 cc, f2 bb, float cs, float bs,
+                                              uint32_t* w) {
+  if (pad8) mask_pad8(s, 32 * C, ncol);
+  if (ncol > 32 * C) softmax_unit<2 * C, FPSA_POLY_MASK, false>(s, cc, bb, cs, bs, nullptr, w);
+  else w[8 * C] = w[8 * C + 1] = w[8 * C + 2] = w[8 * C + 3] = 0u;
+  if (ncol > 32 * C + 16) softmax_unit<2 * C + 1, FPSA_POLY_MASK, false>(s, cc, bb, cs, bs, nullptr, w);
+  else w[8 * C + 4] = w[8 * C + 5] = w[8 * C + 6] = w[8 * C + 7] = 0u;
+}
+
+// Nonzero iff some packed e4m3 code is 0x7E (448, the saturation value): P~ >= 0
+// so codes are <= 0x7E, and adding 2 to each byte sets its top bit only for 0x7E.
+__device__ __forceinline__ uint32_t saturated(const uint32_t* w) {
+  uint32_t a = 0u;
+#pragma unroll
+  for (int i = 0; i < kHalf / 4; i += 2) a |= (w[i] + 0x02020202u) | (w[i + 1] + 0x02020202u);
+  return a & 0x80808080u;
+}
+
+// One half row of one key block: 64 S columns from TMEM, ncol (multiple of
+// 16, 0..64) valid, P~ words of absent columns zero.  The row sum of P~ is
+// not taken here: the PV MMA accumulates it in the "ones" columns of O.
+// Returns nonzero if some P~ reached the e4m3 saturation value.
+__device__ __forceinline__ uint32_t softmax_block(uint32_t s_addr, int ncol, bool pad8, float c, float boff,
+                                                  uint32_t* w) {
+  const f2 cc = bcast(c), bb = bcast(boff);
+  const float cs = c * (1.0f / 256.0f), bs = (boff + 126.0f) * (1.0f / 256.0f);
+  uint32_t sa[32], sb[32];
+  if (ncol == kHalf && !pad8) {
+    // common case: all 64 columns valid, one load wait and a single basic block of
+    // 64 independent elements for the scheduler
+#ifdef FPSA_TRACE
+    const long long tl0 = clock64();
+#endif
+    // 32 columns at a time: fewer live S registers leave the scheduler room for
+    // distinct MUFU source registers (a reused source serialises on the XU queue)
+    tmem_ld32(s_addr, sa);
+    tmem_wait_ld();
+#ifdef FPSA_TRACE
+    if ((threadIdx.x & 31) == 0) atomicAdd(&g_trace[4], (unsigned long long)(clock64() - tl0));
+#endif
+    softmax_chunk32<0>(sa, cc, bb, cs, bs, w);
+    tmem_ld32(s_addr + 32, sb);
+    tmem_wait_ld();
+    softmax_chunk32<1>(sb, cc, bb, cs, bs, w);
+  } else {
+    if (ncol > 0) {
+      tmem_ld32(s_addr, sa);
+      tmem_wait_ld();
+    }
+    if (ncol > 32) tmem_ld32(s_addr + 32, sb);
+    softmax_chunk<0>(sa, ncol, pad8, cc, bb, cs, bs, w);
+    if (ncol > 32) tmem_wait_ld();
+    softmax_chunk<1>(sb, ncol, pad8, cc, bb, cs, bs, w);
+  }
+  return saturated(w);
+}
+
+// Max of the first ncol (0..64) raw S values of a half row (-inf if none).
+__device__ __forceinline__ float block_max(uint32_t s_addr, int ncol, bool pad8) {
+  float m0 = -INFINITY, m1 = -INFINITY;
+#pragma unroll
+  for (int base = 0; base < kHalf; base += 32) {
+    if (base < ncol) {
+      uint32_t s[32];
+      tmem_ld32(s_addr + base, s);
+      tmem_wait_ld();
+      if (pad8) mask_pad8(s, base, ncol);
+#pragma unroll
+      for (int i = 0; i < 32; i += 4) {
+        if (base + i < ncol) {
+          m0 = max3(m0, __uint_as_float(s[i]), __uint_as_float(s[i + 1]));
+          m1 = max3(m1, __uint_as_float(s[i + 2]), __uint_as_float(s[i + 3]));
+        }
+      }
+    }
+  }
+  return fmaxf(m0, m1);
+}
+
+}  // namespace
+}  // namespace fpsa

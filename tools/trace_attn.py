@@ -23,6 +23,19 @@ print(f"attention {s.elapsed_time(e):.3f} ms (traced build)")
 n = max(1, t[6])  # softmax warp-steps
 print(f"softmax per warp-step: loop {t[1]/n:.0f} clk, wait-for-S {t[0]/n:.0f}, first-pass compute {t[2]/n:.0f}, "
       f"rest (setup/store/arrive) {(t[1]-t[0]-t[2])/n:.0f}")
+print(f"   of which S load (tcgen05.ld + wait::ld, full blocks) {t[4]/n:.0f} clk")
 steps = n / 8
 print(f"MMA per step: wait P {t[3]/steps:.0f} clk, wait K/V {t[7]/steps:.0f} clk")
 print(f"redo items: {t[5]} of {plan.n_items}")
+
+# timeline of CTA 0: per step, softmax warps (wait start, S ready, compute end, P arrived) and MMA
+tl = (ctypes.c_longlong * (256 * 10 * 4))()
+lib.fpsa_trace_timeline.argtypes = [ctypes.POINTER(ctypes.c_longlong)]
+lib.fpsa_trace_timeline(tl)
+import numpy as np
+T = np.array(tl, dtype=np.int64).reshape(256, 10, 4)
+t0 = T[0, 0, 0]
+print("step | warp0: wait S-ready comp-end arrived | warp4: ... | MMA: p_ready-ok pv-issued qk-issued   (clk rel. to step 0)")
+for j in range(2, 40):
+    w0 = T[j, 0] - t0; w4 = T[j, 4] - t0; w1 = T[j, 1] - t0; m = T[j, 9] - t0
+    print(f"{j:3d} | {w0[0]:7d} {w0[1]:7d} {w0[2]:7d} {w0[3]:7d} | {w4[1]:7d} {w4[2]:7d} {w4[3]:7d} | w1 {w1[1]:7d} {w1[3]:7d} | {m[1]:7d} {m[2]:7d} {m[3]:7d}")
