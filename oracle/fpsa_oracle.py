@@ -334,9 +334,8 @@ def sparse_forward_f32(q, k, v, tv, offs, ids, softmax_scale=None):
 
 def _poly_columns(block: int = 128) -> np.ndarray:
     """Columns of a key block whose exp2 the GPU kernel evaluates with its polynomial:
-    odd groups of 4 (fpsa_attn.cu softmax_unit, groups with bit 2 of the column set)."""
-    c = np.arange(block)
-    return ((c % 64) // 4) % 2 == 1
+    the odd columns (softmax.cuh softmax_chunk32 / softmax_unit); the even ones use MUFU ex2."""
+    return np.arange(block) % 2 == 1
 
 
 def _exp2_poly(x: np.ndarray) -> np.ndarray:

@@ -30,10 +30,10 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(os.path.join(HERE, s)) <= t for s in SOURCES + HEADERS)
 
 
-def build_trace() -> str:
+def build_trace(extra=(), name="libfpsa_trace.so") -> str:
     """Instrumented variant (-DFPSA_TRACE, cycle counters; tools/trace_attn.py), never loaded by the package."""
-    target = os.path.join(HERE, "libfpsa_trace.so")
-    subprocess.run([nvcc(), *NVCC_FLAGS, "-DFPSA_TRACE", *SOURCES, "-o", target], cwd=HERE, check=True)
+    target = os.path.join(HERE, name)
+    subprocess.run([nvcc(), *NVCC_FLAGS, "-DFPSA_TRACE", *extra, *SOURCES, "-o", target], cwd=HERE, check=True)
     return target
 
 
@@ -51,6 +51,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
 if __name__ == "__main__":
     if "--trace" in sys.argv:
         print(build_trace())
+        if "--nomma" in sys.argv:  # timing experiment: tensor core idle (results invalid)
+            print(build_trace(("-DFPSA_NO_MMA",), "libfpsa_trace_nomma.so"))
         sys.exit(0)
     build(force="--force" in sys.argv, verbose="-v" in sys.argv)
     print(TARGET)

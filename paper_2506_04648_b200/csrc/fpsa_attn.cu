@@ -60,7 +60,9 @@ using namespace sm100;
 constexpr int kSoftmaxWarps = 8;
 constexpr int kTmaWarp = kSoftmaxWarps;
 constexpr int kMmaWarp = kSoftmaxWarps + 1;
-constexpr int kThreads = (kSoftmaxWarps + 2) * 32;
+constexpr int kThreads = (kSoftmaxWarps + 4) * 32;  // 3 warpgroups: 2 softmax, 1 producer (TMA, MMA, 2 idle)
+// setmaxnreg split of the 64K-register file: per SMSP one warp of each warpgroup
+constexpr uint32_t kRegsSoftmax = 224, kRegsProducer = 56;
 
 constexpr int kStages = 4;     // K/V ring depth (128-key blocks)
 constexpr int kBlk = 128;      // rows per query block = keys per key block
@@ -179,6 +181,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   auto tm_s = [tmem](uint32_t g) { return tmem + 256u + 128u * (g & 1u); };
   const float tau = p.exact ? 0.0f : p.tau;
 
+  if (warp >= kSoftmaxWarps) regs_dec<kRegsProducer>();  // producer warpgroup: TMA, MMA, 2 idle warps
   if (warp == kTmaWarp) {
     // ------------------------------------------------------------ TMA producer (warp-uniform, one elected lane issues)
     if (lane == 0) {
@@ -237,9 +240,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_after();
         const uint32_t sk = sk0 + st * S::kTile;
         const uint32_t idq = b == p.nb - 1 ? idesc_qk_tail : idesc_qk;
+#ifndef FPSA_NO_MMA
 #pragma unroll
         for (int k = 0; k < D / 32; ++k)
           mma_f8_ss_w(tm_s(gg), desc_kmajor<D>(sq + 32 * k), desc_kmajor<D>(sk + 32 * k), idq, k > 0 ? 1u : 0u);
+#endif
         mma_commit_w(&bar_s_full[gg & 1]);
       };
       int32_t b2 = 0;  // in-tile block of step s + 2
@@ -269,10 +274,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc_fence_after();
           }
           const uint32_t sv = sv0 + st * S::kTile;
+#ifndef FPSA_NO_MMA
 #pragma unroll
           for (int k = 0; k < kBlk / 32; ++k)
             mma_f8_ts_w(tm_o, tm_s(gs) + 64 * (k >> 1) + 8 * (k & 1), desc_mnmajor_ones<D>(sv + k * 32 * D, sones - sv),
                         idesc_pv, (s > pv0 || k > 0) ? 1u : 0u);
+#endif
         }
         mma_commit_w(&bar_kv_empty[st]);
         FPSA_TL(9, 2, gs);
@@ -286,7 +293,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       mma_commit_w(&bar_o);
       g += steps;
     }
-  } else {
+  } else if (warp < kSoftmaxWarps) {
+    regs_inc<kRegsSoftmax>();
     // ------------------------------------------------------------ softmax: (row, column half)
     const int quarter = warp & 3;
     const int half = warp >> 2;              // S columns [64 half, 64 half + 64)

@@ -104,66 +104,40 @@ __device__ __forceinline__ uint32_t e4m3x4(f2 a, f2 b) {
   return r;
 }
 
-// Which groups of 4 columns of a 32-column chunk take the FMA-pipe
-// polynomial (bit g set -> columns 4g..4g+3) instead of MUFU ex2; the odd
-// groups by default (half of the columns, balancing MUFU and the FMA pipe).
-#ifndef FPSA_POLY_MASK
-#define FPSA_POLY_MASK 0xAA
-#endif
-
 // P~ for 16 S columns [16U, 16U + 16) of a thread's half row, read from the
-// 32-column chunk `s` that holds columns [32 (U/2), 32 (U/2) + 32): 4 groups
-// of 4 keys, polynomial or MUFU per FPSA_POLY_MASK.  Writes 4 packed P words
-// w[4U..4U+3] and (SUM) accumulates the unrounded weights into acc.
-template <int U, int MASK = FPSA_POLY_MASK, bool SUM = true>
-__device__ __forceinline__ void softmax_unit(const uint32_t* s, f2 cc, f2 bb, float cs, float bs, f2* acc,
-                                             uint32_t* w) {
+// 32-column chunk `s` that holds columns [32 (U/2), 32 (U/2) + 32): in each
+// group of 4 keys, columns 0 and 2 on MUFU ex2 and columns 1 and 3 on the
+// FMA-pipe polynomial (the same split as softmax_chunk32).  Writes 4 packed
+// P words w[4U..4U+3].
+template <int U>
+__device__ __forceinline__ void softmax_unit(const uint32_t* s, f2 cc, f2 bb, float cs, float bs, uint32_t* w) {
 #pragma unroll
   for (int g = 0; g < 4; ++g) {
-    const int c0 = 16 * (U & 1) + 4 * g;
-    const f2 a{__uint_as_float(s[c0]), __uint_as_float(s[c0 + 1])};
-    const f2 b{__uint_as_float(s[c0 + 2]), __uint_as_float(s[c0 + 3])};
-    f2 pa, pb;
-    if ((MASK >> (4 * (U & 1) + g)) & 1) {
-      pa = exp2_poly_sat(f2{fma_sat(a.x, cs, bs), fma_sat(a.y, cs, bs)});
-      pb = exp2_poly_sat(f2{fma_sat(b.x, cs, bs), fma_sat(b.y, cs, bs)});
-    } else {
-      pa = fma2(a, cc, bb);
-      pb = fma2(b, cc, bb);
-      pa = f2{ex2(pa.x), ex2(pa.y)};
-      pb = f2{ex2(pb.x), ex2(pb.y)};
-    }
-    if constexpr (SUM) {
-      acc[g & 1] = add2(acc[g & 1], pa);
-      acc[2 + (g & 1)] = add2(acc[2 + (g & 1)], pb);
-    }
-    w[4 * U + g] = e4m3x4(pa, pb);
+    const float* v = reinterpret_cast<const float*>(s + 16 * (U & 1) + 4 * g);
+    f2 m = fma2(f2{v[0], v[2]}, cc, bb);
+    m = f2{ex2(m.x), ex2(m.y)};
+    const f2 pp = exp2_poly_sat(f2{fma_sat(v[1], cs, bs), fma_sat(v[3], cs, bs)});
+    w[4 * U + g] = e4m3x4(f2{m.x, pp.x}, f2{m.y, pp.y});
   }
 }
 
-// All 32 columns of chunk C (P words w[8C..8C+7]) in phases: every MUFU
-// argument and every polynomial argument is formed first, then the MUFU ops
-// are issued, then the polynomials, then the packing.  Keeping all MUFU
-// arguments live at once gives each MUFU its own source register; with a
-// reused register, the next FFMA2 would wait (WAR) until the XU queue has
-// read the previous MUFU's operand.
-template <int C, int MASK = FPSA_POLY_MASK>
+// All 32 columns of chunk C (P words w[8C..8C+7]), columns interleaved
+// between the two exp2 sources: in each group of 4, columns 0 and 2 on MUFU
+// ex2, columns 1 and 3 on the FMA-pipe polynomial.  Every e4m3 pair (cvt)
+// then takes one MUFU and one polynomial result, so a MUFU result stays live
+// until the longer polynomial chain completes and the MUFU operands get
+// distinct registers (a rotating register would serialise each FFMA2 behind
+// the previous MUFU through the XU queue).
+template <int C>
 __device__ __forceinline__ void softmax_chunk32(const uint32_t* s, f2 cc, f2 bb, float cs, float bs, uint32_t* w) {
-  f2 x[16];  // per column pair: MUFU argument or clamped polynomial argument
 #pragma unroll
-  for (int i = 0; i < 16; ++i) {
-    const f2 v{__uint_as_float(s[2 * i]), __uint_as_float(s[2 * i + 1])};
-    if ((MASK >> (i / 2)) & 1) x[i] = f2{fma_sat(v.x, cs, bs), fma_sat(v.y, cs, bs)};
-    else x[i] = fma2(v, cc, bb);
+  for (int q = 0; q < 8; ++q) {
+    const float* v = reinterpret_cast<const float*>(s + 4 * q);
+    f2 m = fma2(f2{v[0], v[2]}, cc, bb);
+    m = f2{ex2(m.x), ex2(m.y)};
+    const f2 pp = exp2_poly_sat(f2{fma_sat(v[1], cs, bs), fma_sat(v[3], cs, bs)});
+    w[8 * C + q] = e4m3x4(f2{m.x, pp.x}, f2{m.y, pp.y});
   }
-#pragma unroll
-  for (int i = 0; i < 16; ++i)
-    if (!((MASK >> (i / 2)) & 1)) x[i] = f2{ex2(x[i].x), ex2(x[i].y)};
-#pragma unroll
-  for (int i = 0; i < 16; ++i)
-    if ((MASK >> (i / 2)) & 1) x[i] = exp2_poly_sat(x[i]);
-#pragma unroll
-  for (int g = 0; g < 8; ++g) w[8 * C + g] = e4m3x4(x[2 * g], x[2 * g + 1]);
 }
 
 // The last 8 of the ncol valid columns are zero K rows (tv % 16 == 8): -inf
@@ -181,9 +155,9 @@ template <int C>
 __device__ __forceinline__ void softmax_chunk(uint32_t* s, int ncol, bool pad8, f2 cc, f2 bb, float cs, float bs,
                                               uint32_t* w) {
   if (pad8) mask_pad8(s, 32 * C, ncol);
-  if (ncol > 32 * C) softmax_unit<2 * C, FPSA_POLY_MASK, false>(s, cc, bb, cs, bs, nullptr, w);
+  if (ncol > 32 * C) softmax_unit<2 * C>(s, cc, bb, cs, bs, w);
   else w[8 * C] = w[8 * C + 1] = w[8 * C + 2] = w[8 * C + 3] = 0u;
-  if (ncol > 32 * C + 16) softmax_unit<2 * C + 1, FPSA_POLY_MASK, false>(s, cc, bb, cs, bs, nullptr, w);
+  if (ncol > 32 * C + 16) softmax_unit<2 * C + 1>(s, cc, bb, cs, bs, w);
   else w[8 * C + 4] = w[8 * C + 5] = w[8 * C + 6] = w[8 * C + 7] = 0u;
 }
 

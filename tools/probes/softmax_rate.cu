@@ -24,33 +24,28 @@ using namespace fpsa;
 
 template <int MASK, bool SUM>
 __device__ __forceinline__ float pass64(uint32_t s_addr, float c, float boff, uint32_t* w) {
+  if (MASK == 1) return (float)softmax_block(s_addr, 64, false, c, boff, w);  // the kernel's entry point
   const f2 cc = bcast(c), bb = bcast(boff);
   const float cs = c * (1.0f / 256.0f), bs = (boff + 126.0f) * (1.0f / 256.0f);
-  f2 acc[4] = {bcast(0.f), bcast(0.f), bcast(0.f), bcast(0.f)};
   uint32_t sa[32], sb[32];
   tmem_ld32(s_addr, sa);
+  tmem_wait_ld();
+  softmax_chunk32<0>(sa, cc, bb, cs, bs, w);
   tmem_ld32(s_addr + 32, sb);
   tmem_wait_ld();
-  softmax_unit<0, MASK, SUM>(sa, cc, bb, cs, bs, acc, w);
-  softmax_unit<1, MASK, SUM>(sa, cc, bb, cs, bs, acc, w);
-  softmax_unit<2, MASK, SUM>(sb, cc, bb, cs, bs, acc, w);
-  softmax_unit<3, MASK, SUM>(sb, cc, bb, cs, bs, acc, w);
-  const f2 t = add2(add2(acc[0], acc[1]), add2(acc[2], acc[3]));
-  return t.x + t.y;
+  softmax_chunk32<1>(sb, cc, bb, cs, bs, w);
+  return __uint_as_float(w[0]);
 }
 
 template <int MASK, bool SUM>
 __device__ __forceinline__ float pass32(uint32_t s_addr, float c, float boff, uint32_t* w) {
   const f2 cc = bcast(c), bb = bcast(boff);
   const float cs = c * (1.0f / 256.0f), bs = (boff + 126.0f) * (1.0f / 256.0f);
-  f2 acc[4] = {bcast(0.f), bcast(0.f), bcast(0.f), bcast(0.f)};
   uint32_t sa[32];
   tmem_ld32(s_addr, sa);
   tmem_wait_ld();
-  softmax_unit<0, MASK, SUM>(sa, cc, bb, cs, bs, acc, w);
-  softmax_unit<1, MASK, SUM>(sa, cc, bb, cs, bs, acc, w);
-  const f2 t = add2(add2(acc[0], acc[1]), add2(acc[2], acc[3]));
-  return t.x + t.y;
+  softmax_chunk32<0>(sa, cc, bb, cs, bs, w);
+  return __uint_as_float(w[0]);
 }
 
 // 16 softmax warps (4 per lane quarter, 32 columns each) + 2 idle warps
@@ -124,7 +119,7 @@ __global__ void __launch_bounds__(320, 1) softmax_rate(int iters, long long* out
     const uint32_t addr = smem_u32(&bar_done);
     while (!mbar_try_wait(addr, 0)) {
       for (int k = 0; k < 4; ++k)
-        mma_f8_ss(tmem_base_probe(s_tmem), smem_desc_sw128(sq + 32 * k, 16, 1024), smem_desc_sw128(sk + 32 * k, 16, 1024), id_qk, k > 0);
+        mma_f8_ss(s_tmem, smem_desc_sw128(sq + 32 * k, 16, 1024), smem_desc_sw128(sk + 32 * k, 16, 1024), id_qk, k > 0);
       for (int k = 0; k < 4; ++k)
         mma_f8_ts(s_tmem + 0, s_tmem + 448 + 8 * k, smem_desc_sw128(sv + k * 4096, 16384, 1024), id_pv, 1);
     }
@@ -165,6 +160,8 @@ __global__ void __launch_bounds__(320, 1) softmax_rate(int iters, long long* out
     for (int it = 0; it < iters; ++it) {
       const uint32_t s_addr = base + 128 * (it & 1);
       uint32_t w[16];
+      if (SPIN == 4) named_bar_sync(1 + quarter, 64);  // the two halves of a row start each step together
+      if (SPIN == 5) named_bar_sync(1, 256);           // all softmax warps start each step together
       l += pass64<MASK, SUM>(s_addr, c, boff, w);
       tmem_st16(s_addr + 32, w);  // P into columns that are not read back (keeps S intact)
       tmem_wait_st();
@@ -229,6 +226,9 @@ int main() {
   CK(cudaMalloc(&sink, 148 * 256 * sizeof(float)));
   run<0xAA, true>("poly 1/2 (0xAA), sum", d, sink);
   run<0xAA, false>("poly 1/2 (0xAA), no sum      [kernel]", d, sink);
+  run<1, false>("kernel softmax_block (64 cols, sat check)", d, sink);
+  run<1, false, 4>("  + pair lockstep (bar.sync 64 per step)", d, sink);
+  run<1, false, 5>("  + all-warp lockstep (bar.sync 256 per step)", d, sink);
   run<0xAA, false, 1>("  + 2 warps spinning on try_wait", d, sink);
   run<0xAA, false, 2>("  + 2 warps try_wait w/ suspend hint", d, sink);
   run<0xAA, false, 3>("  + tensor core busy (QK SS + PV TS loop)", d, sink);

@@ -2,7 +2,7 @@
 import ctypes, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2506_04648_b200._lib as L
-L.LIB_PATH = L.LIB_PATH.replace("libfpsa.so", "libfpsa_trace.so")
+L.LIB_PATH = L.LIB_PATH.replace("libfpsa.so", os.environ.get("FPSA_TRACE_LIB", "libfpsa_trace.so"))
 import torch
 import paper_2506_04648_b200 as F
 cfg = sys.argv[1] if len(sys.argv) > 1 else "c2"
