@@ -68,6 +68,7 @@ constexpr int kStages = 4;     // K/V ring depth (128-key blocks)
 constexpr int kBlk = 128;      // rows per query block = keys per key block
 constexpr float kLog2_448 = 8.807354922057604f;
 constexpr int kRedoHeader = 4;  // int32 words before the redo items in the workspace
+constexpr int kFacCap = 256;    // key-tile factors per item kept in shared memory (more: read from L2)
 
 struct AttnParams {
   const double* q_scales;
@@ -142,6 +143,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __shared__ uint64_t bar_s_full[2], bar_p_ready[2];  // by S buffer / step parity
   __shared__ uint32_t s_tmem;
   __shared__ float s_xchg[2][kBlk];  // [half][row] pair exchange
+  __shared__ float s_fac[kSoftmaxWarps][2][kFacCap];  // per softmax warp, per item parity: key-tile factors
   __shared__ uint32_t s_ovf[2];      // per item parity: some row overflowed
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -220,42 +222,51 @@ __global__ void __launch_bounds__(kThreads, 1)
     constexpr uint32_t idesc_qk = idesc_f8(128, 128, FMT, FMT, 0);
     const uint32_t idesc_qk_tail = idesc_f8(128, (uint32_t)p.n_tail, FMT, FMT, 0);
     constexpr uint32_t idesc_pv = idesc_f8(128, D + 16, FPSA_E4M3, FMT, 1);
-    const uint32_t sk0 = smem_u32(smem + S::kK), sv0 = smem_u32(smem + S::kV);
-    const uint32_t sones = smem_u32(smem + S::kOnes);
+    // Descriptors are built once; a K-chunk / stage step only moves the 14-bit
+    // start-address field (16-byte units), which never carries out.
+    constexpr uint64_t kTileU = S::kTile >> 4;
+    const uint32_t sv0 = smem_u32(smem + S::kV);
+    const uint64_t dq0 = desc_kmajor<D>(smem_u32(smem + S::kQ));
+    const uint64_t dk0 = desc_kmajor<D>(smem_u32(smem + S::kK));
+    // V stage st: start sv0 + st*tile, leading byte offset to the ones atom shrinks by the same amount
+    const uint64_t dv0 = desc_mnmajor_ones<D>(sv0, smem_u32(smem + S::kOnes) - sv0);
+    constexpr uint64_t kVStageStep = kTileU - (kTileU << 16);
     uint32_t g = 0;
     int32_t iter = 0;
+    uint32_t qk_st = 0, qk_ph = 0;  // K/V stage + full-barrier phase of the next QK
+    uint32_t pv_st = 0;             // K/V stage of the next PV
     for (int32_t it = blockIdx.x; it < count; it += gridDim.x, ++iter) {
       const int32_t u = items[3 * it + 1];
       const int32_t n_kt = __ldg(p.offs + u + 1) - __ldg(p.offs + u);
       const int32_t n_kv = n_kt * p.nb, steps = p.exact ? 2 * n_kv : n_kv;
       const int32_t pv0 = p.exact ? n_kv : 0;  // first step with a PV
       const int qbuf = iter & 1;
-      const uint32_t sq = smem_u32(smem + S::kQ + qbuf * S::kTile);
+      const uint64_t dq = dq0 + (uint64_t)qbuf * kTileU;
       mbar_wait(&bar_q[qbuf], (iter >> 1) & 1);
       tc_fence_after();
-      // S(step) = Q K^T into TMEM buffer g % 2; b = in-tile block of the step
-      auto issue_qk = [&](uint32_t gg, int32_t b) {
-        const uint32_t st = gg % kStages;
-        mbar_wait(&bar_kv_full[st], (gg / kStages) & 1);
+      int32_t b2 = 0;  // in-tile block of the next QK
+      // S(step gg) = Q K^T into TMEM buffer gg % 2
+      auto issue_qk = [&](uint32_t gg) {
+        mbar_wait(&bar_kv_full[qk_st], qk_ph);
         tc_fence_after();
-        const uint32_t sk = sk0 + st * S::kTile;
-        const uint32_t idq = b == p.nb - 1 ? idesc_qk_tail : idesc_qk;
+        const uint64_t dk = dk0 + qk_st * kTileU;
+        const uint32_t idq = b2 == p.nb - 1 ? idesc_qk_tail : idesc_qk;
+        const uint32_t ts = tm_s(gg);
 #ifndef FPSA_NO_MMA
 #pragma unroll
-        for (int k = 0; k < D / 32; ++k)
-          mma_f8_ss_w(tm_s(gg), desc_kmajor<D>(sq + 32 * k), desc_kmajor<D>(sk + 32 * k), idq, k > 0 ? 1u : 0u);
+        for (int k = 0; k < D / 32; ++k) mma_f8_ss_w(ts, dq + 2 * k, dk + 2 * k, idq, k > 0 ? 1u : 0u);
 #endif
         mma_commit_w(&bar_s_full[gg & 1]);
-      };
-      int32_t b2 = 0;  // in-tile block of step s + 2
-      for (int32_t s = 0; s < min(steps, 2); ++s) {
-        issue_qk(g + s, b2);
         if (++b2 == p.nb) b2 = 0;
-      }
+        if (++qk_st == kStages) {
+          qk_st = 0;
+          qk_ph ^= 1;
+        }
+      };
+      for (int32_t s = 0; s < min(steps, 2); ++s) issue_qk(g + s);
       if (steps <= 2) mma_commit_w(&bar_qfree[qbuf]);
       for (int32_t s = 0; s < steps; ++s) {
         const uint32_t gs = g + s;
-        const uint32_t st = gs % kStages;
 #ifdef FPSA_TRACE
         const long long tp0 = clock64();
 #endif
@@ -273,20 +284,21 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_wait(&bar_ofree, (iter - 1) & 1);  // the previous item's epilogue has read O
             tc_fence_after();
           }
-          const uint32_t sv = sv0 + st * S::kTile;
+          const uint64_t dv = dv0 + pv_st * kVStageStep;
+          const uint32_t ts = tm_s(gs);
 #ifndef FPSA_NO_MMA
 #pragma unroll
           for (int k = 0; k < kBlk / 32; ++k)
-            mma_f8_ts_w(tm_o, tm_s(gs) + 64 * (k >> 1) + 8 * (k & 1), desc_mnmajor_ones<D>(sv + k * 32 * D, sones - sv),
-                        idesc_pv, (s > pv0 || k > 0) ? 1u : 0u);
+            mma_f8_ts_w(tm_o, ts + 64 * (k >> 1) + 8 * (k & 1), dv + (uint64_t)k * (32 * D / 16), idesc_pv,
+                        (s > pv0 || k > 0) ? 1u : 0u);
 #endif
         }
-        mma_commit_w(&bar_kv_empty[st]);
+        mma_commit_w(&bar_kv_empty[pv_st]);
+        if (++pv_st == kStages) pv_st = 0;
         FPSA_TL(9, 2, gs);
         if (s + 2 < steps) {
-          issue_qk(gs + 2, b2);
+          issue_qk(gs + 2);
           FPSA_TL(9, 3, gs);
-          if (++b2 == p.nb) b2 = 0;
           if (s + 3 == steps) mma_commit_w(&bar_qfree[qbuf]);
         }
       }
@@ -324,6 +336,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       const double* ks = p.k_scales + (int64_t)h * p.M;
       // c(kt) = f32(f32(sq) * f32(sk)) * f32(scale log2 e), the oracle's factor order
       auto factor = [&](int32_t kt) { return (qs * (float)__ldg(ks + __ldg(p.ids + kt0 + kt))) * sl; };
+      // this warp's copy of the item's factors: one round of L2 latency per item, not per key tile
+      float* fac = s_fac[warp][iter & 1];
+      for (int32_t i = lane; i < min(n_kt, kFacCap); i += 32) fac[i] = factor(i);
+      __syncwarp();
+      auto factor_at = [&](int32_t kt) { return kt < kFacCap ? fac[kt] : factor(kt); };
       float m_ref = 0.0f;
       uint32_t sat = 0u;
 #ifdef FPSA_TRACE
@@ -333,7 +350,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // pass 0 (exact mode only): running max of x over all key blocks
         float m_acc = -INFINITY;
         int32_t kt = 0, b = 0;
-        float c = factor(0);
+        float c = factor_at(0);
         for (int32_t j = 0; j < n_kv; ++j, ++g) {
           const bool tail = b == p.nb - 1;
           const int ncol = (tail ? p.n_tail : kBlk) - kHalf * half;
@@ -342,7 +359,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t s_addr = tm_s(g) + lane_off + half * kHalf;
           // next step's factor, loaded while this step waits / computes
           const int32_t kt_next = tail ? kt + 1 : kt;
-          const float c_next = (tail && kt_next < n_kt) ? factor(kt_next) : c;
+          const float c_next = (tail && kt_next < n_kt) ? factor_at(kt_next) : c;
 #ifdef FPSA_TRACE
           const long long ts0 = clock64();
 #endif
