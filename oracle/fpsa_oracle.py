@@ -334,8 +334,9 @@ def sparse_forward_f32(q, k, v, tv, offs, ids, softmax_scale=None):
 
 def _poly_columns(block: int = 128) -> np.ndarray:
     """Columns of a key block whose exp2 the GPU kernel evaluates with its polynomial:
-    the odd columns (softmax.cuh softmax_chunk32 / softmax_unit); the even ones use MUFU ex2."""
-    return np.arange(block) % 2 == 1
+    columns 2 and 3 of every group of 4 (softmax.cuh softmax_chunk32 / softmax_unit);
+    columns 0 and 1 use MUFU ex2."""
+    return np.arange(block) % 4 >= 2
 
 
 def _exp2_poly(x: np.ndarray) -> np.ndarray:

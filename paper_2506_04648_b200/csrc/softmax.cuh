@@ -73,6 +73,15 @@ __device__ __forceinline__ float fma_sat(float a, float b, float c) {
   return d;
 }
 
+// y + (t << 23): adds the rounded exponent to y's exponent field.  Written as
+// a clamped funnel shift so ptxas emits LEA.HI on the ALU pipe instead of an
+// IMAD on the (busier) FMA pipe.
+__device__ __forceinline__ uint32_t exp_insert(uint32_t y, uint32_t t) {
+  uint32_t r;
+  asm("{\n\t.reg .b32 e;\n\tshf.l.clamp.b32 e, 0, %1, 23;\n\tadd.u32 %0, e, %2;\n\t}" : "=r"(r) : "r"(t), "r"(y));
+  return r;
+}
+
 // 2^x on the FMA pipe for a pair, x = s * c + noff given as
 //   xs = sat(s * c/256 + (noff + 126)/256)  in [0, 1]   (x clamped to [-126, 130],
 //   so the exponent add below never leaves the float range)
@@ -88,8 +97,8 @@ __device__ __forceinline__ f2 exp2_poly_sat(f2 xs) {
   const f2 f = fma2(xs, bcast(256.0f), f2{-g.x, -g.y});           // x - round(x)
   f2 y = fma2(bcast(0.238487109541893f), f, bcast(0.703453540802002f));
   y = fma2(y, f, bcast(1.0004364252090454f));
-  return f2{__uint_as_float(__float_as_uint(y.x) + (__float_as_uint(t.x) << 23)),
-            __uint_as_float(__float_as_uint(y.y) + (__float_as_uint(t.y) << 23))};
+  return f2{__uint_as_float(exp_insert(__float_as_uint(y.x), __float_as_uint(t.x))),
+            __uint_as_float(exp_insert(__float_as_uint(y.y), __float_as_uint(t.y)))};
 }
 
 // Four e4m3 codes in one word (a.x lowest byte).
@@ -106,7 +115,7 @@ __device__ __forceinline__ uint32_t e4m3x4(f2 a, f2 b) {
 
 // P~ for 16 S columns [16U, 16U + 16) of a thread's half row, read from the
 // 32-column chunk `s` that holds columns [32 (U/2), 32 (U/2) + 32): in each
-// group of 4 keys, columns 0 and 2 on MUFU ex2 and columns 1 and 3 on the
+// group of 4 keys, columns 0 and 1 on MUFU ex2 and columns 2 and 3 on the
 // FMA-pipe polynomial (the same split as softmax_chunk32).  Writes 4 packed
 // P words w[4U..4U+3].
 template <int U>
@@ -114,29 +123,25 @@ __device__ __forceinline__ void softmax_unit(const uint32_t* s, f2 cc, f2 bb, fl
 #pragma unroll
   for (int g = 0; g < 4; ++g) {
     const float* v = reinterpret_cast<const float*>(s + 16 * (U & 1) + 4 * g);
-    f2 m = fma2(f2{v[0], v[2]}, cc, bb);
+    f2 m = fma2(f2{v[0], v[1]}, cc, bb);
     m = f2{ex2(m.x), ex2(m.y)};
-    const f2 pp = exp2_poly_sat(f2{fma_sat(v[1], cs, bs), fma_sat(v[3], cs, bs)});
-    w[4 * U + g] = e4m3x4(f2{m.x, pp.x}, f2{m.y, pp.y});
+    const f2 pp = exp2_poly_sat(f2{fma_sat(v[2], cs, bs), fma_sat(v[3], cs, bs)});
+    w[4 * U + g] = e4m3x4(m, pp);
   }
 }
 
-// All 32 columns of chunk C (P words w[8C..8C+7]), columns interleaved
-// between the two exp2 sources: in each group of 4, columns 0 and 2 on MUFU
-// ex2, columns 1 and 3 on the FMA-pipe polynomial.  Every e4m3 pair (cvt)
-// then takes one MUFU and one polynomial result, so a MUFU result stays live
-// until the longer polynomial chain completes and the MUFU operands get
-// distinct registers (a rotating register would serialise each FFMA2 behind
-// the previous MUFU through the XU queue).
+// All 32 columns of chunk C (P words w[8C..8C+7]): in each group of 4 keys,
+// columns 0 and 1 on MUFU ex2 (one FFMA2 forms both arguments from an
+// adjacent register pair), columns 2 and 3 on the FMA-pipe polynomial.
 template <int C>
 __device__ __forceinline__ void softmax_chunk32(const uint32_t* s, f2 cc, f2 bb, float cs, float bs, uint32_t* w) {
 #pragma unroll
   for (int q = 0; q < 8; ++q) {
     const float* v = reinterpret_cast<const float*>(s + 4 * q);
-    f2 m = fma2(f2{v[0], v[2]}, cc, bb);
+    f2 m = fma2(f2{v[0], v[1]}, cc, bb);
     m = f2{ex2(m.x), ex2(m.y)};
-    const f2 pp = exp2_poly_sat(f2{fma_sat(v[1], cs, bs), fma_sat(v[3], cs, bs)});
-    w[8 * C + q] = e4m3x4(f2{m.x, pp.x}, f2{m.y, pp.y});
+    const f2 pp = exp2_poly_sat(f2{fma_sat(v[2], cs, bs), fma_sat(v[3], cs, bs)});
+    w[8 * C + q] = e4m3x4(m, pp);
   }
 }
 
