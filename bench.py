@@ -3,10 +3,13 @@
 One step = the hot path over one batch element: per-tile Q/K and per-channel
 V FP8 quantisation of bf16 [L, H, d] inputs in natural (t,h,w) order, then
 the sparse FP8 attention forward writing bf16 [L, H, d] (libfpsa kernels).
-N GPUs: one process per GPU (torchrun), each rank owns one batch element of
-all 40 heads (weak scaling, no data-path collective), timing = max over ranks.
+N GPUs: one process per GPU (torchrun), heads split across ranks
+(head-parallel, strong scaling: the same 40-head problem on 1..8 GPUs, no
+data-path collective); timing = max over ranks.  ``--ulysses`` instead
+feeds sequence-sharded inputs and adds the NCCL sequence<->head all-to-all
+(BASELINE config C3, HunyuanVideo 720p).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config NAME] [--ulysses]
 """
 
 from __future__ import annotations
@@ -48,6 +51,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="budget of the cpu_baseline sample")
+    ap.add_argument("--ulysses", action="store_true", help="sequence-sharded inputs + all-to-all (C3)")
     return ap.parse_args()
 
 
@@ -154,7 +158,8 @@ def ncu_traffic(config_name: str):
 
 # ---------------------------------------------------------------------------- CPU legs
 def cpu_leg(cfg, budget_s: float, seed: int = 0):
-    """Oracle port (reference algorithm) on a bounded sample of one head; returns dict."""
+    """Oracle port (reference algorithm) on the host cores: whole passes over head 0's query tiles
+    until the budget is spent (at least one pass); returns dict."""
     import oracle as O
     from oracle.cpu_sample import sample_forward, sample_tiles
 
@@ -165,12 +170,13 @@ def cpu_leg(cfg, budget_s: float, seed: int = 0):
     dims = O.tile_grid_dims(grid, tile)
     offs, ids = O.window_lists(dims, win)
     M = dims[0] * dims[1] * dims[2]
-    # calibrate on a few tiles, then size the sample to the budget
-    _, fl0, s0 = sample_forward(q, k, v, tv, offs, ids, sample_tiles(M, 4))
-    n = int(max(4, min(M, 4 * budget_s / max(s0, 1e-3) * 0.8)))
-    tiles = sample_tiles(M, n)
-    _, fl, secs = sample_forward(q, k, v, tv, offs, ids, tiles)
-    return {"flops": fl, "seconds": secs, "tiles": len(tiles), "M": M, "L": L}
+    tiles = sample_tiles(M, M)
+    fl = secs = 0.0
+    passes = 0
+    while passes == 0 or secs < budget_s:
+        _, f, t = sample_forward(q, k, v, tv, offs, ids, tiles)
+        fl, secs, passes = fl + f, secs + t, passes + 1
+    return {"flops": fl, "seconds": secs, "tiles": len(tiles), "M": M, "L": L, "passes": passes}
 
 
 def run_reference(args):
@@ -207,7 +213,7 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": tflops, "unit": "TFLOPS", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": secs / args.steps * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (Philox gaussian, reference generator)",
         "config": {"workload": args.config, "grid": grid, "heads": H, "d": d, "tile": tile, "window": win},
         "cpu_baseline": {"value": tflops, "unit": "TFLOPS", "cores": cores, "kind": "port", "sample": sample},
@@ -237,14 +243,35 @@ def main():
     dev = torch.device("cuda", torch.cuda.current_device())
     grid, H, d, tile, win = CONFIGS[args.config]
     L = grid[0] * grid[1] * grid[2]
+    from paper_2506_04648_b200.sharding import UlyssesAttention, head_range
 
+    if args.ulysses:
+        if world < 2 or H % world or L % world:
+            raise SystemExit("--ulysses needs >= 2 ranks dividing both the heads and the tokens")
+        h0, h1 = 0, H  # every rank holds all heads of its token shard
+        Lr, Hr = L // world, H
+    else:
+        h0, h1 = head_range(rank, world, H)
+        Lr, Hr = L, h1 - h0
     gen = torch.Generator(device=dev).manual_seed(1234 + rank)
-    q = torch.randn((L, H, d), generator=gen, device=dev).to(torch.bfloat16)
-    k = torch.randn((L, H, d), generator=gen, device=dev).to(torch.bfloat16)
-    v = torch.randn((L, H, d), generator=gen, device=dev).to(torch.bfloat16)
+    q = torch.randn((Lr, Hr, d), generator=gen, device=dev).to(torch.bfloat16)
+    k = torch.randn((Lr, Hr, d), generator=gen, device=dev).to(torch.bfloat16)
+    v = torch.randn((Lr, Hr, d), generator=gen, device=dev).to(torch.bfloat16)
     out = torch.empty_like(q)
-    plan = fpsa.FpsaPlan(grid, tile, win, H, d, tau=args.tau, device=dev)
-    flops = plan.flops  # per rank (one batch element, all heads)
+    if args.ulysses:
+        uly = UlyssesAttention(grid, tile, win, H, d, device=dev, tau=args.tau)
+        plan = uly.plan
+
+        def step(q_, k_, v_, out_):
+            out_.copy_(uly(q_, k_, v_))
+    else:
+        plan = fpsa.FpsaPlan(grid, tile, win, Hr, d, tau=args.tau, device=dev)
+
+        def step(q_, k_, v_, out_):
+            plan.quantize(q_, k_, v_, "lhd")
+            plan.attention(out_, "lhd")
+    flops = plan.flops  # this rank's heads
+    flops_total = plan.flops // plan.heads * H if not args.ulysses else plan.flops * world
 
     def barrier():
         if world > 1:
@@ -252,10 +279,10 @@ def main():
 
     stream = torch.cuda.current_stream()
     for _ in range(args.warmup):
-        plan.quantize(q, k, v, "lhd")
-        plan.attention(out, "lhd")
+        step(q, k, v, out)
     torch.cuda.synchronize()
     plan.check_finite()
+    redo = plan.redo_count()
 
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
            torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
@@ -267,9 +294,13 @@ def main():
         t0.record(stream)
         for i in range(args.steps):
             ev[i][0].record(stream)
-            plan.quantize(q, k, v, "lhd")
-            ev[i][1].record(stream)
-            plan.attention(out, "lhd")
+            if args.ulysses:
+                step(q, k, v, out)
+                ev[i][1].record(stream)
+            else:
+                plan.quantize(q, k, v, "lhd")
+                ev[i][1].record(stream)
+                plan.attention(out, "lhd")
             ev[i][2].record(stream)
         t1.record(stream)
         torch.cuda.synchronize()
@@ -282,7 +313,7 @@ def main():
         tt = torch.tensor([ms_step, ms_attn, ms_quant], device=dev, dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms_step, ms_attn, ms_quant = tt.tolist()
-    total_flops = flops * world
+    total_flops = flops_total
     value = total_flops / (ms_step * 1e-3) / 1e12
 
     # ---------------- e2e through the public API with pinned host buffers
@@ -294,7 +325,7 @@ def main():
         steps_e2e = max(3, min(args.steps, 10))
         for _ in range(2):
             qd.copy_(qh, non_blocking=True); kd.copy_(kh, non_blocking=True); vd.copy_(vh, non_blocking=True)
-            plan(qd, kd, vd, "lhd", out=out)
+            step(qd, kd, vd, out)
             oh.copy_(out, non_blocking=True)
         torch.cuda.synchronize()
         barrier()
@@ -302,7 +333,7 @@ def main():
         s.record(stream)
         for _ in range(steps_e2e):
             qd.copy_(qh, non_blocking=True); kd.copy_(kh, non_blocking=True); vd.copy_(vh, non_blocking=True)
-            plan(qd, kd, vd, "lhd", out=out)
+            step(qd, kd, vd, out)
             oh.copy_(out, non_blocking=True)
         e.record(stream)
         torch.cuda.synchronize()
@@ -315,7 +346,8 @@ def main():
         e2e = {"value": total_flops / (ms_e2e * 1e-3) / 1e12, "unit": "TFLOPS", "ms_per_step": ms_e2e,
                "h2d_bytes_per_step": 3 * q.numel() * q.element_size(),
                "d2h_bytes_per_step": out.numel() * out.element_size(),
-               "api": "paper_2506_04648_b200.FpsaPlan.__call__ (quantize + attention via the C ABI), pinned host"}
+               "api": ("paper_2506_04648_b200.UlyssesAttention.__call__" if args.ulysses else
+                       "paper_2506_04648_b200.FpsaPlan.quantize + .attention") + " via the C ABI, pinned host"}
 
     if rank != 0:
         if world > 1:
@@ -329,9 +361,9 @@ def main():
     else:
         peak = 2.0 * float(peaks.get("bf16_tflops", 1590.0))
         peak_src = "2 x measured bf16 dense (MEASURED_PEAKS.json)"
-    attn_tflops = flops / (ms_attn * 1e-3) / 1e12
+    attn_tflops = flops / (ms_attn * 1e-3) / 1e12 if not args.ulysses else None
     # quantiser: algorithmic bytes = bf16 q,k,v read once + e4m3 codes written (9 B per element)
-    qbytes = 3 * L * H * d * 2 + 3 * L * H * d
+    qbytes = 3 * L * Hr * d * 2 + 3 * L * Hr * d
     hbm = float(peaks.get("hbm_gbs", 6650.0))
     line = {
         "metric": METRIC,
@@ -342,23 +374,25 @@ def main():
         "warmup": args.warmup,
         "ms_per_step": ms_step,
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong",
         "vs_baseline": None,
         "dtype": "e4m3",
         "data": "synthetic (torch.randn bf16 q/k/v, natural (t,h,w) token order)",
         "config": {
             "workload": args.config, "grid": grid, "heads": H, "d": d, "tile": tile, "window": win,
-            "density": plan.density, "global_batch": world, "per_gpu_batch": 1,
-            "flops_per_step_per_gpu": flops, "tau_log2": args.tau,
-            "parallelism": f"head-parallel x batch, {world} rank(s), no collective",
+            "density": plan.density, "global_batch": 1, "heads_per_gpu": Hr if not args.ulysses else H // world,
+            "flops_per_step": total_flops, "flops_per_step_rank0": flops, "tau_log2": args.tau,
+            "parallelism": (f"ulysses: sequence-sharded inputs, NCCL all-to-all seq<->head, {world} ranks"
+                            if args.ulysses else f"head-parallel, {world} rank(s), no collective"),
             "l2": "inputs larger than L2 (bf16 q,k,v = %.2f GB per rank; codes %.2f GB)" % (
                 3 * q.numel() * 2 / 1e9, 3 * plan.q_codes.numel() / 1e9),
         },
         "ms_attention": ms_attn,
         "ms_quantize": ms_quant,
-        "frac_fp8_spec": attn_tflops / FP8_SPEC_TFLOPS,
+        "redo_items": redo,
+        "frac_fp8_spec": attn_tflops / FP8_SPEC_TFLOPS if attn_tflops else None,
         "step_frac_fp8_spec": value / world / FP8_SPEC_TFLOPS,
-        "roofline": {
+        "roofline": None if args.ulysses else {
             "bound": "tensor", "kernel": "fpsa_attn_kernel", "achieved": attn_tflops, "peak": peak,
             "unit": "TFLOP/s", "frac": attn_tflops / peak, "peak_source": peak_src,
             "traffic": ncu_traffic(args.config),
@@ -370,15 +404,15 @@ def main():
             "frac": qbytes / (ms_quant * 1e-3) / 1e9 / hbm, "algorithmic_bytes": qbytes,
         },
         "clocks": clocks.summary(),
-        "gpu_launches": 3 * args.steps,
+        "gpu_launches": 4 * args.steps,  # chan_amax + quant_tma + fpsa_attn (main + exact redo) per step
         "e2e": e2e,
     }
     if world == 1 and not args.no_cpu:
         cb = cpu_leg(CONFIGS[args.config], args.cpu_seconds)
         line["cpu_baseline"] = {
             "value": cb["flops"] / cb["seconds"] / 1e12, "unit": "TFLOPS", "cores": os.cpu_count(), "kind": "port",
-            "sample": f"{cb['tiles']} of {cb['M']} query tiles of 1 of {H} heads (oracle port of "
-                      f"fp8sta.fp8_sparse_forward, numpy, thread pool), {cb['seconds']:.1f} s",
+            "sample": f"{cb['passes']} pass(es) over all {cb['M']} query tiles of 1 of {H} heads (oracle port of "
+                      f"fp8sta.fp8_sparse_forward, numpy, thread pool over tiles), {cb['seconds']:.1f} s",
         }
     print(json.dumps(line))
     if world > 1:

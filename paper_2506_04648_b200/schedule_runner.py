@@ -1,0 +1,147 @@
+"""Denoising-step driver: per-step (tile, window) from the schedule, one device plan per regime.
+
+Mirrors the reference's per-step loop (fp8sta/experiment.py:178-201: for t
+in 1..D, ``params_at(t)`` picks the regime's tile and window, schedule.py:71-73)
+for the GPU hot path.  Each regime gets one ``FpsaPlan`` (window CSR, work
+list and FP8 buffers built once) and, optionally, one CUDA graph of its
+quantise + attention launches, so a step is a single graph replay.  Rows
+follow the reference CSV schema (experiment.py:25-28) plus timing columns;
+the fidelity columns need an fp32 reference of the full problem and are
+left empty (nan) at video scale.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+from .fp8 import E4M3, Fp8Format
+from .grid import GridShape, build_tile_map
+from .metrics import flops_dense, flops_sparse
+from .ops import FpsaPlan
+from .schedule import ScheduleConfig, params_at, validate
+from .sparsity import build_block_mask, density
+
+CSV_HEADER = (
+    "step,regime,tile_t,tile_h,tile_w,win_t,win_h,win_w,"
+    "density,flops_dense,flops_sparse,cosine_sim,mse,snr_db,ms,eff_tflops"
+)
+
+
+@dataclass(frozen=True)
+class StepRow:
+    step: int
+    regime: str
+    tile: tuple[int, int, int]
+    window: tuple[int, int, int]
+    density: float
+    flops_dense: int  # per head, as the reference reports it
+    flops_sparse: int
+    ms: float  # all heads, quantise + attention
+    eff_tflops: float  # flops_sparse * heads / ms
+
+
+class ScheduleRunner:
+    """Runs the hot path for every sampling step of a schedule on [L, H, d] bf16 inputs."""
+
+    def __init__(self, grid: tuple[int, int, int], schedule: ScheduleConfig, heads: int, d: int,
+                 fmt: Fp8Format = E4M3, device="cuda", use_graphs: bool = True, tau: float = 8.0):
+        problems = validate(schedule)
+        if problems:
+            raise ValueError("invalid schedule: " + "; ".join(problems))
+        self.grid = tuple(int(x) for x in grid)
+        self.schedule, self.heads, self.d = schedule, int(heads), int(d)
+        self.fmt, self.device, self.use_graphs, self.tau = fmt, device, use_graphs, tau
+        self._plans: dict = {}
+        self._graphs: dict = {}
+        gshape = GridShape(*self.grid, self.d)
+        for regime in ("early", "mid", "late"):  # reject indivisible tiles up front (grid.py:95-99)
+            build_tile_map(gshape, schedule.params(regime).tile)
+
+    def plan(self, regime: str) -> FpsaPlan:
+        p = self._plans.get(regime)
+        if p is None:
+            rp = self.schedule.params(regime)
+            p = FpsaPlan(self.grid, rp.tile.dims, rp.window, self.heads, self.d, self.fmt, device=self.device,
+                         tau=self.tau)
+            self._plans[regime] = p
+        return p
+
+    def step(self, t: int, q, k, v, out) -> str:
+        """Quantise + attend for sampling step t (1-based); returns the regime."""
+        regime = self.schedule.regime_of(t)
+        plan = self.plan(regime)
+        if not self.use_graphs:
+            plan.quantize(q, k, v, "lhd")
+            plan.attention(out, "lhd")
+            return regime
+        import torch
+
+        key = (regime, q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr())
+        g = self._graphs.get(key)
+        if g is None:
+            # warm the launch configuration outside the capture, then capture both launches
+            plan.quantize(q, k, v, "lhd")
+            plan.attention(out, "lhd")
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                plan.quantize(q, k, v, "lhd")
+                plan.attention(out, "lhd")
+            self._graphs[key] = g
+        g.replay()
+        return regime
+
+    def run(self, q, k, v, out, steps: int | None = None) -> list[StepRow]:
+        """All (or the first `steps`) sampling steps, each timed with CUDA events."""
+        import torch
+
+        D = self.schedule.total_steps if steps is None else min(steps, self.schedule.total_steps)
+        L = self.grid[0] * self.grid[1] * self.grid[2]
+        stream = torch.cuda.current_stream()
+        rows = []
+        for t in range(1, D + 1):
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record(stream)
+            regime = self.step(t, q, k, v, out)
+            e.record(stream)
+            e.synchronize()
+            ms = s.elapsed_time(e)
+            rp = self.schedule.params(regime)
+            plan = self._plans[regime]
+            dens = plan.density
+            rows.append(StepRow(step=t, regime=regime, tile=rp.tile.dims, window=rp.window.dims, density=dens,
+                                flops_dense=flops_dense(L, self.d), flops_sparse=flops_sparse(L, self.d, dens),
+                                ms=ms, eff_tflops=plan.flops / (ms * 1e-3) / 1e12))
+        return rows
+
+
+def rows_to_csv(rows: list[StepRow]) -> str:
+    """Reference CSV schema (experiment.py:249-260) + ms and effective TFLOPS; fidelity columns nan."""
+    lines = [CSV_HEADER]
+    nan = math.nan
+    for r in rows:
+        lines.append(
+            f"{r.step},{r.regime},{r.tile[0]},{r.tile[1]},{r.tile[2]},{r.window[0]},{r.window[1]},{r.window[2]},"
+            f"{r.density!r},{r.flops_dense},{r.flops_sparse},{nan!r},{nan!r},{nan!r},{r.ms!r},{r.eff_tflops!r}")
+    return "\n".join(lines) + "\n"
+
+
+def c4_schedule(total_steps: int = 50) -> ScheduleConfig:
+    """BASELINE config 5 at the Wan2.1-14B 720p shape: a schedule validate() accepts."""
+    from .grid import TileScheme
+    from .schedule import RegimeParams
+    from .sparsity import WindowSpec
+
+    return ScheduleConfig(alpha1=0.2, alpha2=0.7,
+                          early=RegimeParams(TileScheme(7, 15, 16), WindowSpec(3, 3, 1)),
+                          mid=RegimeParams(TileScheme(3, 5, 16), WindowSpec(5, 5, 3)),
+                          late=RegimeParams(TileScheme(7, 9, 8), WindowSpec(3, 3, 3)),
+                          total_steps=total_steps)
+
+
+def schedule_density(grid, schedule: ScheduleConfig, t: int) -> float:
+    """Density of step t's window (host only; sparsity.py:141-144)."""
+    rp = params_at(t, schedule)
+    tmap = build_tile_map(GridShape(*grid, 1), rp.tile)
+    return density(build_block_mask(rp.window, tmap.tile_grid_dims))

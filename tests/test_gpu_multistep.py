@@ -1,0 +1,72 @@
+"""GPU tests of the drivers above the hot path: the schedule runner (CUDA graphs
+per regime) and the Ulysses sequence<->head path on a single-rank NCCL group."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def fpsa():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2506_04648_b200 as m
+
+    return m
+
+
+def _small_schedule(fpsa, D=10):
+    T, W, R = fpsa.TileScheme, fpsa.WindowSpec, fpsa.RegimeParams
+    # grid 6x10x32: tiles (6,10,16) tv 960 > (3,10,8) tv 240 > (3,5,16) tv 240? -> use (3,10,16) tv 480
+    return fpsa.ScheduleConfig(alpha1=0.2, alpha2=0.6, early=R(T(6, 10, 16), W(1, 1, 1)),
+                               mid=R(T(3, 5, 16), W(3, 3, 3)), late=R(T(3, 10, 16), W(2, 1, 2)), total_steps=D)
+
+
+def test_schedule_runner_graphs_match_eager(fpsa):
+    grid, H, d = (6, 10, 32), 2, 128
+    sc = _small_schedule(fpsa)
+    assert fpsa.validate(sc) == []
+    L = grid[0] * grid[1] * grid[2]
+    g = torch.Generator(device="cuda").manual_seed(3)
+    q, k, v = (torch.randn((L, H, d), generator=g, device="cuda").to(torch.bfloat16) for _ in range(3))
+    eager = fpsa.ScheduleRunner(grid, sc, H, d, use_graphs=False)
+    graph = fpsa.ScheduleRunner(grid, sc, H, d, use_graphs=True)
+    for t in range(1, sc.total_steps + 1):
+        a, b = torch.empty_like(q), torch.empty_like(q)
+        ra = eager.step(t, q, k, v, a)
+        rb = graph.step(t, q, k, v, b)
+        assert ra == rb == sc.regime_of(t)
+        ref = fpsa.fps_attention(q, k, v, grid, fpsa.params_at(t, sc).tile.dims, fpsa.params_at(t, sc).window,
+                                 layout="lhd")
+        assert torch.equal(a, ref) and torch.equal(b, ref)
+    rows = graph.run(q, k, v, torch.empty_like(q))
+    assert [r.regime for r in rows] == [sc.regime_of(t) for t in range(1, 11)]
+    csv = fpsa.rows_to_csv(rows)
+    assert csv.splitlines()[0].startswith("step,regime,tile_t,tile_h,tile_w,win_t,win_h,win_w,density")
+    assert len(csv.splitlines()) == 11
+
+
+def test_ulysses_single_rank_matches_plan(fpsa):
+    import torch.distributed as dist
+
+    if not dist.is_initialized():
+        with socket.socket() as s:
+            s.bind(("127.0.0.1", 0))
+            port = s.getsockname()[1]
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ["MASTER_PORT"] = str(port)
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    grid, tile, win, H, d = (6, 10, 32), (3, 5, 16), (3, 3, 3), 4, 128
+    L = grid[0] * grid[1] * grid[2]
+    g = torch.Generator(device="cuda").manual_seed(9)
+    q, k, v = (torch.randn((L, H, d), generator=g, device="cuda").to(torch.bfloat16) for _ in range(3))
+    uly = fpsa.UlyssesAttention(grid, tile, win, H, d, device="cuda")
+    out = uly(q, k, v)
+    ref = fpsa.fps_attention(q, k, v, grid, tile, win, layout="lhd")
+    assert torch.equal(out, ref)
+    dist.destroy_process_group()
