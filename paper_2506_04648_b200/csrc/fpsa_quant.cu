@@ -492,8 +492,11 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
   for (int32_t it = blockIdx.x; it < n_items; it += gridDim.x, ++k) {
     const int st = k % kTmaStages;
     const int32_t z = it / per_job, rem = it - z * per_job, h = rem / g.M, u = rem - h * g.M;
-    const bool channel = a.channel[z] != 0;
-    uint8_t* out_tile = a.codes[z] + ((int64_t)h * g.M + u) * g.pitch * kTmaD;
+    // select, do not index: a dynamically indexed parameter array is copied to local memory
+    const bool channel = (z == 0 ? a.channel[0] : z == 1 ? a.channel[1] : a.channel[2]) != 0;
+    uint8_t* const codes = z == 0 ? a.codes[0] : z == 1 ? a.codes[1] : a.codes[2];
+    double* const scales = z == 0 ? a.scales[0] : z == 1 ? a.scales[1] : a.scales[2];
+    uint8_t* out_tile = codes + ((int64_t)h * g.M + u) * g.pitch * kTmaD;
     uint8_t* out = out_tile + lane * VEC;
     const uint2* tile = reinterpret_cast<const uint2*>(smem + st * kTmaStageBytes) + lane;
     mbar_wait(&full[st], (k / kTmaStages) & 1);
@@ -525,14 +528,14 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
         pk[e] = peak;
         b[e] = bb;
       }
-      if (warp == 0 && lane == 0) a.scales[z][(int64_t)h * g.M + u] = scale_of(peak, kMax);
+      if (warp == 0 && lane == 0) scales[(int64_t)h * g.M + u] = scale_of(peak, kMax);
     } else {
 #pragma unroll
       for (int e = 0; e < VEC; ++e) {
         const float peak = __uint_as_float(a.amax[(int64_t)h * kTmaD + lane * VEC + e]);
         pk[e] = peak <= FLT_MAX ? peak : 0.0f;
         b[e] = bracket_f32<FMT>(pk[e]);
-        if (u == 0 && warp == 0) a.scales[z][(int64_t)h * kTmaD + lane * VEC + e] = scale_of(pk[e], kMax);
+        if (u == 0 && warp == 0) scales[(int64_t)h * kTmaD + lane * VEC + e] = scale_of(pk[e], kMax);
       }
     }
     bool fast_ok = true;
