@@ -57,18 +57,24 @@ namespace {
 
 using namespace sm100;
 
-constexpr int kSoftmaxWarps = 8;
+#ifndef FPSA_ROW_PARTS
+#define FPSA_ROW_PARTS 2
+#endif
+constexpr int kParts = FPSA_ROW_PARTS;          // softmax warps sharing one TMEM lane quarter (row)
+constexpr int kPartCols = 128 / kParts;         // S columns per softmax thread
+constexpr int kSoftmaxWarps = 4 * kParts;
 constexpr int kTmaWarp = kSoftmaxWarps;
 constexpr int kMmaWarp = kSoftmaxWarps + 1;
-constexpr int kThreads = (kSoftmaxWarps + 4) * 32;  // 3 warpgroups: 2 softmax, 1 producer (TMA, MMA, 2 idle)
+constexpr int kThreads = (kSoftmaxWarps + 4) * 32;  // softmax warpgroups + 1 producer (TMA, MMA, 2 idle)
 // setmaxnreg split of the 64K-register file: per SMSP one warp of each warpgroup
-constexpr uint32_t kRegsSoftmax = 224, kRegsProducer = 56;
+// (kParts 4 was measured slower on B200: 13.4 vs 12.8 ms at C2; 112/64 deadlocks in setmaxnreg.inc)
+constexpr uint32_t kRegsSoftmax = kParts == 2 ? 224 : 104, kRegsProducer = kParts == 2 ? 56 : 64;
 
 constexpr int kStages = 4;     // K/V ring depth (128-key blocks)
 constexpr int kBlk = 128;      // rows per query block = keys per key block
 constexpr float kLog2_448 = 8.807354922057604f;
 constexpr int kRedoHeader = 4;  // int32 words before the redo items in the workspace
-constexpr int kFacCap = 256;    // key-tile factors per item kept in shared memory (more: read from L2)
+constexpr int kFacCap = 128;    // key-tile factors per item kept in shared memory (more: read from L2)
 
 struct AttnParams {
   const double* q_scales;
@@ -142,7 +148,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __shared__ uint64_t bar_kv_full[kStages], bar_kv_empty[kStages];
   __shared__ uint64_t bar_s_full[2], bar_p_ready[2];  // by S buffer / step parity
   __shared__ uint32_t s_tmem;
-  __shared__ float s_xchg[2][kBlk];  // [half][row] pair exchange
+  __shared__ float s_xchg[kParts][kBlk];  // [part][row] exchange between the warps of a row
   __shared__ float s_fac[kSoftmaxWarps][2][kFacCap];  // per softmax warp, per item parity: key-tile factors
   __shared__ uint32_t s_ovf[2];      // per item parity: some row overflowed
 
@@ -278,8 +284,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 #endif
         tc_fence_after();
         if (s >= pv0) {
-          // [O|l] += P~ [V|1]: P~ of keys 64c..64c+63 sits in the first 16 columns of S half c;
-          // the B descriptor's leading byte offset points from V at the ones atom
+          // [O|l] += P~ [V|1]: P~ of the keys of row part c sits in the first columns of that part's
+          // S columns; the B descriptor's leading byte offset points from V at the ones atom
           if (s == pv0 && iter > 0) {
             mbar_wait(&bar_ofree, (iter - 1) & 1);  // the previous item's epilogue has read O
             tc_fence_after();
@@ -289,7 +295,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 #ifndef FPSA_NO_MMA
 #pragma unroll
           for (int k = 0; k < kBlk / 32; ++k)
-            mma_f8_ts_w(tm_o, ts + 64 * (k >> 1) + 8 * (k & 1), dv + (uint64_t)k * (32 * D / 16), idesc_pv,
+            mma_f8_ts_w(tm_o, ts + kPartCols * (32 * k / kPartCols) + 8 * (k % (kPartCols / 32)),
+                        dv + (uint64_t)k * (32 * D / 16), idesc_pv,
                         (s > pv0 || k > 0) ? 1u : 0u);
 #endif
         }
@@ -307,19 +314,21 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp < kSoftmaxWarps) {
     regs_inc<kRegsSoftmax>();
-    // ------------------------------------------------------------ softmax: (row, column half)
+    // ------------------------------------------------------------ softmax: (row, column part)
     const int quarter = warp & 3;
-    const int half = warp >> 2;              // S columns [64 half, 64 half + 64)
+    const int part = warp >> 2;              // S columns [kPartCols part, kPartCols (part + 1))
     const int row = quarter * 32 + lane;     // TMEM lane = row of the query block
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
-    const uint32_t o_addr = tm_o + lane_off + half * (D / 2);
+    const uint32_t o_addr = tm_o + lane_off + part * (D / kParts);
     const float sl = p.softmax_log2;
-    auto pair_sync = [&]() { named_bar_sync(1 + quarter, 64); };
-    auto pair_max = [&](float m) {  // max over both halves of the row
-      s_xchg[half][row] = m;
-      pair_sync();
-      const float r = fmaxf(s_xchg[0][row], s_xchg[1][row]);
-      pair_sync();  // the exchange slots are reused
+    auto row_sync = [&]() { named_bar_sync(1 + quarter, 32 * kParts); };
+    auto row_max = [&](float m) {  // max over all parts of the row
+      s_xchg[part][row] = m;
+      row_sync();
+      float r = s_xchg[0][row];
+#pragma unroll
+      for (int i = 1; i < kParts; ++i) r = fmaxf(r, s_xchg[i][row]);
+      row_sync();  // the exchange slots are reused
       return r;
     };
     uint32_t g = 0;
@@ -353,10 +362,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         float c = factor_at(0);
         for (int32_t j = 0; j < n_kv; ++j, ++g) {
           const bool tail = b == p.nb - 1;
-          const int ncol = (tail ? p.n_tail : kBlk) - kHalf * half;
-          const int ncol_h = min(max(ncol, 0), kHalf);
-          const bool pad8 = tail && p.tail_pad8 && ncol > 0 && ncol <= kHalf;
-          const uint32_t s_addr = tm_s(g) + lane_off + half * kHalf;
+          const int ncol = (tail ? p.n_tail : kBlk) - kPartCols * part;
+          const int ncol_h = min(max(ncol, 0), kPartCols);
+          const bool pad8 = tail && p.tail_pad8 && ncol > 0 && ncol <= kPartCols;
+          const uint32_t s_addr = tm_s(g) + lane_off + part * kPartCols;
           // next step's factor, loaded while this step waits / computes
           const int32_t kt_next = tail ? kt + 1 : kt;
           const float c_next = (tail && kt_next < n_kt) ? factor_at(kt_next) : c;
@@ -373,19 +382,20 @@ __global__ void __launch_bounds__(kThreads, 1)
 #endif
           tc_fence_after();
           if (pass == 0) {
-            m_acc = fmaxf(m_acc, block_max(s_addr, ncol_h, pad8) * c);
+            m_acc = fmaxf(m_acc, block_max<kPartCols>(s_addr, ncol_h, pad8) * c);
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&bar_p_ready[g & 1]);  // S consumed
           } else {
-            if (j == 0 && !p.exact) m_ref = pair_max(block_max(s_addr, ncol_h, pad8)) * c;
-            uint32_t w[kHalf / 4];
-            sat |= softmax_block(s_addr, ncol_h, pad8, c, kLog2_448 - m_ref - tau, w);
+            if (j == 0 && !p.exact) m_ref = row_max(block_max<kPartCols>(s_addr, ncol_h, pad8)) * c;
+            uint32_t w[kPartCols / 4];
+            sat |= softmax_block<kPartCols>(s_addr, ncol_h, pad8, c, kLog2_448 - m_ref - tau, w);
 #ifdef FPSA_TRACE
             w_c += clock64() - tc0;
 #endif
             FPSA_TL(warp, 2, g);
-            tmem_st16(s_addr, w);
+            if constexpr (kPartCols == 64) tmem_st16(s_addr, w);
+            else tmem_st8(s_addr, w);
             tmem_wait_st();
             tc_fence_before();
             __syncwarp();
@@ -400,7 +410,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             ++b;
           }
         }
-        if (pass == 0) m_ref = pair_max(m_acc);
+        if (pass == 0) m_ref = row_max(m_acc);
       }
 #ifdef FPSA_TRACE
       t_loop += clock64() - tl0;
@@ -425,26 +435,29 @@ __global__ void __launch_bounds__(kThreads, 1)
         token = (int64_t)u * p.tv + r;
       }
       const double* vs = p.v_scales + (int64_t)h * D;
+      static_assert(D / kParts >= 16, "each softmax thread stores at least 16 output channels");
 #pragma unroll
-      for (int cc = 0; cc < D / 2; cc += 32) {
-        const int col = half * (D / 2) + cc;
+      for (int cc = 0; cc < D / kParts; cc += 32) {
+        const int col = part * (D / kParts) + cc;
         uint32_t o[32];
-        tmem_ld32(o_addr + cc, o);
+        if constexpr (D / kParts >= 32) tmem_ld32(o_addr + cc, o);
+        else tmem_ld16(o_addr + cc, *reinterpret_cast<uint32_t(*)[16]>(o));
         tmem_wait_ld();
+        constexpr int kN = D / kParts >= 32 ? 32 : 16;
         if (r < p.tv) {
           float f[32];
 #pragma unroll
-          for (int i = 0; i < 32; ++i) f[i] = __uint_as_float(o[i]) * inv_l * (float)__ldg(vs + col + i);
+          for (int i = 0; i < kN; ++i) f[i] = __uint_as_float(o[i]) * inv_l * (float)__ldg(vs + col + i);
           if constexpr (OUT == FPSA_F32) {
             float4* dst =
                 reinterpret_cast<float4*>(static_cast<float*>(p.out) + token * p.out_ts + h * p.out_hs + col);
 #pragma unroll
-            for (int i = 0; i < 8; ++i) dst[i] = make_float4(f[4 * i], f[4 * i + 1], f[4 * i + 2], f[4 * i + 3]);
+            for (int i = 0; i < kN / 4; ++i) dst[i] = make_float4(f[4 * i], f[4 * i + 1], f[4 * i + 2], f[4 * i + 3]);
           } else {
             uint4* dst = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.out) + token * p.out_ts +
                                                   h * p.out_hs + col);
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
+            for (int i = 0; i < kN / 8; ++i) {
               uint32_t wv[4];
 #pragma unroll
               for (int k2 = 0; k2 < 4; ++k2) {

@@ -168,57 +168,63 @@ __device__ __forceinline__ void softmax_chunk(uint32_t* s, int ncol, bool pad8, 
 
 // Nonzero iff some packed e4m3 code is 0x7E (448, the saturation value): P~ >= 0
 // so codes are <= 0x7E, and adding 2 to each byte sets its top bit only for 0x7E.
+template <int NC>
 __device__ __forceinline__ uint32_t saturated(const uint32_t* w) {
   uint32_t a = 0u;
 #pragma unroll
-  for (int i = 0; i < kHalf / 4; i += 2) a |= (w[i] + 0x02020202u) | (w[i + 1] + 0x02020202u);
+  for (int i = 0; i < NC / 4; i += 2) a |= (w[i] + 0x02020202u) | (w[i + 1] + 0x02020202u);
   return a & 0x80808080u;
 }
 
-// One half row of one key block: 64 S columns from TMEM, ncol (multiple of
-// 16, 0..64) valid, P~ words of absent columns zero.  The row sum of P~ is
-// not taken here: the PV MMA accumulates it in the "ones" columns of O.
-// Returns nonzero if some P~ reached the e4m3 saturation value.
+// One row part of one key block: NC (64 or 32) S columns from TMEM, ncol
+// (multiple of 16, 0..NC) valid, P~ words of absent columns zero.  The row
+// sum of P~ is not taken here: the PV MMA accumulates it in the "ones"
+// columns of O.  Returns nonzero if some P~ reached the e4m3 saturation value.
+template <int NC>
 __device__ __forceinline__ uint32_t softmax_block(uint32_t s_addr, int ncol, bool pad8, float c, float boff,
                                                   uint32_t* w) {
   const f2 cc = bcast(c), bb = bcast(boff);
   const float cs = c * (1.0f / 256.0f), bs = (boff + 126.0f) * (1.0f / 256.0f);
   uint32_t sa[32], sb[32];
-  if (ncol == kHalf && !pad8) {
-    // common case: all 64 columns valid, one load wait and a single basic block of
-    // 64 independent elements for the scheduler
+  if (ncol == NC && !pad8) {
+    // common case: all columns valid, no guards around the 32-column chunks
 #ifdef FPSA_TRACE
     const long long tl0 = clock64();
 #endif
-    // 32 columns at a time: fewer live S registers leave the scheduler room for
-    // distinct MUFU source registers (a reused source serialises on the XU queue)
     tmem_ld32(s_addr, sa);
     tmem_wait_ld();
 #ifdef FPSA_TRACE
     if ((threadIdx.x & 31) == 0) atomicAdd(&g_trace[4], (unsigned long long)(clock64() - tl0));
 #endif
     softmax_chunk32<0>(sa, cc, bb, cs, bs, w);
-    tmem_ld32(s_addr + 32, sb);
-    tmem_wait_ld();
-    softmax_chunk32<1>(sb, cc, bb, cs, bs, w);
+    if constexpr (NC == 64) {
+      tmem_ld32(s_addr + 32, sb);
+      tmem_wait_ld();
+      softmax_chunk32<1>(sb, cc, bb, cs, bs, w);
+    }
   } else {
     if (ncol > 0) {
       tmem_ld32(s_addr, sa);
       tmem_wait_ld();
     }
-    if (ncol > 32) tmem_ld32(s_addr + 32, sb);
+    if constexpr (NC == 64) {
+      if (ncol > 32) tmem_ld32(s_addr + 32, sb);
+    }
     softmax_chunk<0>(sa, ncol, pad8, cc, bb, cs, bs, w);
-    if (ncol > 32) tmem_wait_ld();
-    softmax_chunk<1>(sb, ncol, pad8, cc, bb, cs, bs, w);
+    if constexpr (NC == 64) {
+      if (ncol > 32) tmem_wait_ld();
+      softmax_chunk<1>(sb, ncol, pad8, cc, bb, cs, bs, w);
+    }
   }
-  return saturated(w);
+  return saturated<NC>(w);
 }
 
-// Max of the first ncol (0..64) raw S values of a half row (-inf if none).
+// Max of the first ncol (0..NC) raw S values of a row part (-inf if none).
+template <int NC>
 __device__ __forceinline__ float block_max(uint32_t s_addr, int ncol, bool pad8) {
   float m0 = -INFINITY, m1 = -INFINITY;
 #pragma unroll
-  for (int base = 0; base < kHalf; base += 32) {
+  for (int base = 0; base < NC; base += 32) {
     if (base < ncol) {
       uint32_t s[32];
       tmem_ld32(s_addr + base, s);

@@ -1,1 +1,6 @@
-timeout -s KILL 300 python bench.py --steps 10 --warmup 3 --no-cpu --no-e2e > gpurun_out/bench_r1v.json 2> gpurun_out/bench_r1v.err
+timeout -s KILL 60 python -c "
+import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_r1x.txt 2>&1; echo "EXIT $?" >> gpurun_out/smoke_r1x.txt
+if grep -q "smoke ok" gpurun_out/smoke_r1x.txt; then
+timeout -s KILL 300 python -m pytest tests -x -q -m gpu -p no:cacheprovider --timeout 60 > gpurun_out/tests_r1x.txt 2>&1; echo "EXIT $?" >> gpurun_out/tests_r1x.txt
+timeout -s KILL 120 python bench.py --steps 10 --warmup 3 --no-cpu --no-e2e > gpurun_out/bench_r1x.json 2> gpurun_out/bench_r1x.err
+fi
