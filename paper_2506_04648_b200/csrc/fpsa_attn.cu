@@ -68,13 +68,14 @@ constexpr int kMmaWarp = kSoftmaxWarps + 1;
 constexpr int kThreads = (kSoftmaxWarps + 4) * 32;  // softmax warpgroups + 1 producer (TMA, MMA, 2 idle)
 // setmaxnreg split of the 64K-register file: per SMSP one warp of each warpgroup
 // (kParts 4 was measured slower on B200: 13.4 vs 12.8 ms at C2; 112/64 deadlocks in setmaxnreg.inc)
-constexpr uint32_t kRegsSoftmax = kParts == 2 ? 224 : 104, kRegsProducer = kParts == 2 ? 56 : 64;
+constexpr uint32_t kRegsSoftmax = kParts == 2 ? 216 : 104, kRegsProducer = 64;
 
 constexpr int kStages = 4;     // K/V ring depth (128-key blocks)
 constexpr int kBlk = 128;      // rows per query block = keys per key block
 constexpr float kLog2_448 = 8.807354922057604f;
 constexpr int kRedoHeader = 4;  // int32 words before the redo items in the workspace
-constexpr int kFacCap = 128;    // key-tile factors per item kept in shared memory (more: read from L2)
+constexpr int kFacCap = 512;    // key-tile factors per item kept in shared memory (more: read from L2)
+constexpr int kHelperWarp = kSoftmaxWarps + 2;  // producer-warpgroup warp that prefetches item metadata
 
 struct AttnParams {
   const double* q_scales;
@@ -149,7 +150,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   __shared__ uint64_t bar_s_full[2], bar_p_ready[2];  // by S buffer / step parity
   __shared__ uint32_t s_tmem;
   __shared__ float s_xchg[kParts][kBlk];  // [part][row] exchange between the warps of a row
-  __shared__ float s_fac[kSoftmaxWarps][2][kFacCap];  // per softmax warp, per item parity: key-tile factors
+  // per-item metadata, prefetched by the helper warp one item ahead (slot = item parity)
+  __shared__ float s_fac[2][kFacCap];  // key-tile factors c(kt) = (sq * sk) * scale log2 e
+  __shared__ float s_vsc[2][D];        // V channel scales
+  __shared__ int32_t s_hdr[2][4];      // kt0, n_kt, unused, unused
+  __shared__ uint64_t bar_meta_full[2], bar_meta_empty[2];
   __shared__ uint32_t s_ovf[2];      // per item parity: some row overflowed
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -166,6 +171,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     mbar_init(&bar_o, 1);
     mbar_init(&bar_ofree, kSoftmaxWarps);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&bar_meta_full[i], 1);
+      mbar_init(&bar_meta_empty[i], kSoftmaxWarps);
+    }
     for (int i = 0; i < kStages; ++i) {
       mbar_init(&bar_kv_full[i], 1);
       mbar_init(&bar_kv_empty[i], 1);
@@ -312,6 +321,28 @@ __global__ void __launch_bounds__(kThreads, 1)
       mma_commit_w(&bar_o);
       g += steps;
     }
+  } else if (warp == kHelperWarp) {
+    // ------------------------------------------------------------ metadata prefetch (one item ahead)
+    const float sl = p.softmax_log2;
+    int32_t iter = 0;
+    for (int32_t it = blockIdx.x; it < count; it += gridDim.x, ++iter) {
+      const int slot = iter & 1;
+      if (iter >= 2) mbar_wait(&bar_meta_empty[slot], ((iter >> 1) - 1) & 1);
+      const int32_t h = items[3 * it], u = items[3 * it + 1];
+      const int32_t kt0 = __ldg(p.offs + u), n_kt = __ldg(p.offs + u + 1) - kt0;
+      const float qs = (float)__ldg(p.q_scales + h * p.M + u);
+      const double* ks = p.k_scales + (int64_t)h * p.M;
+      // c(kt) = f32(f32(sq) * f32(sk)) * f32(scale log2 e), the oracle's factor order
+      for (int32_t i = lane; i < min(n_kt, kFacCap); i += 32)
+        s_fac[slot][i] = (qs * (float)__ldg(ks + __ldg(p.ids + kt0 + i))) * sl;
+      for (int i = lane; i < D; i += 32) s_vsc[slot][i] = (float)__ldg(p.v_scales + (int64_t)h * D + i);
+      if (lane == 0) {
+        s_hdr[slot][0] = kt0;
+        s_hdr[slot][1] = n_kt;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bar_meta_full[slot]);  // release: the writes above are visible to waiters
+    }
   } else if (warp < kSoftmaxWarps) {
     regs_inc<kRegsSoftmax>();
     // ------------------------------------------------------------ softmax: (row, column part)
@@ -339,17 +370,16 @@ __global__ void __launch_bounds__(kThreads, 1)
 #endif
     for (int32_t it = blockIdx.x; it < count; it += gridDim.x, ++iter) {
       const int32_t h = items[3 * it], u = items[3 * it + 1], qb = items[3 * it + 2];
-      const int32_t kt0 = __ldg(p.offs + u), n_kt = __ldg(p.offs + u + 1) - kt0;
+      const int slot = iter & 1;
+      mbar_wait(&bar_meta_full[slot], (iter >> 1) & 1);
+      const int32_t kt0 = s_hdr[slot][0], n_kt = s_hdr[slot][1];
       const int32_t n_kv = n_kt * p.nb;
-      const float qs = (float)__ldg(p.q_scales + h * p.M + u);
-      const double* ks = p.k_scales + (int64_t)h * p.M;
-      // c(kt) = f32(f32(sq) * f32(sk)) * f32(scale log2 e), the oracle's factor order
-      auto factor = [&](int32_t kt) { return (qs * (float)__ldg(ks + __ldg(p.ids + kt0 + kt))) * sl; };
-      // this warp's copy of the item's factors: one round of L2 latency per item, not per key tile
-      float* fac = s_fac[warp][iter & 1];
-      for (int32_t i = lane; i < min(n_kt, kFacCap); i += 32) fac[i] = factor(i);
-      __syncwarp();
-      auto factor_at = [&](int32_t kt) { return kt < kFacCap ? fac[kt] : factor(kt); };
+      const float* fac = s_fac[slot];
+      auto factor_at = [&](int32_t kt) {
+        if (kt < kFacCap) return fac[kt];
+        const float qs = (float)__ldg(p.q_scales + h * p.M + u);  // windows beyond kFacCap tiles: from L2
+        return (qs * (float)__ldg(p.k_scales + (int64_t)h * p.M + __ldg(p.ids + kt0 + kt))) * sl;
+      };
       float m_ref = 0.0f;
       uint32_t sat = 0u;
 #ifdef FPSA_TRACE
@@ -434,7 +464,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       } else {
         token = (int64_t)u * p.tv + r;
       }
-      const double* vs = p.v_scales + (int64_t)h * D;
+      const float* vs = s_vsc[slot];
       static_assert(D / kParts >= 16, "each softmax thread stores at least 16 output channels");
 #pragma unroll
       for (int cc = 0; cc < D / kParts; cc += 32) {
@@ -447,7 +477,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (r < p.tv) {
           float f[32];
 #pragma unroll
-          for (int i = 0; i < kN; ++i) f[i] = __uint_as_float(o[i]) * inv_l * (float)__ldg(vs + col + i);
+          for (int i = 0; i < kN; ++i) f[i] = __uint_as_float(o[i]) * inv_l * vs[col + i];
           if constexpr (OUT == FPSA_F32) {
             float4* dst =
                 reinterpret_cast<float4*>(static_cast<float*>(p.out) + token * p.out_ts + h * p.out_hs + col);
@@ -471,7 +501,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&bar_ofree);
+      if (lane == 0) {
+        mbar_arrive(&bar_ofree);
+        mbar_arrive(&bar_meta_empty[slot]);  // this item's metadata slot may be refilled
+      }
       if (!p.exact) {
         // items with a possibly saturated P~ are recomputed exactly by the redo launch
         if (__any_sync(0xffffffffu, sat != 0u) && lane == 0) atomicOr(&s_ovf[iter & 1], 1u);
