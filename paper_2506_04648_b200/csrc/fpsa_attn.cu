@@ -235,7 +235,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == kMmaWarp) {
     // ------------------------------------------------------------ MMA issuer (warp-uniform, one elected lane issues)
     constexpr uint32_t idesc_qk = idesc_f8(128, 128, FMT, FMT, 0);
-    const uint32_t idesc_qk_tail = idesc_f8(128, (uint32_t)p.n_tail, FMT, FMT, 0);
     constexpr uint32_t idesc_pv = idesc_f8(128, D + 16, FPSA_E4M3, FMT, 1);
     // Descriptors are built once; a K-chunk / stage step only moves the 14-bit
     // start-address field (16-byte units), which never carries out.
@@ -265,7 +264,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&bar_kv_full[qk_st], qk_ph);
         tc_fence_after();
         const uint64_t dk = dk0 + qk_st * kTileU;
-        const uint32_t idq = b2 == p.nb - 1 ? idesc_qk_tail : idesc_qk;
+        // N = 128 for every block: a tile's last block reads zero K rows past tv (S = 0 there,
+        // finite), which the softmax drops; below N = 256 an MMA costs the same at any N.
+        const uint32_t idq = idesc_qk;
         const uint32_t ts = tm_s(gg);
 #ifndef FPSA_NO_MMA
 #pragma unroll
@@ -419,7 +420,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           } else {
             if (j == 0 && !p.exact) m_ref = row_max(block_max<kPartCols>(s_addr, ncol_h, pad8)) * c;
             uint32_t w[kPartCols / 4];
-            sat |= softmax_block<kPartCols>(s_addr, ncol_h, pad8, c, kLog2_448 - m_ref - tau, w);
+            sat |= softmax_block_full<kPartCols>(s_addr, ncol_h, c, kLog2_448 - m_ref - tau, w);
 #ifdef FPSA_TRACE
             w_c += clock64() - tc0;
 #endif

@@ -23,6 +23,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 
 #include <cfloat>
@@ -791,7 +792,8 @@ extern "C" int fpsa_quantize_qkv(const void* q, const void* k, const void* v, in
     ta.amax = amax;
     ta.err = err_flag;
     const void* xs[3] = {q, k, v};
-    if (try_tma_quant(xs, 3, dtype, token_stride, head_stride, heads, g, d, fmt, ta, st))
+    static const bool no_tma = getenv("FPSA_QUANT_NO_TMA") != nullptr;  // measurement switch
+    if (!no_tma && try_tma_quant(xs, 3, dtype, token_stride, head_stride, heads, g, d, fmt, ta, st))
       return cuda_status("fpsa_quantize_qkv");
   }
   QuantArgs a{};

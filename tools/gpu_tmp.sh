@@ -1,6 +1,6 @@
-timeout -s KILL 60 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_r2a.txt 2>&1; echo "EXIT $?" >> gpurun_out/smoke_r2a.txt
-if grep -q "smoke ok" gpurun_out/smoke_r2a.txt; then
-timeout -s KILL 300 python -m pytest tests -x -q -m gpu -p no:cacheprovider --timeout 60 > gpurun_out/tests_r2a.txt 2>&1; echo "EXIT $?" >> gpurun_out/tests_r2a.txt
-timeout -s KILL 120 python bench.py --steps 10 --warmup 3 --no-cpu --no-e2e > gpurun_out/bench_r2a.json 2> gpurun_out/bench_r2a.err
-timeout -s KILL 120 python tools/trace_attn.py c2 > gpurun_out/trace_r2a.txt 2>&1
+timeout -s KILL 60 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_r2c.txt 2>&1; echo "EXIT $?" >> gpurun_out/smoke_r2c.txt
+if grep -q "smoke ok" gpurun_out/smoke_r2c.txt; then
+timeout -s KILL 300 python -m pytest tests -x -q -m gpu -p no:cacheprovider --timeout 60 > gpurun_out/tests_r2c.txt 2>&1; echo "EXIT $?" >> gpurun_out/tests_r2c.txt
+timeout -s KILL 120 python bench.py --steps 10 --warmup 3 --no-cpu --no-e2e > gpurun_out/bench_r2c.json 2> gpurun_out/bench_r2c.err
+timeout -s KILL 120 python tools/trace_attn.py c2 > gpurun_out/trace_r2c.txt 2>&1
 fi

@@ -24,7 +24,7 @@ using namespace fpsa;
 
 template <int MASK, bool SUM>
 __device__ __forceinline__ float pass64(uint32_t s_addr, float c, float boff, uint32_t* w) {
-  if (MASK == 1) return (float)softmax_block(s_addr, 64, false, c, boff, w);  // the kernel's entry point
+  if (MASK == 1) return (float)softmax_block<64>(s_addr, 64, false, c, boff, w);  // the kernel entry point
   const f2 cc = bcast(c), bb = bcast(boff);
   const float cs = c * (1.0f / 256.0f), bs = (boff + 126.0f) * (1.0f / 256.0f);
   uint32_t sa[32], sb[32];
@@ -99,9 +99,14 @@ template <int MASK, bool SUM, int SPIN = 0>
 __global__ void __launch_bounds__(320, 1) softmax_rate(int iters, long long* out, float* sink) {
   __shared__ uint32_t s_tmem;
   __shared__ uint64_t bar_done;
+  __shared__ uint64_t hs_full[2], hs_ready[2];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     mbar_init(&bar_done, 8);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&hs_full[i], 1);
+      mbar_init(&hs_ready[i], 8);
+    }
     fence_barrier_init();
   }
   if (warp == 8) {
@@ -126,6 +131,17 @@ __global__ void __launch_bounds__(320, 1) softmax_rate(int iters, long long* out
   } else if (SPIN == 3 && warp >= 8) {
     const uint32_t addr = smem_u32(&bar_done);
     while (!mbar_try_wait(addr, 0)) {
+    }
+  }
+  if (SPIN == 6 && warp == 9) {
+    // "MMA warp": after softmax step j completes, make S(j + 2) available
+    if (lane == 0) {
+      mbar_arrive(&hs_full[0]);
+      mbar_arrive(&hs_full[1]);
+      for (int j = 0; j < iters; ++j) {
+        mbar_wait(&hs_ready[j & 1], (j >> 1) & 1);
+        if (j + 2 < iters) mbar_arrive(&hs_full[j & 1]);
+      }
     }
   }
   if (SPIN && SPIN < 3 && warp >= 8) {
@@ -160,6 +176,10 @@ __global__ void __launch_bounds__(320, 1) softmax_rate(int iters, long long* out
     for (int it = 0; it < iters; ++it) {
       const uint32_t s_addr = base + 128 * (it & 1);
       uint32_t w[16];
+      if (SPIN == 6) {
+        mbar_wait(&hs_full[it & 1], (it >> 1) & 1);
+        tc_fence_after();
+      }
       if (SPIN == 4) named_bar_sync(1 + quarter, 64);  // the two halves of a row start each step together
       if (SPIN == 5) named_bar_sync(1, 256);           // all softmax warps start each step together
       l += pass64<MASK, SUM>(s_addr, c, boff, w);
@@ -167,6 +187,7 @@ __global__ void __launch_bounds__(320, 1) softmax_rate(int iters, long long* out
       tmem_wait_st();
       tc_fence_before();
       __syncwarp();
+      if (SPIN == 6 && lane == 0) mbar_arrive(&hs_ready[it & 1]);
     }
     t = clock64() - t0;
     if (lane == 0) mbar_arrive(&bar_done);
@@ -229,6 +250,7 @@ int main() {
   run<1, false>("kernel softmax_block (64 cols, sat check)", d, sink);
   run<1, false, 4>("  + pair lockstep (bar.sync 64 per step)", d, sink);
   run<1, false, 5>("  + all-warp lockstep (bar.sync 256 per step)", d, sink);
+  run<1, false, 6>("  + kernel-like mbarrier handshake per step", d, sink);
   run<0xAA, false, 1>("  + 2 warps spinning on try_wait", d, sink);
   run<0xAA, false, 2>("  + 2 warps try_wait w/ suspend hint", d, sink);
   run<0xAA, false, 3>("  + tensor core busy (QK SS + PV TS loop)", d, sink);

@@ -39,3 +39,8 @@ print("step | warp0: wait S-ready comp-end arrived | warp4: ... | MMA: p_ready-o
 for j in range(2, 40):
     w0 = T[j, 0] - t0; w4 = T[j, 4] - t0; w1 = T[j, 1] - t0; m = T[j, 9] - t0
     print(f"{j:3d} | {w0[0]:7d} {w0[1]:7d} {w0[2]:7d} {w0[3]:7d} | {w4[1]:7d} {w4[2]:7d} {w4[3]:7d} | w1 {w1[1]:7d} {w1[3]:7d} | {m[1]:7d} {m[2]:7d} {m[3]:7d}")
+
+print("per-warp compute+store time (S-ready -> arrived), steps 2..60 mean, by warp (SMSP = warp % 4):")
+for w in range(8):
+    d = [T[j, w, 3] - T[j, w, 1] for j in range(2, 60) if T[j, w, 3] > 0]
+    print(f"  warp {w} (SMSP {w % 4}): {np.mean(d):7.0f} clk")
