@@ -172,8 +172,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_init(&bar_o, 1);
     mbar_init(&bar_ofree, kSoftmaxWarps);
     for (int i = 0; i < 2; ++i) {
-      mbar_init(&bar_meta_full[i], 1);
-      mbar_init(&bar_meta_empty[i], kSoftmaxWarps);
+      mbar_init(&bar_meta_full[i], 32);                 // every helper lane releases its own writes
+      mbar_init(&bar_meta_empty[i], kSoftmaxWarps * 32);  // every softmax thread releases its reads
     }
     for (int i = 0; i < kStages; ++i) {
       mbar_init(&bar_kv_full[i], 1);
@@ -341,8 +341,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         s_hdr[slot][0] = kt0;
         s_hdr[slot][1] = n_kt;
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&bar_meta_full[slot]);  // release: the writes above are visible to waiters
+      mbar_arrive(&bar_meta_full[slot]);  // release: this lane's writes above are visible to waiters
     }
   } else if (warp < kSoftmaxWarps) {
     regs_inc<kRegsSoftmax>();
@@ -502,10 +501,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) {
-        mbar_arrive(&bar_ofree);
-        mbar_arrive(&bar_meta_empty[slot]);  // this item's metadata slot may be refilled
-      }
+      if (lane == 0) mbar_arrive(&bar_ofree);
+      mbar_arrive(&bar_meta_empty[slot]);  // this item's metadata slot may be refilled
       if (!p.exact) {
         // items with a possibly saturated P~ are recomputed exactly by the redo launch
         if (__any_sync(0xffffffffu, sat != 0u) && lane == 0) atomicOr(&s_ovf[iter & 1], 1u);

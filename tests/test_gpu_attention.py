@@ -110,3 +110,44 @@ def test_full_size_head_vs_oracle(fpsa, shape):
     print(f"{grid}: cos={cos:.6f} max-abs={mabs:.3e} rel={mabs / np.abs(ref).max():.3e}")
     assert cos >= COS_REF
     assert mabs <= 2e-2
+
+
+def test_exact_redo_path_forced(fpsa, attn_golden):
+    """tau = 0: every item whose later key blocks exceed the first block's max saturates e4m3 and is
+    recomputed by the exact-max launch; the result follows the oracle's emulation of that schedule."""
+    c = golden_cases(attn_golden)["tv240_d128"]
+    L = c["grid"][0] * c["grid"][1] * c["grid"][2]
+    tv = c["tile"][0] * c["tile"][1] * c["tile"][2]
+    q, k, v = O.gen_inputs(c["seed"], 1, 0, L, c["d"], c["dist"])
+    plan = fpsa.FpsaPlan(c["grid"], c["tile"], c["window"], 1, c["d"], tau=0.0)
+    out = torch.empty((L, c["d"]), dtype=torch.float32, device="cuda")
+    args = [torch.from_numpy(x).cuda() for x in (q, k, v)]
+    plan.quantize(*args, layout="ld", tile_order=True)
+    plan.attention(out, layout="ld", tile_order=True)
+    n_redo = plan.redo_count()
+    got = out.cpu().numpy()
+    offs, ids = O.window_lists(O.tile_grid_dims(c["grid"], c["tile"]), c["window"])
+    ref, codes = O.fp8_sparse_forward(q, k, v, tv, offs, ids)
+    emu, redo = O.onepass_forward(codes, tv, offs, ids, tau=0.0, poly=True, return_redo=True)
+    print(f"redo items: kernel {n_redo}, emulation {len(redo)} of {plan.n_items}; "
+          f"cos(emu)={O.cosine(got, emu):.7f} cos(ref)={O.cosine(got, ref):.6f}")
+    assert n_redo == len(redo) > 0
+    assert O.cosine(got, emu) >= COS_EMU
+    assert O.cosine(got, ref) >= COS_REF
+
+
+def test_full_size_head_large_tile(fpsa):
+    """The C4 early regime at the 14B 720p grid: tile (7,15,16) (1680 tokens, 14 key blocks), window (3,3,1)."""
+    grid, tile, win, d = (21, 45, 80), (7, 15, 16), (3, 3, 1), 128
+    L = grid[0] * grid[1] * grid[2]
+    tv = tile[0] * tile[1] * tile[2]
+    q, k, v = O.gen_inputs(5, 1, 0, L, d)
+    tmap = fpsa.build_tile_map(fpsa.GridShape(*grid, d), fpsa.TileScheme(*tile))
+    out = fpsa.fp8_sparse_forward(fpsa.AttentionInputs(q, k, v, tmap), fpsa.ForwardConfig(window=fpsa.WindowSpec(*win)))
+    offs, ids = O.window_lists(O.tile_grid_dims(grid, tile), win)
+    ref, codes = O.fp8_sparse_forward(q, k, v, tv, offs, ids)
+    cos = O.cosine(out, ref)
+    mabs = O.max_abs(out, ref)
+    print(f"tile {tile}: cos={cos:.6f} max-abs={mabs:.3e}")
+    assert cos >= COS_REF
+    assert mabs <= 2e-2
