@@ -385,54 +385,22 @@ __global__ void __launch_bounds__(kThreads, 1)
 #ifdef FPSA_TRACE
       const long long tl0 = clock64();
 #endif
-      for (int pass = p.exact ? 0 : 1; pass < 2; ++pass) {
+      if (p.exact) {
         // pass 0 (exact mode only): running max of x over all key blocks
         float m_acc = -INFINITY;
         int32_t kt = 0, b = 0;
-        float c = factor_at(0);
         for (int32_t j = 0; j < n_kv; ++j, ++g) {
           const bool tail = b == p.nb - 1;
           const int ncol = (tail ? p.n_tail : kBlk) - kPartCols * part;
           const int ncol_h = min(max(ncol, 0), kPartCols);
           const bool pad8 = tail && p.tail_pad8 && ncol > 0 && ncol <= kPartCols;
-          const uint32_t s_addr = tm_s(g) + lane_off + part * kPartCols;
-          // next step's factor, loaded while this step waits / computes
-          const int32_t kt_next = tail ? kt + 1 : kt;
-          const float c_next = (tail && kt_next < n_kt) ? factor_at(kt_next) : c;
-#ifdef FPSA_TRACE
-          const long long ts0 = clock64();
-#endif
-          FPSA_TL(warp, 0, g);
+          const float c = factor_at(kt);
           mbar_wait(&bar_s_full[g & 1], (g >> 1) & 1);
-          FPSA_TL(warp, 1, g);
-#ifdef FPSA_TRACE
-          w_s += clock64() - ts0;
-          const long long tc0 = clock64();
-          ++n_steps;
-#endif
           tc_fence_after();
-          if (pass == 0) {
-            m_acc = fmaxf(m_acc, block_max<kPartCols>(s_addr, ncol_h, pad8) * c);
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&bar_p_ready[g & 1]);  // S consumed
-          } else {
-            if (j == 0 && !p.exact) m_ref = row_max(block_max<kPartCols>(s_addr, ncol_h, pad8)) * c;
-            uint32_t w[kPartCols / 4];
-            sat |= softmax_block_full<kPartCols>(s_addr, ncol_h, c, kLog2_448 - m_ref - tau, w);
-#ifdef FPSA_TRACE
-            w_c += clock64() - tc0;
-#endif
-            FPSA_TL(warp, 2, g);
-            if constexpr (kPartCols == 64) tmem_st16(s_addr, w);
-            else tmem_st8(s_addr, w);
-            tmem_wait_st();
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&bar_p_ready[g & 1]);
-            FPSA_TL(warp, 3, g);
-          }
-          c = c_next;
+          m_acc = fmaxf(m_acc, block_max<kPartCols>(tm_s(g) + lane_off + part * kPartCols, ncol_h, pad8) * c);
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&bar_p_ready[g & 1]);  // S consumed
           if (tail) {
             b = 0;
             ++kt;
@@ -440,7 +408,69 @@ __global__ void __launch_bounds__(kThreads, 1)
             ++b;
           }
         }
-        if (pass == 0) m_ref = row_max(m_acc);
+        m_ref = row_max(m_acc);
+      }
+      {
+        // main pass, software-pipelined: block j's P~ store is in flight while
+        // block j+1's S is waited for and loaded
+        int32_t kt = 0, b = 0;
+        float c = factor_at(0);
+        uint32_t sreg[kPartCols];
+        auto ncol_of = [&](int32_t bb) {
+          return min(max((bb == p.nb - 1 ? p.n_tail : kBlk) - kPartCols * part, 0), kPartCols);
+        };
+        mbar_wait(&bar_s_full[g & 1], (g >> 1) & 1);
+        tc_fence_after();
+        if (!p.exact) {
+          // reference max = row max of the first key block (a tail block only when nb == 1)
+          const int raw0 = (p.nb == 1 ? p.n_tail : kBlk) - kPartCols * part;
+          const bool pad8 = p.nb == 1 && p.tail_pad8 && raw0 > 0 && raw0 <= kPartCols;
+          m_ref = row_max(block_max<kPartCols>(tm_s(g) + lane_off + part * kPartCols, ncol_of(0), pad8)) * c;
+        }
+        load_s_all<kPartCols>(tm_s(g) + lane_off + part * kPartCols, sreg);
+        tmem_wait_ld();
+        for (int32_t j = 0; j < n_kv; ++j, ++g) {
+#ifdef FPSA_TRACE
+          const long long tc0 = clock64();
+          ++n_steps;
+#endif
+          const bool tail = b == p.nb - 1;
+          uint32_t w[kPartCols / 4];
+          sat |= compute_p_regs<kPartCols>(sreg, ncol_of(b), c, kLog2_448 - m_ref - tau, w);
+#ifdef FPSA_TRACE
+          w_c += clock64() - tc0;
+#endif
+          FPSA_TL(warp, 2, g);
+          const uint32_t s_addr = tm_s(g) + lane_off + part * kPartCols;
+          if constexpr (kPartCols == 64) tmem_st16(s_addr, w);
+          else tmem_st8(s_addr, w);
+          if (tail) {
+            b = 0;
+            if (++kt < n_kt) c = factor_at(kt);
+          } else {
+            ++b;
+          }
+          const bool more = j + 1 < n_kv;
+          if (more) {
+#ifdef FPSA_TRACE
+            const long long ts0 = clock64();
+#endif
+            FPSA_TL(warp, 0, g + 1);
+            mbar_wait(&bar_s_full[(g + 1) & 1], ((g + 1) >> 1) & 1);
+            FPSA_TL(warp, 1, g + 1);
+#ifdef FPSA_TRACE
+            w_s += clock64() - ts0;
+#endif
+            tc_fence_after();
+            load_s_all<kPartCols>(tm_s(g + 1) + lane_off + part * kPartCols, sreg);
+          }
+          tmem_wait_st();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&bar_p_ready[g & 1]);
+          FPSA_TL(warp, 3, g);
+          if (more) tmem_wait_ld();
+        }
       }
 #ifdef FPSA_TRACE
       t_loop += clock64() - tl0;

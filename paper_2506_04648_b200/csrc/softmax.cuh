@@ -244,6 +244,28 @@ __device__ __forceinline__ uint32_t softmax_block_full(uint32_t s_addr, int ncol
   return saturated<NC>(w);
 }
 
+// Software-pipelined form: the row part's S is already in registers (s[0..NC)),
+// loaded while the previous block's P~ store was in flight.  Same math as
+// softmax_block_full.
+template <int NC>
+__device__ __forceinline__ void load_s_all(uint32_t s_addr, uint32_t* s) {
+  tmem_ld32(s_addr, s);
+  if constexpr (NC == 64) tmem_ld32(s_addr + 32, s + 32);
+}
+template <int NC>
+__device__ __forceinline__ uint32_t compute_p_regs(const uint32_t* s, int ncol, float c, float boff, uint32_t* w) {
+  const f2 cc = bcast(c), bb = bcast(boff);
+  const float cs = c * (1.0f / 256.0f), bs = (boff + 126.0f) * (1.0f / 256.0f);
+  softmax_chunk32<0>(s, cc, bb, cs, bs, w);
+  if constexpr (NC == 64) softmax_chunk32<1>(s + 32, cc, bb, cs, bs, w);
+  if (ncol < NC) {
+#pragma unroll
+    for (int i = 0; i < NC / 4; ++i)
+      if (4 * i >= ncol) w[i] = 0u;
+  }
+  return saturated<NC>(w);
+}
+
 // Max of the first ncol (0..NC) raw S values of a row part (-inf if none).
 template <int NC>
 __device__ __forceinline__ float block_max(uint32_t s_addr, int ncol, bool pad8) {
