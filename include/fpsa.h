@@ -145,6 +145,40 @@ int fpsa_attn_fwd(const uint8_t* q_codes, const uint8_t* k_codes, const uint8_t*
                   int64_t out_token_stride, int64_t out_head_stride, int out_order, void* workspace,
                   int64_t workspace_bytes, void* stream);
 
+/* ---------------------------------------------------------------- passthrough (full precision)
+ * The reference's passthrough branch / sparse_reference (fp8sta/attention.py:152-154,
+ * :165-176, :192-194): the same sliding-tile sparse attention without FP8
+ * quantisation, on bf16 operands with f32 softmax and accumulation. */
+
+/* Gather [tokens, heads, d] (f32 or bf16, tokens in in_order, element (t, h, c)
+ * at x + t*token_stride + h*head_stride + c) into the tile-major padded bf16
+ * layout [heads][M][tile_pitch][d] the passthrough kernel reads; rows
+ * tv..tile_pitch-1 of every tile are written as zero.  f32 is rounded to
+ * nearest even.  Replaces AttentionInputs' tile-contiguous f32 copies
+ * (fp8sta/attention.py:36-61) plus tile_contiguous_order (grid.py:132-154). */
+int fpsa_tile_gather_bf16(const void* x, int dtype, int64_t token_stride, int64_t head_stride, int32_t heads,
+                          fpsa_dims3 grid, fpsa_dims3 tile, int32_t d, int32_t tile_pitch, int in_order, void* out,
+                          void* stream);
+
+/* Passthrough attention over fpsa_tile_gather_bf16 buffers: for each query
+ * row, softmax(scale * q k^T) v over the keys of its window tiles, with the
+ * same work list, CSR, workspace, output layout and exact-max redo as
+ * fpsa_attn_fwd (the redo is needed only when a logit exceeds the first key
+ * block's row max by more than 127 / log2 e). */
+int fpsa_attn_bf16_fwd(const void* q_tiles, const void* k_tiles, const void* v_tiles, int32_t heads,
+                       fpsa_dims3 grid, fpsa_dims3 tile, int32_t d, int32_t tile_pitch, const int32_t* offs,
+                       const int32_t* ids, const int32_t* items, int32_t n_items, float softmax_scale, void* out,
+                       int out_dtype, int64_t out_token_stride, int64_t out_head_stride, int out_order,
+                       void* workspace, int64_t workspace_bytes, void* stream);
+
+/* Per-head fidelity sums of an approximation against a reference, both
+ * [tokens, heads, d] with the same strides (f32 or bf16):
+ * out (device, f64 [heads][6]) = sum(r a), sum(r r), sum(a a), sum((r-a)^2),
+ * max|r|, max|a|.  The inputs of cosine_similarity / mse / snr_db
+ * (fp8sta/metrics.py:41-88); the host finishes them. */
+int fpsa_fidelity(const void* ref, int ref_dtype, const void* approx, int approx_dtype, int64_t tokens,
+                  int32_t heads, int32_t d, int64_t token_stride, int64_t head_stride, double* out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -23,7 +23,7 @@ __all__ = [
     "tile_perm", "tile_grid_dims",
     "axis_interval", "window_lists", "density_of", "flops_sparse_of",
     "regime_of", "schedule_valid",
-    "fp8_sparse_forward", "sparse_forward_f32", "onepass_forward",
+    "fp8_sparse_forward", "sparse_forward_f32", "onepass_forward", "bf16_round", "passthrough_emulation",
     "cosine", "max_abs", "gen_inputs",
 ]
 
@@ -411,6 +411,49 @@ def onepass_forward(codes: dict, tv, offs, ids, fmt: Fmt = E4M3, softmax_scale=N
             out[rows] = o
     res = out.astype(np.float32)
     return (res, redo) if return_redo else res
+
+
+def bf16_round(x) -> np.ndarray:
+    """f32 -> nearest-even bfloat16, returned as f32 (finite inputs)."""
+    b = np.ascontiguousarray(x, dtype=np.float32).view(np.uint32).astype(np.uint64)
+    b = (b + 0x7FFF + ((b >> 16) & 1)) & 0xFFFF0000
+    return b.astype(np.uint32).view(np.float32)
+
+
+def passthrough_emulation(q, k, v, tv, offs, ids, softmax_scale=None, block=128):
+    """Emulation of the GPU passthrough kernel's schedule (fpsa_attn_bf16.cu), NOT the reference.
+
+    Operands rounded to bf16; per 128-row work item the keys are visited in
+    `block`-key blocks (per key tile, the last block of a tile shorter); the
+    reference max m of a row is the max of its first key block (x units:
+    s * f32(scale log2 e)); P = 2^(x - m) is summed unrounded into l and
+    rounded to bf16 for the PV product; out = O / l.  (The kernel's exact-max
+    redo triggers only when l overflows f32, which these inputs never do.)
+    """
+    qv = bf16_round(q).astype(np.float64)
+    kv = bf16_round(k).astype(np.float64)
+    vv = bf16_round(v).astype(np.float64)
+    L, d = qv.shape
+    M = L // tv
+    c = float(np.float32(np.float32(_softmax_scale(d, softmax_scale)) * np.float32(1.4426950408889634)))
+    out = np.empty((L, d), dtype=np.float64)
+    for u in range(M):
+        blocks = [(vt * tv + b0, vt * tv + min(b0 + block, tv))
+                  for vt in ids[offs[u]:offs[u + 1]] for b0 in range(0, tv, block)]
+        for r0 in range(0, tv, 128):
+            rows = slice(u * tv + r0, u * tv + min(r0 + 128, tv))
+            qrows = qv[rows]
+            k0, k1 = blocks[0]
+            m = (qrows @ kv[k0:k1].T).astype(np.float32).max(axis=1).astype(np.float64) * c
+            lsum = np.zeros(qrows.shape[0])
+            acc = np.zeros((qrows.shape[0], d))
+            for k0, k1 in blocks:
+                x = (qrows @ kv[k0:k1].T).astype(np.float32).astype(np.float64) * c - m[:, None]
+                p = np.exp2(x).astype(np.float32)
+                lsum += p.sum(axis=1, dtype=np.float64)
+                acc += bf16_round(p).astype(np.float64) @ vv[k0:k1]
+            out[rows] = acc / lsum[:, None]
+    return out.astype(np.float32)
 
 
 # --------------------------------------------------------------------------

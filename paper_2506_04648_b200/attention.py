@@ -5,8 +5,9 @@ semantics of its inputs (single head, rows already tile-contiguous,
 fp8sta/attention.py:36-61 / :179-208) and runs quantisation and attention
 on the GPU.  numpy inputs give a numpy float32 result (a drop-in for the CPU
 path); CUDA tensor inputs give a CUDA tensor.  ``passthrough`` (the
-full-precision oracle branch) has no GPU kernel in this build and raises
-NotImplementedError -- there is no CPU fallback.
+full-precision branch, attention.py:192-194) runs the bf16 tcgen05 kernel
+(``PassthroughPlan``): operands rounded to bf16, softmax and accumulation in
+f32.  There is no CPU fallback.
 """
 
 from __future__ import annotations
@@ -95,8 +96,6 @@ def fp8_sparse_forward(inputs: AttentionInputs, config: ForwardConfig):
 
     from .ops import FpsaPlan
 
-    if config.passthrough:
-        raise NotImplementedError("passthrough (fp32 oracle branch) has no GPU kernel in this build")
     tmap = inputs.tile_map
     scale = _resolve_scale(config.softmax_scale, inputs.d_model)
     host = not _is_torch(inputs.q)
@@ -107,9 +106,16 @@ def fp8_sparse_forward(inputs: AttentionInputs, config: ForwardConfig):
         return t if t.dtype in (torch.float32, torch.bfloat16) else t.float()
 
     q, k, v = dev(inputs.q), dev(inputs.k), dev(inputs.v)
+    out = torch.empty((tmap.grid.tokens, inputs.d_model), dtype=torch.float32, device=q.device)
+    if config.passthrough:
+        from .ops import PassthroughPlan
+
+        pplan = PassthroughPlan(tmap.grid.dims, tmap.scheme.dims, config.window, 1, inputs.d_model, device=q.device)
+        pplan.gather(q, k, v, layout="ld", tile_order=True)
+        pplan.attention(out, layout="ld", tile_order=True, softmax_scale=float(scale))
+        return out.cpu().numpy() if host else out
     plan = FpsaPlan(tmap.grid.dims, tmap.scheme.dims, config.window, 1, inputs.d_model, config.fmt,
                     device=q.device, tau=config.tau)
-    out = torch.empty((tmap.grid.tokens, inputs.d_model), dtype=torch.float32, device=q.device)
     plan.quantize(q, k, v, layout="ld", tile_order=True)
     plan.attention(out, layout="ld", tile_order=True, softmax_scale=float(scale))
     plan.check_finite()

@@ -63,24 +63,16 @@ def worklist(heads: int, mask: BlockMask, tile_volume: int) -> np.ndarray:
     return items
 
 
-class FpsaPlan:
-    """Device buffers + launch parameters for one (grid, tile, window, heads, d, fmt).
+class _TilePlan:
+    """Shape-derived device state shared by the FP8 and passthrough plans:
+    tile grid, window CSR, work list and the attention workspace."""
 
-    Layouts accepted by :meth:`quantize` / :meth:`__call__`:
-      ``"lhd"``  [L, H, d]  (one sample of Wan's [B, L, H, d])
-      ``"hld"``  [H, L, d]
-      ``"ld"``   [L, d]     single head
-    in natural (t, h, w) token order, or with ``tile_order=True`` rows already
-    tile-contiguous (the reference's convention, fp8sta/attention.py:36-61).
-    """
-
-    def __init__(self, grid, tile, window, heads: int, d: int, fmt: Fp8Format = E4M3, *,
-                 device="cuda", tau: float = 8.0, pitch: int | None = None):
+    def __init__(self, grid, tile, window, heads: int, d: int, device, pitch: int | None):
         torch = _torch()
         self.grid = tuple(int(x) for x in grid)
         self.tile = tuple(int(x) for x in tile)
         self.window = window if isinstance(window, WindowSpec) else WindowSpec(*window)
-        self.heads, self.d, self.fmt, self.tau = int(heads), int(d), fmt, float(tau)
+        self.heads, self.d = int(heads), int(d)
         out = _lib.Dims3()
         _lib.check(_lib.lib().fpsa_tile_grid(_lib.dims3(self.grid), _lib.dims3(self.tile), out))
         self.tile_dims = (out.t, out.h, out.w)
@@ -96,18 +88,9 @@ class FpsaPlan:
         items = worklist(self.heads, self.mask, self.tv)
         self.n_items = items.size // 3
         self.items = torch.from_numpy(items).to(dev)
-        rows = self.heads * self.M * self.pitch
-        self.q_codes = torch.empty(rows * self.d, dtype=torch.uint8, device=dev)
-        self.k_codes = torch.empty_like(self.q_codes)
-        self.v_codes = torch.empty_like(self.q_codes)
-        self.q_scales = torch.empty(self.heads * self.M, dtype=torch.float64, device=dev)
-        self.k_scales = torch.empty_like(self.q_scales)
-        self.v_scales = torch.empty(self.heads * self.d, dtype=torch.float64, device=dev)
-        self.workspace = torch.empty(self.heads * self.d, dtype=torch.int32, device=dev)
         need = ctypes.c_int64(0)
         _lib.check(_lib.lib().fpsa_attn_workspace_bytes(self.n_items, ctypes.byref(need)))
         self.attn_ws = torch.zeros(-(-need.value // 4), dtype=torch.int32, device=dev)
-        self.err = torch.zeros(1, dtype=torch.int32, device=dev)
 
     # ------------------------------------------------------------------ accounting
     @property
@@ -118,6 +101,10 @@ class FpsaPlan:
     def flops(self) -> int:
         """Algorithmic FLOPs of one call: heads * sum_u |W(u)| * 4 tv^2 d (metrics.py:91-102)."""
         return self.heads * self.mask.nnz * 4 * self.tv * self.tv * self.d
+
+    def redo_count(self) -> int:
+        """Work items the last attention call recomputed in exact mode (synchronises)."""
+        return int(self.attn_ws[0].item())
 
     # ------------------------------------------------------------------ strides
     def _strides(self, x, layout: str):
@@ -138,6 +125,45 @@ class FpsaPlan:
                 raise ValueError(f"expected [L, d] = {(self.L, self.d)}, got {tuple(x.shape)}")
             return x.stride(0), 0
         raise ValueError(f"unknown layout {layout!r}")
+
+    def _out_args(self, out, layout: str, softmax_scale):
+        torch = _torch()
+        scale = np.float32(1.0 / math.sqrt(self.d)) if softmax_scale is None else np.float32(softmax_scale)
+        if not scale > 0:
+            raise ValueError("softmax_scale must be > 0")
+        ts, hs = self._strides(out, layout)
+        odt = {torch.float32: _lib.F32, torch.bfloat16: _lib.BF16}.get(out.dtype)
+        if odt is None:
+            raise NotImplementedError(f"output dtype {out.dtype} not supported")
+        return float(scale), odt, ts, hs
+
+
+class FpsaPlan(_TilePlan):
+    """Device buffers + launch parameters for one (grid, tile, window, heads, d, fmt).
+
+    Layouts accepted by :meth:`quantize` / :meth:`__call__`:
+      ``"lhd"``  [L, H, d]  (one sample of Wan's [B, L, H, d])
+      ``"hld"``  [H, L, d]
+      ``"ld"``   [L, d]     single head
+    in natural (t, h, w) token order, or with ``tile_order=True`` rows already
+    tile-contiguous (the reference's convention, fp8sta/attention.py:36-61).
+    """
+
+    def __init__(self, grid, tile, window, heads: int, d: int, fmt: Fp8Format = E4M3, *,
+                 device="cuda", tau: float = 8.0, pitch: int | None = None):
+        super().__init__(grid, tile, window, heads, d, device, pitch)
+        torch = _torch()
+        self.fmt, self.tau = fmt, float(tau)
+        dev = self.device
+        rows = self.heads * self.M * self.pitch
+        self.q_codes = torch.empty(rows * self.d, dtype=torch.uint8, device=dev)
+        self.k_codes = torch.empty_like(self.q_codes)
+        self.v_codes = torch.empty_like(self.q_codes)
+        self.q_scales = torch.empty(self.heads * self.M, dtype=torch.float64, device=dev)
+        self.k_scales = torch.empty_like(self.q_scales)
+        self.v_scales = torch.empty(self.heads * self.d, dtype=torch.float64, device=dev)
+        self.workspace = torch.empty(self.heads * self.d, dtype=torch.int32, device=dev)
+        self.err = torch.zeros(1, dtype=torch.int32, device=dev)
 
     # ------------------------------------------------------------------ kernels
     def quantize(self, q, k, v, layout: str = "lhd", tile_order: bool = False, stream=None) -> None:
@@ -167,25 +193,14 @@ class FpsaPlan:
     def attention(self, out, layout: str = "lhd", tile_order: bool = False, softmax_scale: float | None = None,
                   stream=None) -> None:
         """K4 over the quantised buffers; writes `out` (f32 or bf16)."""
-        torch = _torch()
-        scale = np.float32(1.0 / math.sqrt(self.d)) if softmax_scale is None else np.float32(softmax_scale)
-        if not scale > 0:
-            raise ValueError("softmax_scale must be > 0")
-        ts, hs = self._strides(out, layout)
-        odt = {torch.float32: _lib.F32, torch.bfloat16: _lib.BF16}.get(out.dtype)
-        if odt is None:
-            raise NotImplementedError(f"output dtype {out.dtype} not supported")
+        scale, odt, ts, hs = self._out_args(out, layout, softmax_scale)
         st = _stream() if stream is None else stream
         _lib.check(_lib.lib().fpsa_attn_fwd(
             _ptr(self.q_codes), _ptr(self.k_codes), _ptr(self.v_codes), _ptr(self.q_scales), _ptr(self.k_scales),
             _ptr(self.v_scales), self.heads, _lib.dims3(self.grid), _lib.dims3(self.tile), self.d, self.pitch,
-            _ptr(self.offs), _ptr(self.ids), _ptr(self.items), self.n_items, float(scale), self.fmt.abi_id,
+            _ptr(self.offs), _ptr(self.ids), _ptr(self.items), self.n_items, scale, self.fmt.abi_id,
             self.tau, _ptr(out), odt, ts, hs, _lib.ORDER_TILE if tile_order else _lib.ORDER_NATURAL,
             _ptr(self.attn_ws), self.attn_ws.numel() * 4, st))
-
-    def redo_count(self) -> int:
-        """Work items the last attention call recomputed in exact mode (synchronises)."""
-        return int(self.attn_ws[0].item())
 
     def check_finite(self) -> None:
         """Raise ValueError if a quantised input held a non-finite value (synchronises)."""
@@ -202,6 +217,84 @@ class FpsaPlan:
         self.quantize(q, k, v, layout, tile_order)
         self.attention(out, layout, tile_order, softmax_scale)
         return out
+
+class PassthroughPlan(_TilePlan):
+    """Full-precision sliding-tile sparse attention (the reference's passthrough /
+    sparse_reference, fp8sta/attention.py:152-154, :165-176, :192-194) on bf16
+    operands: :meth:`gather` lays q, k, v out tile-major in bf16, :meth:`attention`
+    runs the tcgen05 kind::f16 kernel.  Same layouts and work list as FpsaPlan."""
+
+    def __init__(self, grid, tile, window, heads: int, d: int, *, device="cuda", pitch: int | None = None):
+        super().__init__(grid, tile, window, heads, d, device, pitch)
+        torch = _torch()
+        rows = self.heads * self.M * self.pitch
+        self.q_tiles = torch.empty((rows, self.d), dtype=torch.bfloat16, device=self.device)
+        self.k_tiles = torch.empty_like(self.q_tiles)
+        self.v_tiles = torch.empty_like(self.q_tiles)
+
+    def gather(self, q, k, v, layout: str = "lhd", tile_order: bool = False, stream=None) -> None:
+        """q, k, v -> tile-major padded bf16 (f32 inputs rounded to nearest even)."""
+        L = _lib.lib()
+        st = _stream() if stream is None else stream
+        order = _lib.ORDER_TILE if tile_order else _lib.ORDER_NATURAL
+        g, t = _lib.dims3(self.grid), _lib.dims3(self.tile)
+        for x, dst in ((q, self.q_tiles), (k, self.k_tiles), (v, self.v_tiles)):
+            ts, hs = self._strides(x, layout)
+            _lib.check(L.fpsa_tile_gather_bf16(_ptr(x), _dtype_id(x), ts, hs, self.heads, g, t, self.d, self.pitch,
+                                               order, _ptr(dst), st))
+
+    def attention(self, out, layout: str = "lhd", tile_order: bool = False, softmax_scale: float | None = None,
+                  stream=None) -> None:
+        """Passthrough attention over the gathered tiles; writes `out` (f32 or bf16)."""
+        scale, odt, ts, hs = self._out_args(out, layout, softmax_scale)
+        st = _stream() if stream is None else stream
+        _lib.check(_lib.lib().fpsa_attn_bf16_fwd(
+            _ptr(self.q_tiles), _ptr(self.k_tiles), _ptr(self.v_tiles), self.heads, _lib.dims3(self.grid),
+            _lib.dims3(self.tile), self.d, self.pitch, _ptr(self.offs), _ptr(self.ids), _ptr(self.items),
+            self.n_items, scale, _ptr(out), odt, ts, hs, _lib.ORDER_TILE if tile_order else _lib.ORDER_NATURAL,
+            _ptr(self.attn_ws), self.attn_ws.numel() * 4, st))
+
+    def __call__(self, q, k, v, layout: str = "lhd", out=None, out_dtype=None, tile_order: bool = False,
+                 softmax_scale: float | None = None):
+        torch = _torch()
+        if out is None:
+            dt = out_dtype or (q.dtype if q.dtype in (torch.float32, torch.bfloat16) else torch.float32)
+            out = torch.empty(q.shape, dtype=dt, device=q.device)
+        self.gather(q, k, v, layout, tile_order)
+        self.attention(out, layout, tile_order, softmax_scale)
+        return out
+
+
+def device_fidelity(ref, approx, layout: str = "lhd", stream=None) -> list[tuple[float, float, float]]:
+    """Per-head (cosine, mse, snr_db) of `approx` against `ref`.
+
+    [L, H, d] / [H, L, d] / [L, d] CUDA tensors, f32 or bf16, same shape and
+    strides; reduced on the device (fpsa_fidelity) and finished like
+    fp8sta/metrics.py:41-88.  Synchronises.
+    """
+    torch = _torch()
+    if tuple(ref.shape) != tuple(approx.shape) or ref.stride() != approx.stride():
+        raise ValueError("ref and approx must have the same shape and strides")
+    if ref.stride(-1) != 1:
+        raise ValueError("channel dimension must be contiguous")
+    if layout == "lhd":
+        tokens, heads, d = ref.shape
+        ts, hs = ref.stride(0), ref.stride(1)
+    elif layout == "hld":
+        heads, tokens, d = ref.shape
+        ts, hs = ref.stride(1), ref.stride(0)
+    elif layout == "ld":
+        (tokens, d), heads = ref.shape, 1
+        ts, hs = ref.stride(0), 0
+    else:
+        raise ValueError(f"unknown layout {layout!r}")
+    sums = torch.empty((heads, 6), dtype=torch.float64, device=ref.device)
+    st = _stream() if stream is None else stream
+    _lib.check(_lib.lib().fpsa_fidelity(_ptr(ref), _dtype_id(ref), _ptr(approx), _dtype_id(approx), tokens, heads, d,
+                                        ts, hs, _ptr(sums), st))
+    from .metrics import fidelity_from_sums
+
+    return [fidelity_from_sums(*row, n=tokens * d) for row in sums.cpu().tolist()]
 
 
 _PLANS: dict = {}

@@ -250,3 +250,34 @@ def test_device_calls_reject_bad_arguments_before_cuda(lib):
                            None, _lib.F32, 64, 0, _lib.ORDER_TILE, None, 0, None)
     assert st == _lib.FPSA_EINVAL
     assert lib.fpsa_last_error()
+    # passthrough entry points
+    st = lib.fpsa_tile_gather_bf16(None, _lib.F32, 64, 0, 1, g, t, 64, 128, _lib.ORDER_TILE, None, None)
+    assert st == _lib.FPSA_EINVAL
+    st = lib.fpsa_tile_gather_bf16(None, _lib.F32, 48, 0, 1, g, t, 48, 128, _lib.ORDER_TILE, None, None)
+    assert st == _lib.FPSA_EINVAL  # NULL checked first
+    st = lib.fpsa_attn_bf16_fwd(None, None, None, 1, g, t, 64, 128, None, None, None, 1, 0.125, None, _lib.F32, 64,
+                                0, _lib.ORDER_TILE, None, 0, None)
+    assert st == _lib.FPSA_EINVAL
+    st = lib.fpsa_fidelity(None, _lib.F32, None, _lib.F32, 10, 1, 64, 64, 0, None, None)
+    assert st == _lib.FPSA_EINVAL
+
+
+def test_fidelity_from_sums_matches_reference_metrics(fpsa):
+    """Host finish of the device fidelity sums == fp8sta/metrics.py:41-88 conventions."""
+    import math
+
+    import oracle as O
+
+    rng = np.random.default_rng(3)
+    x = rng.standard_normal(4096)
+    y = x + 1e-2 * rng.standard_normal(4096)
+    sums = (float(x @ y), float(x @ x), float(y @ y), float((x - y) @ (x - y)), float(abs(x).max()),
+            float(abs(y).max()))
+    cos, mse, snr = fpsa.fidelity_from_sums(*sums, n=x.size)
+    assert abs(cos - O.cosine(x, y)) < 1e-12
+    assert abs(mse - float(((x - y) ** 2).mean())) < 1e-15
+    assert abs(snr - 10 * math.log10((x @ x) / ((x - y) @ (x - y)))) < 1e-9
+    with pytest.raises(ValueError):  # all-zero reference: SNR undefined (metrics.py:77-78)
+        fpsa.fidelity_from_sums(0, 0, 0, 0, 0.0, 0.0, n=4)
+    assert fpsa.fidelity_from_sums(0, 1, 0, 1, 1.0, 0.0, n=4)[0] == 0.0  # one zero vector: cosine 0
+    assert fpsa.fidelity_from_sums(*sums[:3], 0.0, *sums[4:], n=x.size)[2] == math.inf

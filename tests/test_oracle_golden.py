@@ -194,6 +194,30 @@ def test_attention_vs_reference(attn_golden, name):
         assert O.max_abs(f32[rows], sref) <= 1e-5 * float(np.abs(sref).max())
 
 
+@pytest.mark.parametrize("name", CASE_NAMES)
+def test_passthrough_vs_reference(attn_golden, name):
+    """The oracle's full-precision branch == the reference's sparse_reference / passthrough
+    (attention.py:165-176, :192-194) on every golden case; the GPU passthrough kernel's
+    emulation (bf16 operands, first-block max, bf16 P) stays within bf16 error of it."""
+    c = golden_cases(attn_golden)[name]
+    L = c["grid"][0] * c["grid"][1] * c["grid"][2]
+    tv = c["tile"][0] * c["tile"][1] * c["tile"][2]
+    q, k, v = O.gen_inputs(c["seed"], 1, 0, L, c["d"], c["dist"])
+    offs, ids = O.window_lists(O.tile_grid_dims(c["grid"], c["tile"]), c["window"])
+    rows = attn_golden[name + "__rows"]
+    sref = attn_golden[name + "__sparse_ref"]
+    f32 = O.sparse_forward_f32(q, k, v, tv, offs, ids)
+    assert O.max_abs(f32[rows], sref) <= 1e-5 * float(np.abs(sref).max())
+    # bf16 operands: logit error ~ |s| 2^-9, largest for the heavy-tailed inputs (3.5e-2 rel there)
+    emu = O.passthrough_emulation(q, k, v, tv, offs, ids)
+    assert O.cosine(emu[rows], sref) >= 0.9999
+    assert O.max_abs(emu[rows], sref) <= 5e-2 * float(np.abs(sref).max())
+    # on bf16-exact inputs only the bf16 rounding of P remains
+    rb = O.sparse_forward_f32(O.bf16_round(q), O.bf16_round(k), O.bf16_round(v), tv, offs, ids)
+    assert O.cosine(emu, rb) >= 0.999995
+    assert O.max_abs(emu, rb) <= 5e-3 * float(np.abs(rb).max())
+
+
 def test_attention_row_stochastic_and_full_window_dense():
     """Full window == dense attention; exactly representable inputs are lossless in Q/K/V."""
     L, d, tv = 64, 16, 16
