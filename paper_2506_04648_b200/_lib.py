@@ -12,7 +12,7 @@ import os
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libfpsa.so")
+LIB_PATH = os.path.join(_HERE, os.environ.get("FPSA_LIB", "libfpsa.so"))  # FPSA_LIB: in-tree variant (experiments)
 
 FPSA_OK = 0
 FPSA_EINVAL = 1

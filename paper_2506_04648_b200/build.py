@@ -50,6 +50,13 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
 
 if __name__ == "__main__":
+    if "--variant" in sys.argv:  # python -m ...build --variant NAME -DFOO=1 ...: in-tree libfpsa_NAME.so
+        i = sys.argv.index("--variant")
+        name, defs = sys.argv[i + 1], [a for a in sys.argv[i + 2:] if a.startswith("-D")]
+        target = os.path.join(HERE, f"libfpsa_{name}.so")
+        subprocess.run([nvcc(), *NVCC_FLAGS, *defs, *SOURCES, "-o", target], cwd=HERE, check=True)
+        print(target)
+        sys.exit(0)
     if "--trace" in sys.argv:
         print(build_trace())
         if "--nomma" in sys.argv:  # timing experiment: tensor core idle (results invalid)

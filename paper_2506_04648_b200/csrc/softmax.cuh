@@ -130,9 +130,14 @@ __device__ __forceinline__ void softmax_unit(const uint32_t* s, f2 cc, f2 bb, fl
   }
 }
 
-// All 32 columns of chunk C (P words w[8C..8C+7]): in each group of 4 keys,
-// columns 0 and 1 on MUFU ex2 (one FFMA2 forms both arguments from an
-// adjacent register pair), columns 2 and 3 on the FMA-pipe polynomial.
+// All 32 columns of chunk C (P words w[8C..8C+7]), in groups of 4 keys:
+// columns 0 and 1 always on MUFU ex2 (one FFMA2 forms both arguments from an
+// adjacent register pair); columns 2 and 3 on the FMA-pipe polynomial in every
+// group (FPSA_POLY_PER8 == 4, the default), in every other group (2: columns
+// 6 and 7 of each 8), or never (0).  oracle.fpsa_oracle._poly_columns mirrors it.
+#ifndef FPSA_POLY_PER8
+#define FPSA_POLY_PER8 2
+#endif
 template <int C>
 __device__ __forceinline__ void softmax_chunk32(const uint32_t* s, f2 cc, f2 bb, float cs, float bs, uint32_t* w) {
 #pragma unroll
@@ -140,7 +145,15 @@ __device__ __forceinline__ void softmax_chunk32(const uint32_t* s, f2 cc, f2 bb,
     const float* v = reinterpret_cast<const float*>(s + 4 * q);
     f2 m = fma2(f2{v[0], v[1]}, cc, bb);
     m = f2{ex2(m.x), ex2(m.y)};
-    const f2 pp = exp2_poly_sat(f2{fma_sat(v[2], cs, bs), fma_sat(v[3], cs, bs)});
+    constexpr int kPer8 = FPSA_POLY_PER8;
+    const bool poly = kPer8 == 4 || (kPer8 == 2 && (q & 1));
+    f2 pp;
+    if (poly) {
+      pp = exp2_poly_sat(f2{fma_sat(v[2], cs, bs), fma_sat(v[3], cs, bs)});
+    } else {
+      pp = fma2(f2{v[2], v[3]}, cc, bb);
+      pp = f2{ex2(pp.x), ex2(pp.y)};
+    }
     w[8 * C + q] = e4m3x4(m, pp);
   }
 }
