@@ -187,13 +187,24 @@ __device__ __forceinline__ uint32_t encode_fast(const float (&v)[VEC], const Bra
   return clo;
 }
 
+// Scalar arguments, not array references: a reference to a register array forces
+// the caller to keep that array in local memory around every call site.
 template <int FMT, int VEC>
-__device__ __noinline__ uint32_t encode_slow(const float (&v)[VEC], const float (&peak)[VEC]) {
+__device__ __noinline__ uint32_t encode_slow4(float v0, float v1, float v2, float v3, float p0, float p1, float p2,
+                                              float p3) {
   constexpr double kMax = FMT == FPSA_E4M3 ? 448.0 : 57344.0;
+  const float v[4] = {v0, v1, v2, v3}, peak[4] = {p0, p1, p2, p3};
   uint32_t c = 0;
 #pragma unroll
   for (int e = 0; e < VEC; ++e) c |= encode_exact<FMT>(v[e], scale_of(peak[e], kMax)) << (8 * e);
   return c;
+}
+template <int FMT, int VEC>
+__device__ __forceinline__ uint32_t encode_slow(const float (&v)[VEC], const float (&peak)[VEC]) {
+  if constexpr (VEC == 4)
+    return encode_slow4<FMT, 4>(v[0], v[1], v[2], v[3], peak[0], peak[1], peak[2], peak[3]);
+  else
+    return encode_slow4<FMT, 2>(v[0], v[1], 0.0f, 0.0f, peak[0], peak[1], 0.0f, 0.0f);
 }
 
 template <int VEC>
