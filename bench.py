@@ -321,20 +321,29 @@ def main():
     if not args.no_e2e:
         qh, kh, vh = (x.cpu().pin_memory() for x in (q, k, v))
         oh = torch.empty(out.shape, dtype=out.dtype).pin_memory()
-        qd, kd, vd = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
         steps_e2e = max(3, min(args.steps, 10))
+        if args.ulysses:
+            qd, kd, vd = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
+
+            def e2e_step():
+                qd.copy_(qh, non_blocking=True); kd.copy_(kh, non_blocking=True); vd.copy_(vh, non_blocking=True)
+                step(qd, kd, vd, out)
+                oh.copy_(out, non_blocking=True)
+        else:
+            # head chunks: the H2D of chunk c+1 and the D2H of chunk c-1 overlap chunk c's kernels
+            streamer = fpsa.HostStreamer(grid, tile, win, Hr, d, chunk_heads=max(1, Hr // 8), tau=args.tau,
+                                         device=dev)
+
+            def e2e_step():
+                streamer(qh, kh, vh, oh)
         for _ in range(2):
-            qd.copy_(qh, non_blocking=True); kd.copy_(kh, non_blocking=True); vd.copy_(vh, non_blocking=True)
-            step(qd, kd, vd, out)
-            oh.copy_(out, non_blocking=True)
+            e2e_step()
         torch.cuda.synchronize()
         barrier()
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record(stream)
         for _ in range(steps_e2e):
-            qd.copy_(qh, non_blocking=True); kd.copy_(kh, non_blocking=True); vd.copy_(vh, non_blocking=True)
-            step(qd, kd, vd, out)
-            oh.copy_(out, non_blocking=True)
+            e2e_step()
         e.record(stream)
         torch.cuda.synchronize()
         barrier()
@@ -347,7 +356,8 @@ def main():
                "h2d_bytes_per_step": 3 * q.numel() * q.element_size(),
                "d2h_bytes_per_step": out.numel() * out.element_size(),
                "api": ("paper_2506_04648_b200.UlyssesAttention.__call__" if args.ulysses else
-                       "paper_2506_04648_b200.FpsaPlan.quantize + .attention") + " via the C ABI, pinned host"}
+                       "paper_2506_04648_b200.HostStreamer.__call__ (FpsaPlan.quantize + .attention per head chunk, "
+                       "fpsa_copy2d transfers overlapped)") + " via the C ABI, pinned host"}
 
     if rank != 0:
         if world > 1:

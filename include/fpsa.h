@@ -179,6 +179,15 @@ int fpsa_attn_bf16_fwd(const void* q_tiles, const void* k_tiles, const void* v_t
 int fpsa_fidelity(const void* ref, int ref_dtype, const void* approx, int approx_dtype, int64_t tokens,
                   int32_t heads, int32_t d, int64_t token_stride, int64_t head_stride, double* out, void* stream);
 
+/* Strided 2D copy (cudaMemcpy2DAsync, direction from the pointers): `rows`
+ * rows of `width` bytes, row r from src + r*src_pitch to dst + r*dst_pitch.
+ * Used by the streamed host path to move a run of heads of every token
+ * between a pinned host [tokens, heads, d] array and a device
+ * [tokens, chunk, d] buffer (the reference copies its inputs into f32
+ * contiguous arrays, fp8sta/attention.py:50-57). */
+int fpsa_copy2d(void* dst, int64_t dst_pitch, const void* src, int64_t src_pitch, int64_t width, int64_t rows,
+                void* stream);
+
 #ifdef __cplusplus
 }
 #endif

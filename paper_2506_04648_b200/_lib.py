@@ -67,6 +67,7 @@ SIGNATURES = {
     "fpsa_attn_bf16_fwd": (_c.c_int, [_vp, _vp, _vp, _i32, Dims3, Dims3, _i32, _i32, _vp, _vp, _vp, _i32, _f32, _vp,
                                       _c.c_int, _i64, _i64, _c.c_int, _vp, _i64, _vp]),
     "fpsa_fidelity": (_c.c_int, [_vp, _c.c_int, _vp, _c.c_int, _i64, _i32, _i32, _i64, _i64, _vp, _vp]),
+    "fpsa_copy2d": (_c.c_int, [_vp, _i64, _vp, _i64, _i64, _i64, _vp]),
 }
 
 

@@ -8,7 +8,7 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 SOURCES = ["csrc/fpsa_attn.cu", "csrc/fpsa_attn_bf16.cu", "csrc/fpsa_quant.cu", "csrc/fpsa_metrics.cu",
-           "csrc/fpsa_host.cpp"]
+           "csrc/fpsa_io.cu", "csrc/fpsa_host.cpp"]
 HEADERS = ["csrc/sm100.cuh", "csrc/softmax.cuh", "csrc/fpsa_internal.h", "../include/fpsa.h"]
 TARGET = os.path.join(HERE, "libfpsa.so")
 NVCC_FLAGS = [

@@ -218,6 +218,93 @@ class FpsaPlan(_TilePlan):
         self.attention(out, layout, tile_order, softmax_scale)
         return out
 
+class HostStreamer:
+    """Quantise + attention of pinned host [L, H, d] tensors with transfers overlapped.
+
+    Heads are processed in chunks: while chunk c is quantised and attended on
+    the compute stream, chunk c+1's q, k, v travel host -> device on a copy
+    stream and chunk c-1's output device -> host on another (PCIe is full
+    duplex), through double-buffered device staging.  Per-head independence
+    (scales, windows and outputs are per head) is what makes
+    head chunks exact.  Transfers use fpsa_copy2d (strided rows: a chunk is a
+    run of heads of every token).  The call is asynchronous with respect to
+    the host and ordered on the caller's current stream: synchronising that
+    stream makes ``out_host`` complete.
+    """
+
+    def __init__(self, grid, tile, window, heads: int, d: int, fmt: Fp8Format = E4M3, *, chunk_heads: int = 5,
+                 device="cuda", tau: float = 8.0):
+        torch = _torch()
+        self.heads, self.d = int(heads), int(d)
+        self.chunk = max(1, min(int(chunk_heads), self.heads))
+        self.device = torch.device(device)
+        sizes = {min(self.chunk, self.heads - h0) for h0 in range(0, self.heads, self.chunk)}
+        self.plans = {hc: FpsaPlan(grid, tile, window, hc, d, fmt, device=self.device, tau=tau) for hc in sizes}
+        any_plan = next(iter(self.plans.values()))
+        self.L = any_plan.L
+        shape = (self.L, self.chunk, self.d)
+        self.stage_in = [[torch.empty(shape, dtype=torch.bfloat16, device=self.device) for _ in range(3)]
+                         for _ in range(2)]
+        self.stage_out = [torch.empty(shape, dtype=torch.bfloat16, device=self.device) for _ in range(2)]
+        self.s_in = torch.cuda.Stream(self.device)
+        self.s_out = torch.cuda.Stream(self.device)
+
+    @property
+    def flops(self) -> int:
+        p = next(iter(self.plans.values()))
+        return p.flops // p.heads * self.heads
+
+    def __call__(self, q_host, k_host, v_host, out_host) -> None:
+        torch = _torch()
+        for x in (q_host, k_host, v_host, out_host):
+            if x.device.type != "cpu" or not x.is_pinned() or not x.is_contiguous() or x.dtype != torch.bfloat16:
+                raise ValueError("host tensors must be pinned, contiguous bf16")
+            if tuple(x.shape) != (self.L, self.heads, self.d):
+                raise ValueError(f"expected [L, H, d] = {(self.L, self.heads, self.d)}, got {tuple(x.shape)}")
+        L = _lib.lib()
+        comp = torch.cuda.current_stream(self.device)
+        row = self.heads * self.d * 2  # host pitch (bytes)
+        ev_in_ready = [torch.cuda.Event() for _ in range(2)]
+        ev_in_free = [torch.cuda.Event() for _ in range(2)]
+        ev_out_ready = [torch.cuda.Event() for _ in range(2)]
+        ev_out_free = [torch.cuda.Event() for _ in range(2)]
+        start = torch.cuda.Event()
+        start.record(comp)
+        self.s_in.wait_event(start)
+        self.s_out.wait_event(start)
+        for c, h0 in enumerate(range(0, self.heads, self.chunk)):
+            b, hc = c % 2, min(self.chunk, self.heads - h0)
+            plan = self.plans[hc]
+            width = hc * self.d * 2
+            dpitch = self.chunk * self.d * 2
+            if c >= 2:
+                self.s_in.wait_event(ev_in_free[b])
+            for src, dst in zip((q_host, k_host, v_host), self.stage_in[b]):
+                _lib.check(L.fpsa_copy2d(_ptr(dst), dpitch, src.data_ptr() + h0 * self.d * 2, row, width, self.L,
+                                         self.s_in.cuda_stream))
+            ev_in_ready[b].record(self.s_in)
+            comp.wait_event(ev_in_ready[b])
+            qd, kd, vd = (t[:, :hc] for t in self.stage_in[b])
+            plan.quantize(qd, kd, vd, "lhd", stream=comp.cuda_stream)
+            ev_in_free[b].record(comp)
+            if c >= 2:
+                comp.wait_event(ev_out_free[b])
+            od = self.stage_out[b][:, :hc]
+            plan.attention(od, "lhd", stream=comp.cuda_stream)
+            ev_out_ready[b].record(comp)
+            self.s_out.wait_event(ev_out_ready[b])
+            _lib.check(L.fpsa_copy2d(out_host.data_ptr() + h0 * self.d * 2, row, _ptr(od), dpitch, width, self.L,
+                                     self.s_out.cuda_stream))
+            ev_out_free[b].record(self.s_out)
+        done = torch.cuda.Event()
+        done.record(self.s_out)
+        comp.wait_event(done)
+        # the staging buffers are reused by the next call: make the copy streams wait for this call's compute
+        done_c = torch.cuda.Event()
+        done_c.record(comp)
+        self.s_in.wait_event(done_c)
+
+
 class PassthroughPlan(_TilePlan):
     """Full-precision sliding-tile sparse attention (the reference's passthrough /
     sparse_reference, fp8sta/attention.py:152-154, :165-176, :192-194) on bf16

@@ -70,3 +70,23 @@ def test_ulysses_single_rank_matches_plan(fpsa):
     ref = fpsa.fps_attention(q, k, v, grid, tile, win, layout="lhd")
     assert torch.equal(out, ref)
     dist.destroy_process_group()
+
+
+def test_host_streamer_matches_plan(fpsa):
+    """Pinned-host streamed path (head chunks, overlapped transfers) == the device plan, bitwise,
+    with a chunk size that does not divide the head count."""
+    grid, tile, win, H, d = (6, 10, 32), (3, 5, 16), (3, 3, 3), 7, 128
+    L = grid[0] * grid[1] * grid[2]
+    gen = torch.Generator(device="cuda").manual_seed(9)
+    q, k, v = (torch.randn((L, H, d), generator=gen, device="cuda").to(torch.bfloat16) for _ in range(3))
+    ref = fpsa.FpsaPlan(grid, tile, win, H, d)(q, k, v, "lhd")
+    qh, kh, vh = (x.cpu().pin_memory() for x in (q, k, v))
+    oh = torch.empty((L, H, d), dtype=torch.bfloat16).pin_memory()
+    streamer = fpsa.HostStreamer(grid, tile, win, H, d, chunk_heads=3)
+    for _ in range(2):  # the second call reuses the staging buffers
+        oh.zero_()
+        streamer(qh, kh, vh, oh)
+        torch.cuda.current_stream().synchronize()
+        assert torch.equal(oh, ref.cpu())
+    with pytest.raises(ValueError):
+        streamer(q, k, v, oh)  # device tensors are rejected
