@@ -52,6 +52,8 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="budget of the cpu_baseline sample")
     ap.add_argument("--ulysses", action="store_true", help="sequence-sharded inputs + all-to-all (C3)")
+    ap.add_argument("--ulysses-chunk", type=int, default=1,
+                    help="heads per pipelined all-to-all chunk (0: one all-to-all per tensor, no overlap)")
     return ap.parse_args()
 
 
@@ -259,7 +261,8 @@ def main():
     v = torch.randn((Lr, Hr, d), generator=gen, device=dev).to(torch.bfloat16)
     out = torch.empty_like(q)
     if args.ulysses:
-        uly = UlyssesAttention(grid, tile, win, H, d, device=dev, tau=args.tau)
+        uly = UlyssesAttention(grid, tile, win, H, d, device=dev, tau=args.tau,
+                               chunk_heads=args.ulysses_chunk or None)
         plan = uly.plan
 
         def step(q_, k_, v_, out_):

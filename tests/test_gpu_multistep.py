@@ -69,6 +69,9 @@ def test_ulysses_single_rank_matches_plan(fpsa):
     out = uly(q, k, v)
     ref = fpsa.fps_attention(q, k, v, grid, tile, win, layout="lhd")
     assert torch.equal(out, ref)
+    # per-head-chunk pipeline: async NCCL all-to-alls around each chunk's kernels
+    uly3 = fpsa.UlyssesAttention(grid, tile, win, H, d, device="cuda", chunk_heads=3)
+    assert torch.equal(uly3(q, k, v), ref)
     dist.destroy_process_group()
 
 

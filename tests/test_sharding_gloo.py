@@ -16,7 +16,8 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2506_04648_b200.sharding import gather_heads, head_range, head_to_seq, seq_to_head, shard_heads
+from paper_2506_04648_b200.sharding import (gather_heads, head_range, head_to_seq, seq_to_head, shard_heads,
+                                            ulysses_pipeline)
 
 
 def _free_port() -> int:
@@ -50,6 +51,12 @@ def _worker(rank, world, port, L, H, d, out_dir):
         ref = _per_head_op(full, H)
         got = head_to_seq(_per_head_op_local(hs, rank, hp))
         assert torch.allclose(got, ref[rank * Ll:(rank + 1) * Ll], rtol=1e-6, atol=1e-5)
+        # per-head-chunk pipeline (async all-to-alls around each chunk's compute) == the unchunked path
+        for chunk in (1, 3, hp):
+            got_p = ulysses_pipeline(local, local * 2, local * 3,
+                                     lambda qc, kc, vc, c0, c1: _chunk_op(qc, kc, vc, rank * hp + c0), chunk)
+            full_op = _chunk_op(full, full * 2, full * 3, 0)
+            assert torch.allclose(got_p, full_op[rank * Ll:(rank + 1) * Ll], rtol=1e-6, atol=1e-5), chunk
         # head-parallel shard + gather (uneven head counts allowed)
         h0, h1 = head_range(rank, world, H + 1)
         full2 = torch.randn((L, H + 1, d), generator=torch.Generator().manual_seed(7))
@@ -59,6 +66,12 @@ def _worker(rank, world, port, L, H, d, out_dir):
         open(os.path.join(out_dir, f"ok{rank}"), "w").close()
     finally:
         dist.destroy_process_group()
+
+
+def _chunk_op(q, k, v, h_first):
+    """Per-head stand-in taking three inputs; the scale depends on the global head index."""
+    scale = torch.arange(h_first + 1, h_first + q.shape[1] + 1, dtype=q.dtype).view(1, -1, 1)
+    return torch.cumsum(q, dim=0) * scale + k.flip(0) - v * 0.5
 
 
 def _per_head_op_local(x, rank, hp):
