@@ -8,8 +8,8 @@
 // u is the concatenation of its admissible key tiles in ascending id order
 // (sparsity.py:63-67, the reference's reduction order), each key tile cut
 // into 128-key blocks; a tile's last block has n_tail = tv - 128 (nb - 1)
-// keys (rounded up to 16), so no padding key of a 240-token tile is
-// multiplied or exponentiated.  Per key block j:
+// valid keys (a multiple of 8); the P~ words of the zero padding keys past
+// them are zeroed, so they add nothing to O or to the row sum l.  Per key block j:
 //
 //   S(j)  = Q K_j^T                  tcgen05.mma kind::f8f6f4 M128 N128, A/B from
 //                                    smem, fp32 accumulator in TMEM buffer j % 2
@@ -88,8 +88,8 @@ struct AttnParams {
   int32_t* redo;         // [0]: count, [kRedoHeader..]: triples of items to recompute exactly
   int32_t exact;         // 1: this launch recomputes the redo list with the exact row max
   int32_t M, tv, pitch, nb;  // nb: 128-key blocks per tile
-  int32_t n_tail;     // S columns of the last key block of a tile (tv - 128 (nb-1), rounded up to 16)
-  int32_t tail_pad8;  // 1 if the last 8 of those columns are zero padding (tv % 16 == 8)
+  int32_t n_tail;     // valid keys of the last key block of a tile: tv - 128 (nb-1), a multiple of 8; the
+                      // QK MMA still runs N = 128 over zero K rows, whose S = 0 the softmax drops
   float softmax_log2;  // f32(softmax_scale * log2 e)
   float tau;
   void* out;
@@ -393,11 +393,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           const bool tail = b == p.nb - 1;
           const int ncol = (tail ? p.n_tail : kBlk) - kPartCols * part;
           const int ncol_h = min(max(ncol, 0), kPartCols);
-          const bool pad8 = tail && p.tail_pad8 && ncol > 0 && ncol <= kPartCols;
           const float c = factor_at(kt);
           mbar_wait(&bar_s_full[g & 1], (g >> 1) & 1);
           tc_fence_after();
-          m_acc = fmaxf(m_acc, block_max<kPartCols>(tm_s(g) + lane_off + part * kPartCols, ncol_h, pad8) * c);
+          m_acc = fmaxf(m_acc, block_max<kPartCols>(tm_s(g) + lane_off + part * kPartCols, ncol_h, false) * c);
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&bar_p_ready[g & 1]);  // S consumed
@@ -423,9 +422,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_after();
         if (!p.exact) {
           // reference max = row max of the first key block (a tail block only when nb == 1)
-          const int raw0 = (p.nb == 1 ? p.n_tail : kBlk) - kPartCols * part;
-          const bool pad8 = p.nb == 1 && p.tail_pad8 && raw0 > 0 && raw0 <= kPartCols;
-          m_ref = row_max(block_max<kPartCols>(tm_s(g) + lane_off + part * kPartCols, ncol_of(0), pad8)) * c;
+          m_ref = row_max(block_max<kPartCols>(tm_s(g) + lane_off + part * kPartCols, ncol_of(0), false)) * c;
         }
         load_s_all<kPartCols>(tm_s(g) + lane_off + part * kPartCols, sreg);
         tmem_wait_ld();
@@ -674,11 +671,7 @@ extern "C" int fpsa_attn_fwd(const uint8_t* q_codes, const uint8_t* k_codes, con
   p.tv = tv;
   p.pitch = tile_pitch;
   p.nb = (tv + kBlk - 1) / kBlk;
-  {
-    const int32_t tail = tv - kBlk * (p.nb - 1);  // valid keys of a tile's last 128-key block
-    p.n_tail = (tail + 15) / 16 * 16;
-    p.tail_pad8 = p.n_tail != tail;
-  }
+  p.n_tail = tv - kBlk * (p.nb - 1);  // valid keys of a tile's last 128-key block
   p.softmax_log2 = softmax_scale * 1.4426950408889634f;
   p.tau = tau_log2;
   p.out = out;
