@@ -76,6 +76,13 @@ constexpr float kLog2_448 = 8.807354922057604f;
 constexpr int kRedoHeader = 4;  // int32 words before the redo items in the workspace
 constexpr int kFacCap = 512;    // key-tile factors per item kept in shared memory (more: read from L2)
 constexpr int kHelperWarp = kSoftmaxWarps + 2;  // producer-warpgroup warp that prefetches item metadata
+// Ping-pong softmax: the warps w and w+4 of an SMSP (same TMEM lane quarter) take alternate key blocks,
+// each computing whole 128-key rows, instead of the two 64-column halves of every block.
+#ifndef FPSA_PINGPONG
+#define FPSA_PINGPONG 1
+#endif
+constexpr bool kPingPong = FPSA_PINGPONG != 0;
+static_assert(!kPingPong || kParts == 2, "ping-pong pairs the two warps of a TMEM lane quarter");
 
 struct AttnParams {
   const double* q_scales;
@@ -167,7 +174,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&bar_q[i], 1);
       mbar_init(&bar_qfree[i], 1);
       mbar_init(&bar_s_full[i], 1);
-      mbar_init(&bar_p_ready[i], kSoftmaxWarps);  // one arrival per softmax warp
+      mbar_init(&bar_p_ready[i], kPingPong ? kSoftmaxWarps / 2 : kSoftmaxWarps);  // one arrival per writing warp
     }
     mbar_init(&bar_o, 1);
     mbar_init(&bar_ofree, kSoftmaxWarps);
@@ -305,7 +312,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #ifndef FPSA_NO_MMA
 #pragma unroll
           for (int k = 0; k < kBlk / 32; ++k)
-            mma_f8_ts_w(tm_o, ts + kPartCols * (32 * k / kPartCols) + 8 * (k % (kPartCols / 32)),
+            mma_f8_ts_w(tm_o, kPingPong ? ts + 8 * k : ts + kPartCols * (32 * k / kPartCols) + 8 * (k % (kPartCols / 32)),
                         dv + (uint64_t)k * (32 * D / 16), idesc_pv,
                         (s > pv0 || k > 0) ? 1u : 0u);
 #endif
@@ -385,6 +392,95 @@ __global__ void __launch_bounds__(kThreads, 1)
 #ifdef FPSA_TRACE
       const long long tl0 = clock64();
 #endif
+      if constexpr (kPingPong) {
+        // ping-pong: this warp computes the whole 128-key rows of its lane quarter for the steps with
+        // g % 2 == part (S buffer g % 2 == part), the other warp of the SMSP the other steps, so one
+        // warp's TMEM load / store and hand-off latency overlaps the other's exp work
+        const uint32_t s_row = tm_s((uint32_t)part) + lane_off;
+        auto owned = [&](uint32_t gg) { return (int)(gg & 1u) == part; };
+        auto ncol_blk = [&](int32_t bb) { return bb == p.nb - 1 ? p.n_tail : kBlk; };
+        if (p.exact) {
+          // pass 0 (exact mode only): running max over this warp's key blocks, then over the pair
+          float m_acc = -INFINITY;
+          int32_t kt = 0, b = 0;
+          for (int32_t j = 0; j < n_kv; ++j, ++g) {
+            if (owned(g)) {
+              const float c = factor_at(kt);
+              mbar_wait(&bar_s_full[g & 1], (g >> 1) & 1);
+              tc_fence_after();
+              m_acc = fmaxf(m_acc, block_max<kBlk>(s_row, ncol_blk(b), false) * c);
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive(&bar_p_ready[g & 1]);  // S consumed
+            }
+            if (b == p.nb - 1) {
+              b = 0;
+              ++kt;
+            } else {
+              ++b;
+            }
+          }
+          m_ref = row_max(m_acc);
+        } else {
+          // reference max = row max of the item's first key block, taken by the warp that owns it
+          float m0 = -INFINITY;
+          if (owned(g)) {
+            mbar_wait(&bar_s_full[g & 1], (g >> 1) & 1);
+            tc_fence_after();
+            m0 = block_max<kBlk>(s_row, ncol_blk(0), false) * factor_at(0);
+          }
+          m_ref = row_max(m0);
+        }
+        int32_t kt = 0, b = 0;
+        float c = factor_at(0);
+        for (int32_t j = 0; j < n_kv; ++j, ++g) {
+          if (owned(g)) {
+#ifdef FPSA_TRACE
+            const long long ts0 = clock64();
+#endif
+            FPSA_TL(warp, 0, g);
+            mbar_wait(&bar_s_full[g & 1], (g >> 1) & 1);
+            FPSA_TL(warp, 1, g);
+#ifdef FPSA_TRACE
+            w_s += clock64() - ts0;
+            const long long tc0 = clock64();
+            ++n_steps;
+#endif
+            tc_fence_after();
+            const int n = ncol_blk(b);
+            const float bias = kLog2_448 - m_ref - tau;
+            uint32_t w[kBlk / 4];
+            {
+              uint32_t sreg[64];
+              load_s_all<64>(s_row, sreg);
+              tmem_wait_ld();
+              sat |= compute_p_regs<64>(sreg, min(n, 64), c, bias, w);
+            }
+            {
+              uint32_t sreg[64];
+              load_s_all<64>(s_row + 64, sreg);
+              tmem_wait_ld();
+              sat |= compute_p_regs<64>(sreg, max(n - 64, 0), c, bias, w + 16);
+            }
+#ifdef FPSA_TRACE
+            w_c += clock64() - tc0;
+#endif
+            FPSA_TL(warp, 2, g);
+            tmem_st32(s_row, w);  // P~ of the 128 keys over the first 32 columns of this S buffer
+            tmem_wait_st();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&bar_p_ready[g & 1]);
+            FPSA_TL(warp, 3, g);
+          }
+          if (b == p.nb - 1) {
+            b = 0;
+            if (++kt < n_kt) c = factor_at(kt);
+          } else {
+            ++b;
+          }
+        }
+      } else {
       if (p.exact) {
         // pass 0 (exact mode only): running max of x over all key blocks
         float m_acc = -INFINITY;
@@ -468,6 +564,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           FPSA_TL(warp, 3, g);
           if (more) tmem_wait_ld();
         }
+      }
       }
 #ifdef FPSA_TRACE
       t_loop += clock64() - tl0;

@@ -1,2 +1,6 @@
-timeout -s KILL 120 python tools/debug_pad8.py > gpurun_out/pad8b.txt 2>&1
-timeout -s KILL 400 python -m pytest tests/test_gpu_attention.py -q -s -p no:cacheprovider --timeout 100 -k "emulation or golden or redo or full_size" > gpurun_out/tests_attn_r2v.txt 2>&1; echo "EXIT $?" >> gpurun_out/tests_attn_r2v.txt
+timeout -s KILL 60 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_r2w.txt 2>&1; echo "EXIT $?" >> gpurun_out/smoke_r2w.txt
+if grep -q "smoke ok" gpurun_out/smoke_r2w.txt; then
+timeout -s KILL 400 python -m pytest tests/test_gpu_attention.py tests/test_gpu_multistep.py -x -q -p no:cacheprovider --timeout 60 > gpurun_out/tests_r2w.txt 2>&1; echo "EXIT $?" >> gpurun_out/tests_r2w.txt
+bash tools/ab.sh pp libfpsa_np.so libfpsa.so > gpurun_out/ab_pp.txt 2>&1
+timeout -s KILL 120 python tools/trace_attn.py c2 > gpurun_out/trace_r2w.txt 2>&1
+fi
