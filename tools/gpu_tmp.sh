@@ -1,6 +1,3 @@
-timeout -s KILL 60 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_r2w.txt 2>&1; echo "EXIT $?" >> gpurun_out/smoke_r2w.txt
-if grep -q "smoke ok" gpurun_out/smoke_r2w.txt; then
-timeout -s KILL 400 python -m pytest tests/test_gpu_attention.py tests/test_gpu_multistep.py -x -q -p no:cacheprovider --timeout 60 > gpurun_out/tests_r2w.txt 2>&1; echo "EXIT $?" >> gpurun_out/tests_r2w.txt
-bash tools/ab.sh pp libfpsa_np.so libfpsa.so > gpurun_out/ab_pp.txt 2>&1
-timeout -s KILL 120 python tools/trace_attn.py c2 > gpurun_out/trace_r2w.txt 2>&1
-fi
+for tool in memcheck racecheck synccheck; do
+  timeout -s KILL 600 compute-sanitizer --tool $tool python tools/sanitize_small.py > gpurun_out/sanitizer_${tool}_r2z.txt 2>&1; echo "EXIT $?" >> gpurun_out/sanitizer_${tool}_r2z.txt
+done

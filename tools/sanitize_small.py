@@ -1,0 +1,17 @@
+"""Small FP8 + passthrough runs for compute-sanitizer (memcheck / racecheck / synccheck)."""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+import paper_2506_04648_b200 as fpsa
+
+grid, tile, win, H, d = (6, 10, 32), (3, 5, 16), (3, 3, 3), 2, 128
+L = grid[0] * grid[1] * grid[2]
+g = torch.Generator(device="cuda").manual_seed(3)
+q, k, v = (torch.randn((L, H, d), generator=g, device="cuda").to(torch.bfloat16) for _ in range(3))
+out = fpsa.FpsaPlan(grid, tile, win, H, d)(q, k, v, "lhd")
+redo = fpsa.FpsaPlan(grid, tile, win, H, d, tau=0.0)  # forces the exact-mode launch
+redo(q, k, v, "lhd")
+pt = fpsa.PassthroughPlan(grid, tile, win, H, d)(q, k, v, "lhd", out_dtype=torch.float32)
+fid = fpsa.device_fidelity(pt, out.float(), "lhd")
+torch.cuda.synchronize()
+print("ok", redo.redo_count(), fid[0])
