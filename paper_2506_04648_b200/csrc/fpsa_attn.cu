@@ -33,11 +33,13 @@
 // double-buffered, QK(j+1) runs while the softmax works on S(j), and the MMA
 // issue order PV(j), QK(j+2) never makes the softmax wait on its own P.
 //
-// Warp roles (320 threads): warps w and w+4 (w < 4) own TMEM lane quarter w
-// (rows 32w..32w+31), warp w the S columns 0-63, warp w+4 the columns
-// 64-127; each writes the P~ of its 64 keys into the first 16 columns of its
-// own half, so the halves never wait for each other.  Warp 8 is the TMA
-// producer (and TMEM allocator), warp 9 the MMA issuer.
+// Warp roles (384 threads): warps w and w+4 (w < 4) share TMEM lane quarter w
+// (rows 32w..32w+31) and take alternate key blocks (ping-pong): warp w the
+// even steps, warp w+4 the odd ones, each computing whole 128-key rows and
+// writing their P~ over the first 32 columns of the step's S buffer, so one
+// warp's TMEM traffic and hand-off overlap the other's exp work.  Warp 8 is
+// the TMA producer (and TMEM allocator), warp 9 the MMA issuer, warp 10
+// prefetches per-item metadata, warp 11 is idle.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
