@@ -133,10 +133,10 @@ __device__ __forceinline__ void softmax_unit(const uint32_t* s, f2 cc, f2 bb, fl
 // All 32 columns of chunk C (P words w[8C..8C+7]), in groups of 4 keys:
 // columns 0 and 1 always on MUFU ex2 (one FFMA2 forms both arguments from an
 // adjacent register pair); columns 2 and 3 on the FMA-pipe polynomial in every
-// group (FPSA_POLY_PER8 == 4, the default), in every other group (2: columns
-// 6 and 7 of each 8), or never (0).  oracle.fpsa_oracle._poly_columns mirrors it.
+// group (FPSA_POLY_PER8 == 4, the default: measured best with the ping-pong
+// softmax), in every other group (2: columns 6 and 7 of each 8), or never (0).  oracle.fpsa_oracle._poly_columns mirrors it.
 #ifndef FPSA_POLY_PER8
-#define FPSA_POLY_PER8 2
+#define FPSA_POLY_PER8 4
 #endif
 template <int C>
 __device__ __forceinline__ void softmax_chunk32(const uint32_t* s, f2 cc, f2 bb, float cs, float bs, uint32_t* w) {
