@@ -338,8 +338,12 @@ POLY_PER8 = 4  # softmax.cuh FPSA_POLY_PER8
 def _poly_columns(block: int = 128, per8: int = POLY_PER8) -> np.ndarray:
     """Columns of a key block whose exp2 the GPU kernel evaluates with its polynomial
     (softmax.cuh softmax_chunk32): columns 2, 3, 6, 7 of every group of 8 (per8 = 4, the
-    build default), columns 6 and 7 (per8 = 2) or none (0); the rest use MUFU ex2."""
+    build default), columns 6 and 7 (per8 = 2), 2-7 (6), all (8) or none (0); the rest use MUFU ex2."""
     col = np.arange(block) % 8
+    if per8 == 8:
+        return np.ones(block, dtype=bool)
+    if per8 == 6:
+        return col >= 2
     if per8 == 4:
         return col % 4 >= 2
     if per8 == 2:

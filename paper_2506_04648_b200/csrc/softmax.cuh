@@ -143,10 +143,15 @@ __device__ __forceinline__ void softmax_chunk32(const uint32_t* s, f2 cc, f2 bb,
 #pragma unroll
   for (int q = 0; q < 8; ++q) {
     const float* v = reinterpret_cast<const float*>(s + 4 * q);
-    f2 m = fma2(f2{v[0], v[1]}, cc, bb);
-    m = f2{ex2(m.x), ex2(m.y)};
     constexpr int kPer8 = FPSA_POLY_PER8;
-    const bool poly = kPer8 == 4 || (kPer8 == 2 && (q & 1));
+    f2 m;
+    if (kPer8 == 8 || (kPer8 == 6 && (q & 1))) {  // columns 0 and 1 on the polynomial too
+      m = exp2_poly_sat(f2{fma_sat(v[0], cs, bs), fma_sat(v[1], cs, bs)});
+    } else {
+      m = fma2(f2{v[0], v[1]}, cc, bb);
+      m = f2{ex2(m.x), ex2(m.y)};
+    }
+    const bool poly = kPer8 >= 4 || (kPer8 == 2 && (q & 1));
     f2 pp;
     if (poly) {
       pp = exp2_poly_sat(f2{fma_sat(v[2], cs, bs), fma_sat(v[3], cs, bs)});

@@ -1,2 +1,1 @@
-timeout -s KILL 90 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_r3e.txt 2>&1; echo "EXIT $?" >> gpurun_out/smoke_r3e.txt
-timeout -s KILL 500 python -m pytest tests -x -q -m gpu -p no:cacheprovider --timeout 100 > gpurun_out/tests_r3e.txt 2>&1; echo "EXIT $?" >> gpurun_out/tests_r3e.txt
+REPS=3 STEPS=20 bash tools/ab.sh poly3 libfpsa.so libfpsa_p6.so libfpsa_p8.so > gpurun_out/ab_poly3_pp.txt 2>&1
