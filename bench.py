@@ -412,7 +412,7 @@ def main():
             "algorithmic": "sum_u |W(u)| * 4 tv^2 d per head (metrics.py:91-102), %d FLOP per launch" % flops,
         },
         "roofline_quantize": {
-            "bound": "hbm", "kernels": "chan_amax_kernel + quant_kernel (q,k,v fused)",
+            "bound": "hbm", "kernels": "chan_amax_kernel + quant_tma_kernel (q,k,v in one launch)",
             "achieved": qbytes / (ms_quant * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
             "frac": qbytes / (ms_quant * 1e-3) / 1e9 / hbm, "algorithmic_bytes": qbytes,
         },
