@@ -59,18 +59,15 @@ namespace {
 
 using namespace sm100;
 
-#ifndef FPSA_ROW_PARTS
-#define FPSA_ROW_PARTS 2
-#endif
-constexpr int kParts = FPSA_ROW_PARTS;          // softmax warps sharing one TMEM lane quarter (row)
-constexpr int kPartCols = 128 / kParts;         // S columns per softmax thread
+constexpr int kParts = 2;                       // softmax warps sharing one TMEM lane quarter (row)
+constexpr int kPartCols = 128 / kParts;         // S columns per softmax thread in the FPSA_PINGPONG=0 variant
 constexpr int kSoftmaxWarps = 4 * kParts;
 constexpr int kTmaWarp = kSoftmaxWarps;
 constexpr int kMmaWarp = kSoftmaxWarps + 1;
-constexpr int kThreads = (kSoftmaxWarps + 4) * 32;  // softmax warpgroups + 1 producer (TMA, MMA, 2 idle)
+constexpr int kThreads = (kSoftmaxWarps + 4) * 32;  // softmax warpgroups + 1 producer (TMA, MMA, helper, idle)
 // setmaxnreg split of the 64K-register file: per SMSP one warp of each warpgroup
-// (kParts 4 was measured slower on B200: 13.4 vs 12.8 ms at C2; 112/64 deadlocks in setmaxnreg.inc)
-constexpr uint32_t kRegsSoftmax = kParts == 2 ? 216 : 104, kRegsProducer = 64;
+// (4 warps per quarter at 104 registers was measured slower: 13.4 vs 12.8 ms at C2; 112/64 deadlocks)
+constexpr uint32_t kRegsSoftmax = 216, kRegsProducer = 64;
 
 constexpr int kStages = 4;     // K/V ring depth (128-key blocks)
 constexpr int kBlk = 128;      // rows per query block = keys per key block
@@ -79,7 +76,8 @@ constexpr int kRedoHeader = 4;  // int32 words before the redo items in the work
 constexpr int kFacCap = 512;    // key-tile factors per item kept in shared memory (more: read from L2)
 constexpr int kHelperWarp = kSoftmaxWarps + 2;  // producer-warpgroup warp that prefetches item metadata
 // Ping-pong softmax: the warps w and w+4 of an SMSP (same TMEM lane quarter) take alternate key blocks,
-// each computing whole 128-key rows, instead of the two 64-column halves of every block.
+// each computing whole 128-key rows.  FPSA_PINGPONG=0 builds the earlier variant in which the two warps
+// take the two 64-column halves of every block (slower: 12.65 vs 12.1 ms at C2).
 #ifndef FPSA_PINGPONG
 #define FPSA_PINGPONG 1
 #endif
