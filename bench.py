@@ -49,6 +49,8 @@ def parse():
     ap.add_argument("--config", default="wan14b_720p", choices=sorted(CONFIGS))
     ap.add_argument("--tau", type=float, default=8.0)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-chunk", type=int, default=0,
+                    help="heads per host-streaming chunk (0: 2, the measured best at C2: 44.8 ms vs 46.6 for 5)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="budget of the cpu_baseline sample")
     ap.add_argument("--ulysses", action="store_true", help="sequence-sharded inputs + all-to-all (C3)")
@@ -334,8 +336,8 @@ def main():
                 oh.copy_(out, non_blocking=True)
         else:
             # head chunks: the H2D of chunk c+1 and the D2H of chunk c-1 overlap chunk c's kernels
-            streamer = fpsa.HostStreamer(grid, tile, win, Hr, d, chunk_heads=max(1, Hr // 8), tau=args.tau,
-                                         device=dev)
+            streamer = fpsa.HostStreamer(grid, tile, win, Hr, d, chunk_heads=args.e2e_chunk or min(Hr, 2),
+                                         tau=args.tau, device=dev)
 
             def e2e_step():
                 streamer(qh, kh, vh, oh)

@@ -1,2 +1,4 @@
-timeout -s KILL 300 python -m pytest tests/test_gpu_quant.py -x -q -p no:cacheprovider --timeout 100 > gpurun_out/tests_q_r3i.txt 2>&1; echo "EXIT $?" >> gpurun_out/tests_q_r3i.txt
-REPS=3 bash tools/ab.sh q4 libfpsa_qold.so libfpsa.so > gpurun_out/ab_q4.txt 2>&1
+for c in 1 2 4; do
+timeout -s KILL 200 python bench.py --steps 5 --warmup 3 --no-cpu --e2e-chunk $c > gpurun_out/e2e_c$c.json 2>/dev/null
+python -c "import json,sys; d=json.load(open(sys.argv[1])); print(sys.argv[2], d['e2e']['ms_per_step'], d['ms_per_step'])" gpurun_out/e2e_c$c.json $c >> gpurun_out/e2e_chunks2.txt
+done
