@@ -232,7 +232,7 @@ class HostStreamer:
     stream makes ``out_host`` complete.
     """
 
-    def __init__(self, grid, tile, window, heads: int, d: int, fmt: Fp8Format = E4M3, *, chunk_heads: int = 5,
+    def __init__(self, grid, tile, window, heads: int, d: int, fmt: Fp8Format = E4M3, *, chunk_heads: int = 2,
                  device="cuda", tau: float = 8.0):
         torch = _torch()
         self.heads, self.d = int(heads), int(d)
