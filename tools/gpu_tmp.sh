@@ -1,4 +1,2 @@
-for c in 1 2 4; do
-timeout -s KILL 200 python bench.py --steps 5 --warmup 3 --no-cpu --e2e-chunk $c > gpurun_out/e2e_c$c.json 2>/dev/null
-python -c "import json,sys; d=json.load(open(sys.argv[1])); print(sys.argv[2], d['e2e']['ms_per_step'], d['ms_per_step'])" gpurun_out/e2e_c$c.json $c >> gpurun_out/e2e_chunks2.txt
-done
+FPSA_LIB=libfpsa_pp4.so timeout -s KILL 400 python -m pytest tests/test_gpu_attention.py -x -q -p no:cacheprovider --timeout 60 > gpurun_out/tests_pp4.txt 2>&1; echo "EXIT $?" >> gpurun_out/tests_pp4.txt
+REPS=3 STEPS=20 bash tools/ab.sh pp4 libfpsa.so libfpsa_pp4.so > gpurun_out/ab_pp4.txt 2>&1
