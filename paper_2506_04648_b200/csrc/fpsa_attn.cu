@@ -8,8 +8,9 @@
 // u is the concatenation of its admissible key tiles in ascending id order
 // (sparsity.py:63-67, the reference's reduction order), each key tile cut
 // into 128-key blocks; a tile's last block has n_tail = tv - 128 (nb - 1)
-// valid keys (a multiple of 8); the P~ words of the zero padding keys past
-// them are zeroed, so they add nothing to O or to the row sum l.  Per key block j:
+// valid keys.  The zero padding keys past them have zero V rows, and the PV of
+// a last block uses a "ones" atom whose rows past n_tail are zero, so their P~
+// codes add nothing to O or to the row sum l (no per-step masking).  Per key block j:
 //
 //   S(j)  = Q K_j^T                  tcgen05.mma kind::f8f6f4 M128 N128, A/B from
 //                                    smem, fp32 accumulator in TMEM buffer j % 2
@@ -95,7 +96,7 @@ struct AttnParams {
   int32_t* redo;         // [0]: count, [kRedoHeader..]: triples of items to recompute exactly
   int32_t exact;         // 1: this launch recomputes the redo list with the exact row max
   int32_t M, tv, pitch, nb;  // nb: 128-key blocks per tile
-  int32_t n_tail;     // valid keys of the last key block of a tile: tv - 128 (nb-1), a multiple of 8; the
+  int32_t n_tail;     // valid keys of the last key block of a tile: tv - 128 (nb-1); the
                       // QK MMA still runs N = 128 over zero K rows, whose S = 0 the softmax drops
   float softmax_log2;  // f32(softmax_scale * log2 e)
   float tau;
@@ -112,7 +113,8 @@ struct Smem {
   static constexpr int kK = 2 * kTile;
   static constexpr int kV = kK + kStages * kTile;
   static constexpr int kOnes = kV + kStages * kTile;  // 128 rows x D bytes of e4m3 1.0 (the "ones" MN atom)
-  static constexpr int kBytes = kOnes + kTile;
+  static constexpr int kOnesTail = kOnes + kTile;      // the same with rows >= n_tail (padding keys) zero
+  static constexpr int kBytes = kOnesTail + kTile;
   static constexpr uint32_t kSBO = 8 * D;  // 8 rows of D bytes
 };
 
@@ -193,8 +195,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     tmem_alloc(&s_tmem, 512);
     tmem_relinquish();
   }
-  for (int i = threadIdx.x; i < S::kTile / 4; i += kThreads)  // 1.0 in V's format
-    reinterpret_cast<uint32_t*>(smem + S::kOnes)[i] = FMT == FPSA_E4M3 ? 0x38383838u : 0x3C3C3C3Cu;
+  for (int i = threadIdx.x; i < S::kTile / 4; i += kThreads) {  // 1.0 in V's format; row = key of the block
+    const uint32_t one = FMT == FPSA_E4M3 ? 0x38383838u : 0x3C3C3C3Cu;
+    reinterpret_cast<uint32_t*>(smem + S::kOnes)[i] = one;
+    reinterpret_cast<uint32_t*>(smem + S::kOnesTail)[i] = (4 * i) / D < p.n_tail ? one : 0u;
+  }
   fence_proxy_async_smem();  // generic-proxy writes read by the tensor core
   tc_fence_before();
   __syncthreads();
@@ -251,6 +256,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint64_t dk0 = desc_kmajor<D>(smem_u32(smem + S::kK));
     // V stage st: start sv0 + st*tile, leading byte offset to the ones atom shrinks by the same amount
     const uint64_t dv0 = desc_mnmajor_ones<D>(sv0, smem_u32(smem + S::kOnes) - sv0);
+    // a tile's last block: padding keys (zero K and V rows) get zero rows in the ones atom, so their
+    // P~ codes, whatever they are, add nothing to the row sum either
+    const uint64_t dvt0 = desc_mnmajor_ones<D>(sv0, smem_u32(smem + S::kOnesTail) - sv0);
     constexpr uint64_t kVStageStep = kTileU - (kTileU << 16);
     uint32_t g = 0;
     int32_t iter = 0;
@@ -266,6 +274,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&bar_q[qbuf], (iter >> 1) & 1);
       tc_fence_after();
       int32_t b2 = 0;  // in-tile block of the next QK
+      int32_t bp = 0;  // in-tile block of the current step (both passes cycle through whole tiles)
       // S(step gg) = Q K^T into TMEM buffer gg % 2
       auto issue_qk = [&](uint32_t gg) {
         mbar_wait(&bar_kv_full[qk_st], qk_ph);
@@ -307,7 +316,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_wait(&bar_ofree, (iter - 1) & 1);  // the previous item's epilogue has read O
             tc_fence_after();
           }
-          const uint64_t dv = dv0 + pv_st * kVStageStep;
+          const uint64_t dv = (bp == p.nb - 1 ? dvt0 : dv0) + pv_st * kVStageStep;
           const uint32_t ts = tm_s(gs);
 #ifndef FPSA_NO_MMA
 #pragma unroll
@@ -319,6 +328,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         mma_commit_w(&bar_kv_empty[pv_st]);
         if (++pv_st == kStages) pv_st = 0;
+        if (++bp == p.nb) bp = 0;
         FPSA_TL(9, 2, gs);
         if (s + 2 < steps) {
           issue_qk(gs + 2);
@@ -739,7 +749,6 @@ extern "C" int fpsa_attn_fwd(const uint8_t* q_codes, const uint8_t* k_codes, con
   if (d != 64 && d != 128) return fail(FPSA_EUNSUPPORTED, "head dim must be 64 or 128, got " + std::to_string(d));
   const int32_t tv = tile.t * tile.h * tile.w;
   if (tile_pitch < tv || tile_pitch % kBlk) return fail(FPSA_EINVAL, "tile_pitch must be a multiple of 128 >= tile volume");
-  if (tv % 8) return fail(FPSA_EUNSUPPORTED, "tile volume must be a multiple of 8, got " + std::to_string(tv));
   if (!(softmax_scale > 0.0f)) return fail(FPSA_EINVAL, "softmax_scale must be > 0");
   if (fmt != FPSA_E4M3 && fmt != FPSA_E5M2) return fail(FPSA_EINVAL, "fmt must be e4m3 or e5m2");
   if (out_dtype != FPSA_F32 && out_dtype != FPSA_BF16) return fail(FPSA_EUNSUPPORTED, "out dtype must be f32 or bf16");

@@ -61,7 +61,7 @@ struct Params {
   int32_t n_items;
   int32_t* redo;
   int32_t exact;
-  int32_t M, tv, pitch, nb, n_tail;  // n_tail: valid keys of a tile's last block (multiple of 8)
+  int32_t M, tv, pitch, nb, n_tail;  // n_tail: valid keys of a tile's last block
   float softmax_log2;
   void* out;
   int64_t out_ts, out_hs;
@@ -118,16 +118,13 @@ __device__ __forceinline__ uint32_t bf16x2(float lo, float hi) {
 // kind::f16 instruction descriptor: bf16 A and B, f32 accumulate (same field layout as idesc_f8).
 __host__ __device__ constexpr uint32_t idesc_bf16(uint32_t M, uint32_t N, uint32_t b_mn_major) { return idesc_f8(M, N, 1, 1, b_mn_major); }
 
-// One 64-key row part: P = 2^(s c - m) for ncol valid columns (multiple of 8),
+// One 64-key row part: P = 2^(s c - m) for ncol valid columns,
 // packed bf16 pairs into w[32]; returns the f32 sum of the (unrounded) P.
 __device__ __forceinline__ float softmax_part_bf16(uint32_t* s, int ncol, float c, float neg_m, uint32_t* w) {
-  if (ncol < kPartCols) {
+  if (ncol < kPartCols) {  // tail block: columns >= ncol (any ncol) drop out of P and of the sum
 #pragma unroll
-    for (int i = 0; i < kPartCols; i += 8)
-      if (i >= ncol) {
-#pragma unroll
-        for (int k = i; k < i + 8; ++k) s[k] = kNegInf;
-      }
+    for (int k = 0; k < kPartCols; ++k)
+      if (k >= ncol) s[k] = kNegInf;
   }
   const f2 cc = bcast(c), bb = bcast(neg_m);
   f2 acc[4] = {bcast(0.0f), bcast(0.0f), bcast(0.0f), bcast(0.0f)};
@@ -583,7 +580,6 @@ extern "C" int fpsa_attn_bf16_fwd(const void* q_tiles, const void* k_tiles, cons
   if (d != 64 && d != 128) return fail(FPSA_EUNSUPPORTED, "head dim must be 64 or 128, got " + std::to_string(d));
   const int32_t tv = tile.t * tile.h * tile.w;
   if (tile_pitch < tv || tile_pitch % pt::kBlk) return fail(FPSA_EINVAL, "tile_pitch must be a multiple of 128 >= tile volume");
-  if (tv % 8) return fail(FPSA_EUNSUPPORTED, "tile volume must be a multiple of 8, got " + std::to_string(tv));
   if (!(softmax_scale > 0.0f)) return fail(FPSA_EINVAL, "softmax_scale must be > 0");
   if (out_dtype != FPSA_F32 && out_dtype != FPSA_BF16) return fail(FPSA_EUNSUPPORTED, "out dtype must be f32 or bf16");
   if (heads < 1 || n_items < 1) return fail(FPSA_EINVAL, "empty problem");

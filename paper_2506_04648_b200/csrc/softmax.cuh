@@ -276,11 +276,11 @@ __device__ __forceinline__ uint32_t compute_p_regs(const uint32_t* s, int ncol, 
   const float cs = c * (1.0f / 256.0f), bs = (boff + 126.0f) * (1.0f / 256.0f);
   softmax_chunk32<0>(s, cc, bb, cs, bs, w);
   if constexpr (NC == 64) softmax_chunk32<1>(s + 32, cc, bb, cs, bs, w);
-  if (ncol < NC) {
-#pragma unroll
-    for (int i = 0; i < NC / 4; ++i)
-      if (4 * i >= ncol) w[i] = 0u;
-  }
+  // Columns >= ncol (the zero padding keys of a tile's last block) are left as computed: their V rows
+  // and their rows of the kernel's tail "ones" atom are zero, so they add nothing to O or to l.  (A
+  // padding code can only look saturated when the reference max is below -tau, which just triggers a
+  // redundant exact-mode redo.)
+  (void)ncol;
   return saturated<NC>(w);
 }
 
@@ -295,12 +295,15 @@ __device__ __forceinline__ float block_max(uint32_t s_addr, int ncol, bool pad8)
       tmem_ld32(s_addr + base, s);
       tmem_wait_ld();
       if (pad8) mask_pad8(s, base, ncol);
+      if (base + 32 > ncol) {  // tail: drop the columns >= ncol (any ncol)
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          if (base + i >= ncol) s[i] = kNegInf;
+      }
 #pragma unroll
       for (int i = 0; i < 32; i += 4) {
-        if (base + i < ncol) {
-          m0 = max3(m0, __uint_as_float(s[i]), __uint_as_float(s[i + 1]));
-          m1 = max3(m1, __uint_as_float(s[i + 2]), __uint_as_float(s[i + 3]));
-        }
+        m0 = max3(m0, __uint_as_float(s[i]), __uint_as_float(s[i + 1]));
+        m1 = max3(m1, __uint_as_float(s[i + 2]), __uint_as_float(s[i + 3]));
       }
     }
   }
