@@ -1,3 +1,4 @@
-timeout -s KILL 90 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_r3q.txt 2>&1; echo "EXIT $?" >> gpurun_out/smoke_r3q.txt
-timeout -s KILL 500 python -m pytest tests/test_gpu_attention.py tests/test_gpu_multistep.py -x -q -p no:cacheprovider --timeout 100 > gpurun_out/tests_r3q.txt 2>&1; echo "EXIT $?" >> gpurun_out/tests_r3q.txt
-REPS=3 STEPS=20 bash tools/ab.sh half libfpsa_r3p.so libfpsa.so > gpurun_out/ab_half.txt 2>&1
+for i in 1 2 3 4 5; do
+timeout -s KILL 300 python bench.py --no-cpu > gpurun_out/rep_$i.json 2>/dev/null
+python -c "import json,sys; d=json.load(open(sys.argv[1])); print('run', sys.argv[2], 'step', round(d['ms_per_step'],3), 'attn', round(d['ms_attention'],3), 'quant', round(d['ms_quantize'],3), 'TF', round(d['value'],1), 'frac', round(d['roofline']['frac'],3), 'e2e_ms', round(d['e2e']['ms_per_step'],2), 'clk', d['clocks']['sm_mhz'], d['clocks']['reasons'])" gpurun_out/rep_$i.json $i >> gpurun_out/bench_repeats.txt
+done
