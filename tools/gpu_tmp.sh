@@ -1,1 +1,1 @@
-timeout -s KILL 60 tools/probes/mma2_rate > gpurun_out/mma2_rate.txt 2>&1; echo "EXIT $?" >> gpurun_out/mma2_rate.txt
+FPSA_TRACE_LIB=libfpsa_trace_pp4.so timeout -s KILL 120 python tools/trace_attn.py c2 > gpurun_out/trace_pp4.txt 2>&1
