@@ -191,3 +191,37 @@ def test_odd_tile_volumes(fpsa, grid, tile, win, d):
     pt = fpsa.fp8_sparse_forward(inputs, fpsa.ForwardConfig(window=fpsa.WindowSpec(*win), passthrough=True))
     f32 = O.sparse_forward_f32(q, k, v, tv, offs, ids)
     assert O.cosine(pt, f32) >= 0.9999
+
+
+def test_full_size_head_e5m2(fpsa):
+    """E5M2 Q/K/V (P stays E4M3, attention.py:208) at the C2 shape, window (3,3,3), against the oracle."""
+    grid, tile, win, d = (21, 45, 80), (3, 5, 16), (3, 3, 3), 128
+    L = grid[0] * grid[1] * grid[2]
+    tv = tile[0] * tile[1] * tile[2]
+    q, k, v = O.gen_inputs(4, 1, 0, L, d)
+    tmap = fpsa.build_tile_map(fpsa.GridShape(*grid, d), fpsa.TileScheme(*tile))
+    out = fpsa.fp8_sparse_forward(fpsa.AttentionInputs(q, k, v, tmap),
+                                  fpsa.ForwardConfig(window=fpsa.WindowSpec(*win), fmt=fpsa.E5M2))
+    offs, ids = O.window_lists(O.tile_grid_dims(grid, tile), win)
+    ref, _ = O.fp8_sparse_forward(q, k, v, tv, offs, ids, O.E5M2)
+    cos, mabs = O.cosine(out, ref), O.max_abs(out, ref)
+    print(f"e5m2 {grid}: cos={cos:.6f} max-abs={mabs:.3e}")
+    assert cos >= COS_REF
+    assert mabs <= 2e-2
+
+
+def test_full_size_head_passthrough(fpsa):
+    """Passthrough at the C2 shape, window (3,3,3): bf16 operands against the oracle's f32 sparse attention."""
+    grid, tile, win, d = (21, 45, 80), (3, 5, 16), (3, 3, 3), 128
+    L = grid[0] * grid[1] * grid[2]
+    tv = tile[0] * tile[1] * tile[2]
+    q, k, v = O.gen_inputs(5, 1, 0, L, d)
+    tmap = fpsa.build_tile_map(fpsa.GridShape(*grid, d), fpsa.TileScheme(*tile))
+    out = fpsa.fp8_sparse_forward(fpsa.AttentionInputs(q, k, v, tmap),
+                                  fpsa.ForwardConfig(window=fpsa.WindowSpec(*win), passthrough=True))
+    offs, ids = O.window_lists(O.tile_grid_dims(grid, tile), win)
+    ref = O.sparse_forward_f32(q, k, v, tv, offs, ids)
+    cos, mabs = O.cosine(out, ref), O.max_abs(out, ref)
+    print(f"passthrough {grid}: cos={cos:.7f} max-abs={mabs:.3e}")
+    assert cos >= 0.9999
+    assert mabs <= 1e-2 * float(np.abs(ref).max())
