@@ -47,6 +47,7 @@
 #include <cudaTypedefs.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstdint>
 #include <mutex>
 
@@ -734,6 +735,16 @@ int launch(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, 
 
 using namespace fpsa;
 
+#ifdef FPSA_ATTN2
+extern "C" int fpsa_attn2_fwd(const uint8_t* q_codes, const uint8_t* k_codes, const uint8_t* v_codes,
+                              const double* q_scales, const double* k_scales, const double* v_scales, int32_t heads,
+                              fpsa_dims3 grid, fpsa_dims3 tile, int32_t d, int32_t tile_pitch, const int32_t* offs,
+                              const int32_t* ids, const int32_t* items, int32_t n_items, float softmax_scale,
+                              int fmt, float tau_log2, void* out, int out_dtype, int64_t out_token_stride,
+                              int64_t out_head_stride, int out_order, void* workspace, int64_t workspace_bytes,
+                              void* stream);
+#endif
+
 extern "C" int fpsa_attn_fwd(const uint8_t* q_codes, const uint8_t* k_codes, const uint8_t* v_codes,
                              const double* q_scales, const double* k_scales, const double* v_scales, int32_t heads,
                              fpsa_dims3 grid, fpsa_dims3 tile, int32_t d, int32_t tile_pitch, const int32_t* offs,
@@ -758,6 +769,12 @@ extern "C" int fpsa_attn_fwd(const uint8_t* q_codes, const uint8_t* k_codes, con
   fpsa_attn_workspace_bytes(n_items, &need);
   if (!workspace || workspace_bytes < need)
     return fail(FPSA_ECAPACITY, "attention workspace must hold " + std::to_string(need) + " bytes");
+#ifdef FPSA_ATTN2
+  if (d == 128 && tv > kBlk && getenv("FPSA_ATTN_1CTA") == nullptr)
+    return fpsa_attn2_fwd(q_codes, k_codes, v_codes, q_scales, k_scales, v_scales, heads, grid, tile, d, tile_pitch,
+                          offs, ids, items, n_items, softmax_scale, fmt, tau_log2, out, out_dtype, out_token_stride,
+                          out_head_stride, out_order, workspace, workspace_bytes, stream);
+#endif
   const int32_t M = td.t * td.h * td.w;
   const int64_t rows = (int64_t)heads * M * tile_pitch;
   CUtensorMap tq, tk, tvm;

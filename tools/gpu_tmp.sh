@@ -1,1 +1,1 @@
-timeout -s KILL 400 python -m pytest tests/test_gpu_attention.py -q -s -p no:cacheprovider --timeout 200 -k "full_size" > gpurun_out/tests_full_r3s.txt 2>&1; echo "EXIT $?" >> gpurun_out/tests_full_r3s.txt
+REPS=1 STEPS=10 bash tools/ab.sh a2x libfpsa_a2.so libfpsa_a2n.so > gpurun_out/ab_a2x.txt 2>&1
