@@ -42,6 +42,17 @@ namespace {
 using namespace sm100;
 
 namespace a2 {
+#ifdef A2_TRACE
+__device__ long long g_a2[3][128][4];  // [leader MMA, leader softmax warp 0, peer softmax warp 0][step][event]
+#define A2_TL(who, step, ev)                                                            \
+  do {                                                                                  \
+    if ((blockIdx.x >> 1) == 0 && (threadIdx.x & 31) == 0 && (step) < 128) g_a2[who][step][ev] = clock64(); \
+  } while (0)
+#else
+#define A2_TL(who, step, ev) \
+  do {                       \
+  } while (0)
+#endif
 constexpr int D = 128;
 constexpr int kSoftmaxWarps = 8;
 constexpr int kTmaWarp = 8, kMmaWarp = 9, kHelperWarp = 10, kRelayWarp = 11;
@@ -94,7 +105,7 @@ __device__ __forceinline__ void cluster_sync_all() {
 __device__ __forceinline__ void mbar_arrive_remote(uint64_t* bar, uint32_t rank) {
   asm volatile(
       "{\n\t.reg .b32 ra;\n\tmapa.shared::cluster.u32 ra, %0, %1;\n\t"
-      "mbarrier.arrive.release.cluster.shared::cluster.b64 _, [ra];\n\t}" ::"r"(smem_u32(bar)),
+      "mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [ra];\n\t}" ::"r"(smem_u32(bar)),
       "r"(rank)
       : "memory");
 }
@@ -167,8 +178,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const int32_t cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
   const int32_t* items = p.exact ? p.redo + kRedoHeader : p.items;
   const int32_t count = p.exact ? *reinterpret_cast<volatile int32_t*>(p.redo) : p.n_items;
-  if (cid >= count) return;  // both CTAs of the pair leave together
+  if ((p.exact ? cid : 2 * cid) >= count) return;  // both CTAs of the pair leave together
   auto skip = [&](int32_t it) { return !p.exact && (items[3 * it + 2] & 1); };  // odd blocks ride with the pair
+  // The main list holds (tile, query block) items with the blocks of a tile adjacent; clusters walk it two
+  // items at a time so that every cluster meets the even blocks (TODO: a compacted pair list for tiles with
+  // an odd number of query blocks, which shift the parity).
+  const int32_t stride = p.exact ? ncl : 2 * ncl;
+  auto first_item = [&](int32_t c) { return p.exact ? c : 2 * c; };
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < 2; ++i) {
@@ -217,7 +233,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     __syncwarp();
     uint32_t g = 0;
     int32_t iter = 0;
-    for (int32_t it = cid; it < count; it += ncl) {
+    for (int32_t it = first_item(cid); it < count; it += stride) {
       if (skip(it)) continue;
       const int32_t h = items[3 * it], u = items[3 * it + 1], qb = items[3 * it + 2] + (int32_t)rank;
       const int32_t kt0 = __ldg(p.offs + u), n_kt = __ldg(p.offs + u + 1) - kt0;
@@ -254,7 +270,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       uint32_t g = 0;
       int32_t iter = 0;
       uint32_t qk_st = 0, qk_ph = 0, pv_st = 0;
-      for (int32_t it = cid; it < count; it += ncl) {
+      for (int32_t it = first_item(cid); it < count; it += stride) {
         if (skip(it)) continue;
         const int32_t u = items[3 * it + 1];
         const int32_t n_kt = __ldg(p.offs + u + 1) - __ldg(p.offs + u);
@@ -282,7 +298,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         if (steps <= 2) commit2_w(&bar_qfree[qbuf]);
         for (int32_t s = 0; s < steps; ++s) {
           const uint32_t gs = g + s;
+          A2_TL(0, gs, 0);
           mbar_wait(&bar_p_ready[gs & 1], (gs >> 1) & 1);
+          A2_TL(0, gs, 1);
           tc_fence_after();
           if (s >= pv0) {
             if (s == pv0 && iter > 0) {
@@ -297,10 +315,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           }
           commit2_w(&bar_kv_empty[pv_st]);
           if (++pv_st == kStages) pv_st = 0;
+          A2_TL(0, gs, 2);
           if (s + 2 < steps) {
             issue_qk(gs + 2);
             if (s + 3 == steps) commit2_w(&bar_qfree[qbuf]);
           }
+          A2_TL(0, gs, 3);
         }
         commit2_w(&bar_o);
         g += steps;
@@ -313,7 +333,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       // of this CTA's Q and K/V loads to the leader, whose MMAs read both CTAs' shared memory
       uint32_t g = 0;
       int32_t iter = 0;
-      for (int32_t it = cid; it < count; it += ncl) {
+      for (int32_t it = first_item(cid); it < count; it += stride) {
         if (skip(it)) continue;
         const int32_t u = items[3 * it + 1];
         const int32_t n_kt = __ldg(p.offs + u + 1) - __ldg(p.offs + u);
@@ -332,7 +352,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   } else if (warp == kHelperWarp) {
     const float sl = p.softmax_log2;
     int32_t iter = 0;
-    for (int32_t it = cid; it < count; it += ncl) {
+    for (int32_t it = first_item(cid); it < count; it += stride) {
       if (skip(it)) continue;
       const int slot = iter & 1;
       if (iter >= 2) mbar_wait(&bar_meta_empty[slot], ((iter >> 1) - 1) & 1);
@@ -376,7 +396,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     auto ncol_blk = [&](int32_t bb) { return bb == p.nb - 1 ? p.n_tail : kBlk; };
     uint32_t g = 0;
     int32_t iter = 0;
-    for (int32_t it = cid; it < count; it += ncl) {
+    for (int32_t it = first_item(cid); it < count; it += stride) {
       if (skip(it)) continue;
       const int32_t h = items[3 * it], u = items[3 * it + 1], qb = items[3 * it + 2] + (int32_t)rank;
       const bool live = qb * kBlk < p.tv;  // a tile with an odd number of blocks pairs its last with nothing
@@ -427,7 +447,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const float bias = kLog2_448 - m_ref - tau;
         for (int32_t j = 0; j < n_kv; ++j, ++g) {
           if (owned(g)) {
+            if (warp == 0 || warp == 4) A2_TL(1 + rank, g, 0);
             mbar_wait(&bar_s_full[g & 1], (g >> 1) & 1);
+            if (warp == 0 || warp == 4) A2_TL(1 + rank, g, 1);
             tc_fence_after();
             const uint32_t s_row = tm_s(g) + lane_off;
             const int n = ncol_blk(b);
@@ -444,9 +466,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               tmem_wait_ld();
               sat |= p_regs_sum<64>(sreg, max(n - 64, 0), c, bias, w + 16, lsum);
             }
+            if (warp == 0 || warp == 4) A2_TL(1 + rank, g, 2);
             tmem_st32(s_row, w);
             tmem_wait_st();
             signal(&bar_p_ready[g & 1]);
+            if (warp == 0 || warp == 4) A2_TL(1 + rank, g, 3);
           }
           if (b == p.nb - 1) {
             b = 0;
@@ -665,3 +689,10 @@ extern "C" int fpsa_attn2_fwd(const uint8_t* q_codes, const uint8_t* k_codes, co
   if (out_dtype == FPSA_F32) return a2::launch<FPSA_E5M2, FPSA_F32>(tq, tk, tvm, p, st);
   return a2::launch<FPSA_E5M2, FPSA_BF16>(tq, tk, tvm, p, st);
 }
+
+#ifdef A2_TRACE
+extern "C" int fpsa_a2_trace(long long* out) {
+  cudaMemcpyFromSymbol(out, fpsa::a2::g_a2, sizeof(fpsa::a2::g_a2));
+  return 0;
+}
+#endif

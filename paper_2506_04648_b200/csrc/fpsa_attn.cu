@@ -62,7 +62,7 @@ namespace {
 using namespace sm100;
 
 constexpr int kParts = 2;                       // softmax warps sharing one TMEM lane quarter (row)
-constexpr int kPartCols = 128 / kParts;         // S columns per softmax thread in the FPSA_PINGPONG=0 variant
+[[maybe_unused]] constexpr int kPartCols = 128 / kParts;  // S columns per softmax thread in the FPSA_PINGPONG=0 variant
 constexpr int kSoftmaxWarps = 4 * kParts;
 constexpr int kTmaWarp = kSoftmaxWarps;
 constexpr int kMmaWarp = kSoftmaxWarps + 1;
@@ -286,8 +286,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t idq = idesc_qk;
         const uint32_t ts = tm_s(gg);
 #ifndef FPSA_NO_MMA
+        if constexpr (D == 128) {  // one elect for the four K32 MMAs (shorter issue path)
+          mma_f8_ss_x4_w(ts, dq, dq + 2, dq + 4, dq + 6, dk, dk + 2, dk + 4, dk + 6, idq, 0u);
+        } else {
 #pragma unroll
-        for (int k = 0; k < D / 32; ++k) mma_f8_ss_w(ts, dq + 2 * k, dk + 2 * k, idq, k > 0 ? 1u : 0u);
+          for (int k = 0; k < D / 32; ++k) mma_f8_ss_w(ts, dq + 2 * k, dk + 2 * k, idq, k > 0 ? 1u : 0u);
+        }
 #endif
         mma_commit_w(&bar_s_full[gg & 1]);
         if (++b2 == p.nb) b2 = 0;
@@ -320,11 +324,17 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint64_t dv = (bp == p.nb - 1 ? dvt0 : dv0) + pv_st * kVStageStep;
           const uint32_t ts = tm_s(gs);
 #ifndef FPSA_NO_MMA
+          if constexpr (kPingPong) {  // one elect for the four K32 MMAs (shorter issue path)
+            constexpr uint64_t kVk = 32 * D / 16;
+            mma_f8_ts_x4_w(tm_o, ts, ts + 8, ts + 16, ts + 24, dv, dv + kVk, dv + 2 * kVk, dv + 3 * kVk, idesc_pv,
+                           s > pv0 ? 1u : 0u);
+          } else {
 #pragma unroll
-          for (int k = 0; k < kBlk / 32; ++k)
-            mma_f8_ts_w(tm_o, kPingPong ? ts + 8 * k : ts + kPartCols * (32 * k / kPartCols) + 8 * (k % (kPartCols / 32)),
-                        dv + (uint64_t)k * (32 * D / 16), idesc_pv,
-                        (s > pv0 || k > 0) ? 1u : 0u);
+            for (int k = 0; k < kBlk / 32; ++k)
+              mma_f8_ts_w(tm_o, kPingPong ? ts + 8 * k : ts + kPartCols * (32 * k / kPartCols) + 8 * (k % (kPartCols / 32)),
+                          dv + (uint64_t)k * (32 * D / 16), idesc_pv,
+                          (s > pv0 || k > 0) ? 1u : 0u);
+          }
 #endif
         }
         mma_commit_w(&bar_kv_empty[pv_st]);

@@ -1,1 +1,2 @@
-REPS=1 STEPS=10 bash tools/ab.sh a2x libfpsa_a2.so libfpsa_a2n.so > gpurun_out/ab_a2x.txt 2>&1
+timeout -s KILL 90 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_r3t.txt 2>&1; echo "EXIT $?" >> gpurun_out/smoke_r3t.txt
+timeout -s KILL 600 python -m pytest tests -x -q -m gpu -p no:cacheprovider --timeout 200 > gpurun_out/tests_r3t.txt 2>&1; echo "EXIT $?" >> gpurun_out/tests_r3t.txt
