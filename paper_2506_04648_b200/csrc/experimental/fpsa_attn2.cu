@@ -11,10 +11,16 @@
 // completions, its softmax warps arrive remotely on the leader's p_ready /
 // ofree barriers; commits multicast to both CTAs.
 //
-// Status (round 1): correct on the tv = 240 golden cases, but 29.7 ms at C2
-// against 12.0 ms for the single-CTA kernel with the GPU mostly idle (clocks
-// unthrottled), i.e. latency-bound on the cross-CTA signalling: to be
-// instrumented next.  Build and A/B:
+// Status (round 1): correct on the tv = 240 golden cases; 14.2 ms at C2 against
+// 11.8 ms for the single-CTA kernel.  Measured on the way (tools/trace_a2.py with
+// -DA2_TRACE): remote arrives with .release.cluster cost ~1300 clk (now
+// .relaxed: ~170); a cluster stride over the item list must keep the query-block
+// parity (odd-cid clusters otherwise got only odd blocks, 29.7 ms); what is left
+// is the softmax: the CUDA-core row sum and the per-column tail masking make the
+// exp work ~1700 clk per owned block against ~1100 in the single-CTA kernel (which
+// sums through the ones atom and drops padding keys through a zero-row atom).
+// Next: the N = 160 split of [V | ones], or the row sum with the
+// padding keys' known contribution subtracted instead of masked.  Build and A/B:
 //   cd paper_2506_04648_b200 && nvcc -shared -Xcompiler -fPIC -std=c++17 -O3 -lineinfo \
 //     -gencode arch=compute_100a,code=sm_100a -DFPSA_ATTN2 csrc/fpsa_attn.cu csrc/experimental/fpsa_attn2.cu \
 //     csrc/fpsa_attn_bf16.cu csrc/fpsa_quant.cu csrc/fpsa_metrics.cu csrc/fpsa_io.cu csrc/fpsa_host.cpp \
