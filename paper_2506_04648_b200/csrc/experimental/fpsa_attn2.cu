@@ -5,22 +5,30 @@
 // probe tools/probes/mma2_rate.cu measures at the full per-SM tensor rate.
 // Per key block j, in each CTA of the pair (rows = its query block):
 //   S(j)  = Q K_j^T     M256 N128, K half (64 keys) in each CTA's smem
-//   P~    = e4m3(448 2^-tau 2^(x - m)),  l += sum of the unrounded weights (CUDA cores)
-//   O    += P~ V_j      M256 N128, A = P~ from each CTA's TMEM, V half (64 channels) per CTA
-// The leader CTA issues all MMAs; the peer's relay warp forwards its TMA
-// completions, its softmax warps arrive remotely on the leader's p_ready /
-// ofree barriers; commits multicast to both CTAs.
+//   P~    = e4m3(448 2^-tau 2^(x - m))
+//   [O|l] += P~ [V_j|1] M256 N160, A = P~ from each CTA's TMEM; each CTA's B half is [64 V channels | 16
+//                       ones] (SWIZZLE_64B MN-major, the ones tile reached through the descriptor's LBO as in
+//                       the single-CTA kernel, a zero-row tail variant for a tile's last block), so O columns
+//                       0-63 / 80-143 hold the channels and 64-79 / 144-159 the row sum of the rounded P~
+// The leader CTA issues all MMAs; the peer's relay warp forwards its TMA completions, its softmax warps
+// arrive remotely on the leader's p_ready / ofree barriers; commits multicast to both CTAs.
+// -DA2_PBUF: P~ in its own TMEM columns (160..223) and an s_free barrier, so QK(j+2) is issued as soon as
+// the owners hold S(j) in registers instead of after PV(j).
 //
-// Status (round 1): correct on the tv = 240 golden cases; 14.2 ms at C2 against
-// 11.8 ms for the single-CTA kernel.  Measured on the way (tools/trace_a2.py with
-// -DA2_TRACE): remote arrives with .release.cluster cost ~1300 clk (now
-// .relaxed: ~170); a cluster stride over the item list must keep the query-block
-// parity (odd-cid clusters otherwise got only odd blocks, 29.7 ms); what is left
-// is the softmax: the CUDA-core row sum and the per-column tail masking make the
-// exp work ~1700 clk per owned block against ~1100 in the single-CTA kernel (which
-// sums through the ones atom and drops padding keys through a zero-row atom).
-// Next: the N = 160 split of [V | ones], or the row sum with the
-// padding keys' known contribution subtracted instead of masked.  Build and A/B:
+// Status (round 1): passes tests/test_gpu_attention.py (28 cases incl. E5M2, odd tile volumes, exact
+// mode). C2 attention, same box, interleaved (profiles/r01_ab_a2_r3x.txt): single-CTA 11.7 ms, this
+// kernel 12.4-12.6 ms (14.2 before the ones split), -DA2_PBUF 12.8 ms.
+// What the measurements say (profiles/r01_probe_mma2_rate.txt, r01_trace_a2_n160.txt, r01_trace_a2_pbuf.txt):
+// the pair's QK + PV step takes 576 clk back to back and 974 clk issue-to-completion in isolation, and
+// neither concurrent tcgen05.ld traffic nor FMA/MUFU-saturated warps on the same SM change that by more
+// than 5 %; in the kernel one MMA-warp iteration takes ~1450 clk, ~650 of them between p_ready and the last
+// PV issue. ncu's source counters for the single-CTA kernel show the same: the MMA warp is resident the
+// whole time, ~20 % waiting for p_ready and ~80 % executing its ~180-instruction step (descriptor
+// arithmetic, R2UR moves, elect / divergence checks, barrier address math) at a few cycles per dependent
+// instruction ('wait' and 'long_sb' stalls, 'not_selected' against the softmax warps). Halving the MMA
+// work per SM therefore does not shorten the step; the issue path does. Tried without gain: in-asm
+// descriptor steps (ptxas adds SELs), issuing from one lane (ptxas wraps each MMA in an elect loop), more
+// producer registers (same SASS).  Build and A/B:
 //   cd paper_2506_04648_b200 && nvcc -shared -Xcompiler -fPIC -std=c++17 -O3 -lineinfo \
 //     -gencode arch=compute_100a,code=sm_100a -DFPSA_ATTN2 csrc/fpsa_attn.cu csrc/experimental/fpsa_attn2.cu \
 //     csrc/fpsa_attn_bf16.cu csrc/fpsa_quant.cu csrc/fpsa_metrics.cu csrc/fpsa_io.cu csrc/fpsa_host.cpp \
@@ -96,7 +104,9 @@ struct Smem {
   static constexpr int kQ = 0;
   static constexpr int kK = 2 * kQTile;
   static constexpr int kV = kK + kStages * kKHalf;
-  static constexpr int kBytes = kV + kStages * kVHalf;
+  static constexpr int kOnes = kV + kStages * kVHalf;  // 128 keys x 64 B of e4m3 1.0: the ones MN atom
+  static constexpr int kOnesTail = kOnes + kVHalf;      // the same with rows >= n_tail (padding keys) zero
+  static constexpr int kBytes = kOnesTail + kVHalf;
 };
 
 __device__ __forceinline__ uint32_t cta_rank() {
@@ -115,18 +125,30 @@ __device__ __forceinline__ void mbar_arrive_remote(uint64_t* bar, uint32_t rank)
       "r"(rank)
       : "memory");
 }
-__device__ __forceinline__ void mma2_ss_w(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+// four MMAs of one step under one elect; `acc` predicates only the first; the descriptors advance by
+// ak / bk (16-byte units) per K32 step
+__device__ __forceinline__ void mma2_ss_x4_w(uint32_t d, uint64_t a, uint64_t ak, uint64_t b, uint64_t bk,
+                                             uint32_t idesc, uint32_t acc) {
   asm volatile(
-      "{\n\t.reg .pred p, e;\n\tsetp.ne.b32 p, %4, 0;\n\telect.sync _|e, 0xffffffff;\n\t"
-      "@e tcgen05.mma.cta_group::2.kind::f8f6f4 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
-      "l"(a), "l"(b), "r"(idesc), "r"(acc)
+      "{\n\t.reg .pred p, t, e;\n\tsetp.ne.b32 p, %4, 0;\n\tsetp.eq.u32 t, 0, 0;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f8f6f4 [%0], %1, %2, %3, p;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f8f6f4 [%0], %5, %6, %3, t;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f8f6f4 [%0], %7, %8, %3, t;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f8f6f4 [%0], %9, %10, %3, t;\n\t}" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc), "l"(a + ak), "l"(b + bk), "l"(a + 2 * ak), "l"(b + 2 * bk),
+      "l"(a + 3 * ak), "l"(b + 3 * bk)
       : "memory");
 }
-__device__ __forceinline__ void mma2_ts_w(uint32_t d, uint32_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+__device__ __forceinline__ void mma2_ts_x4_w(uint32_t d, uint32_t a, uint64_t b, uint64_t bk, uint32_t idesc,
+                                             uint32_t acc) {
   asm volatile(
-      "{\n\t.reg .pred p, e;\n\tsetp.ne.b32 p, %4, 0;\n\telect.sync _|e, 0xffffffff;\n\t"
-      "@e tcgen05.mma.cta_group::2.kind::f8f6f4 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
-      "r"(a), "l"(b), "r"(idesc), "r"(acc)
+      "{\n\t.reg .pred p, t, e;\n\tsetp.ne.b32 p, %4, 0;\n\tsetp.eq.u32 t, 0, 0;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f8f6f4 [%0], [%1], %2, %3, p;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f8f6f4 [%0], [%5], %6, %3, t;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f8f6f4 [%0], [%7], %8, %3, t;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f8f6f4 [%0], [%9], %10, %3, t;\n\t}" ::"r"(d),
+      "r"(a), "l"(b), "r"(idesc), "r"(acc), "r"(a + 8), "l"(b + bk), "r"(a + 16), "l"(b + 2 * bk), "r"(a + 24),
+      "l"(b + 3 * bk)
       : "memory");
 }
 __device__ __forceinline__ void commit2_w(uint64_t* bar) {  // arrives on `bar` in both CTAs of the pair
@@ -136,28 +158,6 @@ __device__ __forceinline__ void commit2_w(uint64_t* bar) {  // arrives on `bar` 
           smem_u32(bar)),
       "h"((uint16_t)3)
       : "memory");
-}
-
-// As compute_p_regs, with the row sum of the unrounded weights; columns >= ncol set to -inf first.
-template <int NC>
-__device__ __forceinline__ uint32_t p_regs_sum(uint32_t* s, int ncol, float c, float boff, uint32_t* w, f2& sum) {
-  if (ncol < NC) {
-#pragma unroll
-    for (int k = 0; k < NC; ++k)
-      if (k >= ncol) s[k] = kNegInf;
-  }
-  const f2 cc = bcast(c), bb = bcast(boff);
-  const float cs = c * (1.0f / 256.0f), bs = (boff + 126.0f) * (1.0f / 256.0f);
-#pragma unroll
-  for (int q = 0; q < NC / 4; ++q) {
-    const float* v = reinterpret_cast<const float*>(s + 4 * q);
-    f2 m = fma2(f2{v[0], v[1]}, cc, bb);
-    m = f2{ex2(m.x), ex2(m.y)};
-    const f2 pp = exp2_poly_sat(f2{fma_sat(v[2], cs, bs), fma_sat(v[3], cs, bs)});
-    sum = add2(sum, add2(m, pp));
-    w[q] = e4m3x4(m, pp);
-  }
-  return saturated<NC>(w);
 }
 
 template <int FMT, int OUT>
@@ -171,6 +171,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   __shared__ uint64_t bar_o, bar_ofree;
   __shared__ uint64_t bar_kv_full[kStages], bar_kv_peer[kStages], bar_kv_empty[kStages];
   __shared__ uint64_t bar_s_full[2], bar_p_ready[2];
+#ifdef A2_PBUF
+  __shared__ uint64_t bar_s_free[2], bar_p_free[2];
+#endif
   __shared__ uint32_t s_tmem;
   __shared__ float s_xchg[2][kBlk];
   __shared__ float s_fac[2][kFacCap];
@@ -199,6 +202,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       mbar_init(&bar_qfree[i], 1);
       mbar_init(&bar_s_full[i], 1);
       mbar_init(&bar_p_ready[i], 8);  // the step owner's 4 warps in each CTA (leader only)
+#ifdef A2_PBUF
+      mbar_init(&bar_s_free[i], 8);  // S(j) is in the owners' registers (leader only)
+      mbar_init(&bar_p_free[i], 1);  // PV(j) has read P~(j) (multicast commit)
+#endif
     }
     mbar_init(&bar_o, 1);
     mbar_init(&bar_ofree, 2 * kSoftmaxWarps);  // leader only: both CTAs' softmax warps
@@ -214,6 +221,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     s_ovf[0] = s_ovf[1] = 0;
     fence_barrier_init();
   }
+  {
+    const uint32_t one = FMT == FPSA_E4M3 ? 0x38383838u : 0x3C3C3C3Cu;  // 1.0 in V's format
+    for (int i = threadIdx.x; i < S::kVHalf / 4; i += kThreads) {
+      reinterpret_cast<uint32_t*>(smem + S::kOnes)[i] = one;
+      reinterpret_cast<uint32_t*>(smem + S::kOnesTail)[i] = (4 * i) / 64 < p.n_tail ? one : 0u;
+    }
+    fence_proxy_async_smem();  // generic-proxy writes read by the tensor core
+  }
   if (warp == kTmaWarp) {
     asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&s_tmem)),
                  "r"(512u)
@@ -224,8 +239,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   cluster_sync_all();  // barriers of both CTAs initialised before any remote arrive or multicast commit
   tc_fence_after();
   const uint32_t tmem = s_tmem;
-  const uint32_t tm_o = tmem;  // O: columns 0..127
+  const uint32_t tm_o = tmem;  // O: columns 0..159 (channels 0-63, row sum, channels 64-127, row sum)
   auto tm_s = [tmem](uint32_t g) { return tmem + 256u + 128u * (g & 1u); };
+#ifdef A2_PBUF
+  // P~ of each step parity in its own 32 columns (160..223) so QK(j+2) may overwrite S(j) before P~(j) exists
+  auto tm_p = [tmem](uint32_t g) { return tmem + 160u + 32u * (g & 1u); };
+#else
+  auto tm_p = [tm_s](uint32_t g) { return tm_s(g); };  // P~ over the first 32 columns of S(j)
+#endif
   const float tau = p.exact ? 0.0f : p.tau;
 
   if (warp >= kSoftmaxWarps) regs_dec<kRegsProducer>();
@@ -268,11 +289,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     if (rank == 0) {
       // ------------------------------------------------------------ MMA issuer (leader CTA only)
       constexpr uint32_t idesc_qk = idesc_f8(256, 128, FMT, FMT, 0);
-      constexpr uint32_t idesc_pv = idesc_f8(256, 128, FPSA_E4M3, FMT, 1);
+      // PV: N = 160, each CTA's B half is [64 V channels | 16 ones]: O columns 0-63 and 80-143 hold the
+      // channels, 64-79 and 144-159 the row sum of P~ (the tensor core sums the rounded weights)
+      constexpr uint32_t idesc_pv = idesc_f8(256, 160, FPSA_E4M3, FMT, 1);
       const uint64_t dq0 = smem_desc_sw128(smem_u32(smem + S::kQ), 16, 1024);
       const uint64_t dk0 = smem_desc_sw128(smem_u32(smem + S::kK), 16, 1024);
-      uint64_t dv0 = smem_desc_sw128(smem_u32(smem + S::kV), 16, 512);
-      dv0 = (dv0 & ~((uint64_t)7 << 61)) | ((uint64_t)4 << 61);  // SWIZZLE_64B: 64-channel V halves
+      // SWIZZLE_64B MN-major V halves; the second MN atom (LBO) is the ones tile, the tail ones tile for a
+      // tile's last key block. Each stage step moves the start and shortens LBO by the same amount.
+      const uint32_t sv0 = smem_u32(smem + S::kV);
+      auto sw64 = [](uint64_t d) { return (d & ~((uint64_t)7 << 61)) | ((uint64_t)4 << 61); };
+      const uint64_t dv0 = sw64(smem_desc_sw128(sv0, smem_u32(smem + S::kOnes) - sv0, 512));
+      const uint64_t dvt0 = sw64(smem_desc_sw128(sv0, smem_u32(smem + S::kOnesTail) - sv0, 512));
+      constexpr uint64_t kVStageStep = (uint64_t)(S::kVHalf >> 4) - ((uint64_t)(S::kVHalf >> 4) << 16);
       uint32_t g = 0;
       int32_t iter = 0;
       uint32_t qk_st = 0, qk_ph = 0, pv_st = 0;
@@ -292,18 +320,34 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           mbar_wait(&bar_kv_peer[qk_st], qk_ph);
           tc_fence_after();
           const uint64_t dk = dk0 + qk_st * (S::kKHalf >> 4);
-#pragma unroll
-          for (int k = 0; k < D / 32; ++k) mma2_ss_w(tm_s(gg), dq + 2 * k, dk + 2 * k, idesc_qk, k > 0 ? 1u : 0u);
+          mma2_ss_x4_w(tm_s(gg), dq, 2, dk, 2, idesc_qk, 0u);
           commit2_w(&bar_s_full[gg & 1]);
           if (++qk_st == kStages) {
             qk_st = 0;
             qk_ph ^= 1;
           }
         };
-        for (int32_t s = 0; s < min(steps, 2); ++s) issue_qk(g + s);
+#ifdef A2_PBUF
+        auto wait_sfree = [&](uint32_t gg) {  // QK(gg) overwrites S(gg - 2): its owners must have loaded it
+          if (gg >= 2) mbar_wait(&bar_s_free[gg & 1], ((gg >> 1) - 1) & 1);
+        };
+#else
+        auto wait_sfree = [](uint32_t) {};  // PV(gg - 2), issued before QK(gg), has read P~ from S(gg - 2)
+#endif
+        for (int32_t s = 0; s < min(steps, 2); ++s) {
+          wait_sfree(g + s);
+          issue_qk(g + s);
+        }
         if (steps <= 2) commit2_w(&bar_qfree[qbuf]);
         for (int32_t s = 0; s < steps; ++s) {
           const uint32_t gs = g + s;
+#ifdef A2_PBUF
+          if (s + 2 < steps) {  // QK(j+2) as soon as S(j) is in registers, ahead of PV(j)
+            wait_sfree(gs + 2);
+            issue_qk(gs + 2);
+            if (s + 3 == steps) commit2_w(&bar_qfree[qbuf]);
+          }
+#endif
           A2_TL(0, gs, 0);
           mbar_wait(&bar_p_ready[gs & 1], (gs >> 1) & 1);
           A2_TL(0, gs, 1);
@@ -313,19 +357,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               mbar_wait(&bar_ofree, (iter - 1) & 1);
               tc_fence_after();
             }
-            const uint64_t dv = dv0 + pv_st * (S::kVHalf >> 4);
-            const uint32_t ts = tm_s(gs);
-#pragma unroll
-            for (int k = 0; k < kBlk / 32; ++k)  // keys 32k..: P~ columns 8k.., V rows 32k.. (32 x 64 B)
-              mma2_ts_w(tm_o, ts + 8 * k, dv + (uint64_t)k * (32 * 64 / 16), idesc_pv, (s > pv0 || k > 0) ? 1u : 0u);
+            const uint64_t dv = ((s - pv0) % p.nb == p.nb - 1 ? dvt0 : dv0) + pv_st * kVStageStep;
+            // keys 32k..: P~ columns 8k.., V rows 32k.. (32 x 64 B)
+            mma2_ts_x4_w(tm_o, tm_p(gs), dv, 32 * 64 / 16, idesc_pv, s > pv0 ? 1u : 0u);
           }
+          A2_TL(0, gs, 2);
+#ifdef A2_PBUF
+          commit2_w(&bar_p_free[gs & 1]);
+#endif
           commit2_w(&bar_kv_empty[pv_st]);
           if (++pv_st == kStages) pv_st = 0;
-          A2_TL(0, gs, 2);
+#ifndef A2_PBUF
           if (s + 2 < steps) {
             issue_qk(gs + 2);
             if (s + 3 == steps) commit2_w(&bar_qfree[qbuf]);
           }
+#endif
           A2_TL(0, gs, 3);
         }
         commit2_w(&bar_o);
@@ -418,7 +465,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       };
       float m_ref = 0.0f;
       uint32_t sat = 0u;
-      f2 lsum = bcast(0.0f);
       if (p.exact) {
         float m_acc = -INFINITY;
         int32_t kt = 0, b = 0;
@@ -428,6 +474,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             mbar_wait(&bar_s_full[g & 1], (g >> 1) & 1);
             tc_fence_after();
             m_acc = fmaxf(m_acc, block_max<kBlk>(tm_s(g) + lane_off, ncol_blk(b), false) * c);
+#ifdef A2_PBUF
+            signal(&bar_s_free[g & 1]);
+            if (g >= 2) mbar_wait(&bar_p_free[g & 1], ((g >> 1) - 1) & 1);  // keeps the phases in step
+#endif
             signal(&bar_p_ready[g & 1]);
           }
           if (b == p.nb - 1) {
@@ -464,16 +514,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
               uint32_t sreg[64];
               load_s_all<64>(s_row, sreg);
               tmem_wait_ld();
-              sat |= p_regs_sum<64>(sreg, min(n, 64), c, bias, w, lsum);
+              sat |= compute_p_regs<64>(sreg, min(n, 64), c, bias, w);
             }
             {
               uint32_t sreg[64];
               load_s_all<64>(s_row + 64, sreg);
               tmem_wait_ld();
-              sat |= p_regs_sum<64>(sreg, max(n - 64, 0), c, bias, w + 16, lsum);
+#ifdef A2_PBUF
+              signal(&bar_s_free[g & 1]);
+#endif
+              sat |= compute_p_regs<64>(sreg, max(n - 64, 0), c, bias, w + 16);
             }
             if (warp == 0 || warp == 4) A2_TL(1 + rank, g, 2);
-            tmem_st32(s_row, w);
+#ifdef A2_PBUF
+            if (g >= 2) {
+              mbar_wait(&bar_p_free[g & 1], ((g >> 1) - 1) & 1);  // PV(j-2) has read this P~ buffer
+              tc_fence_after();
+            }
+#endif
+            tmem_st32(tm_p(g) + lane_off, w);
             tmem_wait_st();
             signal(&bar_p_ready[g & 1]);
             if (warp == 0 || warp == 4) A2_TL(1 + rank, g, 3);
@@ -487,10 +546,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
       }
       // ---------------------------------------------------------- epilogue
-      const float l = row_comb(lsum.x + lsum.y, false);
       mbar_wait(&bar_o, iter & 1);
       tc_fence_after();
-      const float inv_l = 1.0f / l;
+      float inv_l;
+      {
+        uint32_t lw[16];
+        tmem_ld16(tm_o + lane_off + 64, lw);  // row sum of P~ (the ones columns of CTA 0's half)
+        tmem_wait_ld();
+        inv_l = 1.0f / __uint_as_float(lw[0]);
+      }
       const int32_t r = qb * kBlk + row;
       int64_t token;
       if (p.natural) {
@@ -505,7 +569,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       for (int cc = 0; cc < D / 2; cc += 32) {
         const int col = part * (D / 2) + cc;
         uint32_t o[32];
-        tmem_ld32(tm_o + lane_off + col, o);
+        tmem_ld32(tm_o + lane_off + col + (col >= 64 ? 16 : 0), o);
         tmem_wait_ld();
         if (r < p.tv) {
           float f[32];
