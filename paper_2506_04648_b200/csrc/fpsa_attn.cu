@@ -56,6 +56,11 @@
 #include "sm100.cuh"
 #include "softmax.cuh"
 
+#ifndef FPSA_MMA_HOIST
+#define FPSA_MMA_HOIST 1
+#endif
+
+
 namespace fpsa {
 namespace {
 
@@ -302,49 +307,100 @@ __global__ void __launch_bounds__(kThreads, 1)
       };
       for (int32_t s = 0; s < min(steps, 2); ++s) issue_qk(g + s);
       if (steps <= 2) mma_commit_w(&bar_qfree[qbuf]);
-      for (int32_t s = 0; s < steps; ++s) {
-        const uint32_t gs = g + s;
-#ifdef FPSA_TRACE
-        const long long tp0 = clock64();
-#endif
-        FPSA_TL(9, 0, gs);
-        mbar_wait(&bar_p_ready[gs & 1], (gs >> 1) & 1);
-        FPSA_TL(9, 1, gs);
-#ifdef FPSA_TRACE
-        if (lane == 0) atomicAdd(&g_trace[3], (unsigned long long)(clock64() - tp0));
-#endif
-        tc_fence_after();
-        if (s >= pv0) {
-          // [O|l] += P~ [V|1]: P~ of the keys of row part c sits in the first columns of that part's
-          // S columns; the B descriptor's leading byte offset points from V at the ones atom
-          if (s == pv0 && iter > 0) {
-            mbar_wait(&bar_ofree, (iter - 1) & 1);  // the previous item's epilogue has read O
-            tc_fence_after();
+#if FPSA_MMA_HOIST
+      if constexpr (kPingPong && D == 128) {
+        // Everything that does not depend on P~(j) is done before waiting for it: the K/V-full wait and
+        // descriptors of QK(j+2), the V descriptor of PV(j), the O-free wait. After p_ready(j) the warp
+        // only issues PV(j), QK(j+2) and the commits (the issue path is the step's critical path).
+        for (int32_t s = 0; s < steps; ++s) {
+          const uint32_t gs = g + s;
+          const bool do_qk = s + 2 < steps;
+          uint64_t dk = 0;
+          if (do_qk) {
+            mbar_wait(&bar_kv_full[qk_st], qk_ph);
+            dk = dk0 + qk_st * kTileU;
           }
-          const uint64_t dv = (bp == p.nb - 1 ? dvt0 : dv0) + pv_st * kVStageStep;
-          const uint32_t ts = tm_s(gs);
-#ifndef FPSA_NO_MMA
-          if constexpr (kPingPong) {  // one elect for the four K32 MMAs (shorter issue path)
-            constexpr uint64_t kVk = 32 * D / 16;
-            mma_f8_ts_x4_w(tm_o, ts, ts + 8, ts + 16, ts + 24, dv, dv + kVk, dv + 2 * kVk, dv + 3 * kVk, idesc_pv,
-                           s > pv0 ? 1u : 0u);
-          } else {
+          constexpr uint64_t kVk = 32 * D / 16;
+          uint64_t dv[4], dkk[4], dqq[4];
+          uint32_t ta[4];
+          dv[0] = (bp == p.nb - 1 ? dvt0 : dv0) + pv_st * kVStageStep;
+          const uint32_t ts = tm_s(gs);  // S(j), P~(j) and S(j+2) share the buffer
 #pragma unroll
-            for (int k = 0; k < kBlk / 32; ++k)
-              mma_f8_ts_w(tm_o, kPingPong ? ts + 8 * k : ts + kPartCols * (32 * k / kPartCols) + 8 * (k % (kPartCols / 32)),
-                          dv + (uint64_t)k * (32 * D / 16), idesc_pv,
-                          (s > pv0 || k > 0) ? 1u : 0u);
+          for (int k = 0; k < 4; ++k) {
+            dv[k] = dv[0] + k * kVk;
+            dkk[k] = dk + 2 * k;
+            dqq[k] = dq + 2 * k;
+            ta[k] = ts + 8 * k;
           }
-#endif
+          if (s == pv0 && iter > 0) mbar_wait(&bar_ofree, (iter - 1) & 1);  // the previous item's epilogue read O
+          FPSA_TL(9, 0, gs);
+          mbar_wait(&bar_p_ready[gs & 1], (gs >> 1) & 1);
+          FPSA_TL(9, 1, gs);
+          tc_fence_after();
+          if (s >= pv0)
+            mma_f8_ts_x4_w(tm_o, ta[0], ta[1], ta[2], ta[3], dv[0], dv[1], dv[2], dv[3], idesc_pv, s > pv0 ? 1u : 0u);
+          FPSA_TL(9, 2, gs);
+          if (do_qk) {
+            mma_f8_ss_x4_w(ts, dqq[0], dqq[1], dqq[2], dqq[3], dkk[0], dkk[1], dkk[2], dkk[3], idesc_qk, 0u);
+            mma_commit_w(&bar_s_full[gs & 1]);
+            FPSA_TL(9, 3, gs);
+            if (++qk_st == kStages) {
+              qk_st = 0;
+              qk_ph ^= 1;
+            }
+            if (s + 3 == steps) mma_commit_w(&bar_qfree[qbuf]);
+          }
+          mma_commit_w(&bar_kv_empty[pv_st]);  // after QK(j+2): the stage is released when both are done
+          if (++pv_st == kStages) pv_st = 0;
+          if (++bp == p.nb) bp = 0;
         }
-        mma_commit_w(&bar_kv_empty[pv_st]);
-        if (++pv_st == kStages) pv_st = 0;
-        if (++bp == p.nb) bp = 0;
-        FPSA_TL(9, 2, gs);
-        if (s + 2 < steps) {
-          issue_qk(gs + 2);
-          FPSA_TL(9, 3, gs);
-          if (s + 3 == steps) mma_commit_w(&bar_qfree[qbuf]);
+      } else
+#endif
+      {
+      for (int32_t s = 0; s < steps; ++s) {
+          const uint32_t gs = g + s;
+  #ifdef FPSA_TRACE
+          const long long tp0 = clock64();
+  #endif
+          FPSA_TL(9, 0, gs);
+          mbar_wait(&bar_p_ready[gs & 1], (gs >> 1) & 1);
+          FPSA_TL(9, 1, gs);
+  #ifdef FPSA_TRACE
+          if (lane == 0) atomicAdd(&g_trace[3], (unsigned long long)(clock64() - tp0));
+  #endif
+          tc_fence_after();
+          if (s >= pv0) {
+            // [O|l] += P~ [V|1]: P~ of the keys of row part c sits in the first columns of that part's
+            // S columns; the B descriptor's leading byte offset points from V at the ones atom
+            if (s == pv0 && iter > 0) {
+              mbar_wait(&bar_ofree, (iter - 1) & 1);  // the previous item's epilogue has read O
+              tc_fence_after();
+            }
+            const uint64_t dv = (bp == p.nb - 1 ? dvt0 : dv0) + pv_st * kVStageStep;
+            const uint32_t ts = tm_s(gs);
+  #ifndef FPSA_NO_MMA
+            if constexpr (kPingPong) {  // one elect for the four K32 MMAs (shorter issue path)
+              constexpr uint64_t kVk = 32 * D / 16;
+              mma_f8_ts_x4_w(tm_o, ts, ts + 8, ts + 16, ts + 24, dv, dv + kVk, dv + 2 * kVk, dv + 3 * kVk, idesc_pv,
+                             s > pv0 ? 1u : 0u);
+            } else {
+  #pragma unroll
+              for (int k = 0; k < kBlk / 32; ++k)
+                mma_f8_ts_w(tm_o, kPingPong ? ts + 8 * k : ts + kPartCols * (32 * k / kPartCols) + 8 * (k % (kPartCols / 32)),
+                            dv + (uint64_t)k * (32 * D / 16), idesc_pv,
+                            (s > pv0 || k > 0) ? 1u : 0u);
+            }
+  #endif
+          }
+          mma_commit_w(&bar_kv_empty[pv_st]);
+          if (++pv_st == kStages) pv_st = 0;
+          if (++bp == p.nb) bp = 0;
+          FPSA_TL(9, 2, gs);
+          if (s + 2 < steps) {
+            issue_qk(gs + 2);
+            FPSA_TL(9, 3, gs);
+            if (s + 3 == steps) mma_commit_w(&bar_qfree[qbuf]);
+          }
         }
       }
       mma_commit_w(&bar_o);
