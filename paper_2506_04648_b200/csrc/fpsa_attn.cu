@@ -59,6 +59,9 @@
 #ifndef FPSA_MMA_HOIST
 #define FPSA_MMA_HOIST 1
 #endif
+#ifndef FPSA_MMA_ONE_ELECT
+#define FPSA_MMA_ONE_ELECT 1
+#endif
 
 
 namespace fpsa {
@@ -337,6 +340,20 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(&bar_p_ready[gs & 1], (gs >> 1) & 1);
           FPSA_TL(9, 1, gs);
           tc_fence_after();
+#if FPSA_MMA_ONE_ELECT
+          mma_attn_step_w(tm_o, ts, dv[0], dv[1], dv[2], dv[3], idesc_pv, s > pv0 ? 1u : 0u, s >= pv0 ? 1u : 0u, ts,
+                          dqq[0], dqq[1], dqq[2], dqq[3], dkk[0], dkk[1], dkk[2], dkk[3], idesc_qk, do_qk ? 1u : 0u,
+                          smem_u32(&bar_s_full[gs & 1]), smem_u32(&bar_kv_empty[pv_st]));
+          FPSA_TL(9, 2, gs);
+          if (do_qk) {
+            FPSA_TL(9, 3, gs);
+            if (++qk_st == kStages) {
+              qk_st = 0;
+              qk_ph ^= 1;
+            }
+            if (s + 3 == steps) mma_commit_w(&bar_qfree[qbuf]);
+          }
+#else
           if (s >= pv0)
             mma_f8_ts_x4_w(tm_o, ta[0], ta[1], ta[2], ta[3], dv[0], dv[1], dv[2], dv[3], idesc_pv, s > pv0 ? 1u : 0u);
           FPSA_TL(9, 2, gs);
@@ -351,6 +368,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (s + 3 == steps) mma_commit_w(&bar_qfree[qbuf]);
           }
           mma_commit_w(&bar_kv_empty[pv_st]);  // after QK(j+2): the stage is released when both are done
+#endif
           if (++pv_st == kStages) pv_st = 0;
           if (++bp == p.nb) bp = 0;
         }
