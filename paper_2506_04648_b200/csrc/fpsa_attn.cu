@@ -176,7 +176,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   __shared__ uint32_t s_ovf[2];      // per item parity: some row overflowed
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int32_t* items = p.exact ? p.redo + kRedoHeader : p.items;
+  // re-read from the parameter bank at each use (a long-lived pointer is spilled across the role switch)
+  auto item_at = [&p](int32_t i) { return (p.exact ? p.redo + kRedoHeader : p.items)[i]; };
   const int32_t count = p.exact ? *reinterpret_cast<volatile int32_t*>(p.redo) : p.n_items;
   if ((int32_t)blockIdx.x >= count) return;
 
@@ -231,7 +232,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t g = 0;  // K/V block counter over all items of this CTA
     int32_t iter = 0;
     for (int32_t it = blockIdx.x; it < count; it += gridDim.x, ++iter) {
-      const int32_t h = items[3 * it], u = items[3 * it + 1], qb = items[3 * it + 2];
+      const int32_t h = item_at(3 * it), u = item_at(3 * it + 1), qb = item_at(3 * it + 2);
       const int32_t kt0 = __ldg(p.offs + u), n_kt = __ldg(p.offs + u + 1) - kt0;
       const int32_t n_kv = n_kt * p.nb, steps = p.exact ? 2 * n_kv : n_kv;
       const int qbuf = iter & 1;
@@ -274,7 +275,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t qk_st = 0, qk_ph = 0;  // K/V stage + full-barrier phase of the next QK
     uint32_t pv_st = 0;             // K/V stage of the next PV
     for (int32_t it = blockIdx.x; it < count; it += gridDim.x, ++iter) {
-      const int32_t u = items[3 * it + 1];
+      const int32_t u = item_at(3 * it + 1);
       const int32_t n_kt = __ldg(p.offs + u + 1) - __ldg(p.offs + u);
       const int32_t n_kv = n_kt * p.nb, steps = p.exact ? 2 * n_kv : n_kv;
       const int32_t pv0 = p.exact ? n_kv : 0;  // first step with a PV
@@ -431,7 +432,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int32_t it = blockIdx.x; it < count; it += gridDim.x, ++iter) {
       const int slot = iter & 1;
       if (iter >= 2) mbar_wait(&bar_meta_empty[slot], ((iter >> 1) - 1) & 1);
-      const int32_t h = items[3 * it], u = items[3 * it + 1];
+      const int32_t h = item_at(3 * it), u = item_at(3 * it + 1);
       const int32_t kt0 = __ldg(p.offs + u), n_kt = __ldg(p.offs + u + 1) - kt0;
       const float qs = (float)__ldg(p.q_scales + h * p.M + u);
       const double* ks = p.k_scales + (int64_t)h * p.M;
@@ -471,7 +472,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     int64_t n_steps = 0;
 #endif
     for (int32_t it = blockIdx.x; it < count; it += gridDim.x, ++iter) {
-      const int32_t h = items[3 * it], u = items[3 * it + 1], qb = items[3 * it + 2];
+      const int32_t h = item_at(3 * it), u = item_at(3 * it + 1), qb = item_at(3 * it + 2);
       const int slot = iter & 1;
       mbar_wait(&bar_meta_full[slot], (iter >> 1) & 1);
       const int32_t kt0 = s_hdr[slot][0], n_kt = s_hdr[slot][1];
