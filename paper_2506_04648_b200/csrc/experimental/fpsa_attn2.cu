@@ -22,10 +22,10 @@
 // the pair's QK + PV step takes 576 clk back to back and 974 clk issue-to-completion in isolation, and
 // neither concurrent tcgen05.ld traffic nor FMA/MUFU-saturated warps on the same SM change that by more
 // than 5 %; in the kernel one MMA-warp iteration takes ~1450 clk, ~650 of them between p_ready and the last
-// PV issue. ncu's source counters for the single-CTA kernel show the same: the MMA warp is resident the
-// whole time, ~20 % waiting for p_ready and ~80 % executing its ~180-instruction step (descriptor
+// PV issue. ncu's source counters for the single-CTA kernel point the same way (tools/mma_warp_share.py):
+// the MMA warp spends about half of the launch executing its ~140-instruction step body (descriptor
 // arithmetic, R2UR moves, elect / divergence checks, barrier address math) at a few cycles per dependent
-// instruction ('wait' and 'long_sb' stalls, 'not_selected' against the softmax warps). Halving the MMA
+// instruction ('wait', 'selected', 'not_selected' against the softmax warps) and ~20 % waiting for p_ready. Halving the MMA
 // work per SM therefore does not shorten the step; the issue path does. Tried without gain: in-asm
 // descriptor steps (ptxas adds SELs), issuing from one lane (ptxas wraps each MMA in an elect loop), more
 // producer registers (same SASS).  Build and A/B:
