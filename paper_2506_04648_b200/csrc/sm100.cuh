@@ -38,20 +38,38 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                : "memory");
 }
+#ifndef FPSA_MBAR_SUSPEND_NS
+#define FPSA_MBAR_SUSPEND_NS 100000
+#endif
+// kSuspendNs > 0: suspend-time hint; the waiting warp sleeps until the phase completes (or the hint
+// elapses) instead of re-issuing try_wait, which takes issue slots from the warps that share its SM
+// sub-partition (attention at C2: 11.54 -> 11.13 ms, profiles/r01_ab_mbar_suspend_r3z.txt).
+template <uint32_t kSuspendNs = FPSA_MBAR_SUSPEND_NS>
 __device__ __forceinline__ bool mbar_try_wait(uint32_t addr, uint32_t parity) {
   uint32_t ok;
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-      "selp.u32 %0, 1, 0, p;\n\t}"
-      : "=r"(ok)
-      : "r"(addr), "r"(parity)
-      : "memory");
+  if constexpr (kSuspendNs > 0) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(addr), "r"(parity), "n"(kSuspendNs)
+        : "memory");
+  } else {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(addr), "r"(parity)
+        : "memory");
+  }
   return ok != 0;
 }
+template <uint32_t kSuspendNs = FPSA_MBAR_SUSPEND_NS>
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t addr = smem_u32(bar);
-  while (!mbar_try_wait(addr, parity)) {
+  while (!mbar_try_wait<kSuspendNs>(addr, parity)) {
   }
 }
 
