@@ -41,9 +41,9 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
 #ifndef FPSA_MBAR_SUSPEND_NS
 #define FPSA_MBAR_SUSPEND_NS 100000
 #endif
-// kSuspendNs > 0: suspend-time hint; the waiting warp sleeps until the phase completes (or the hint
-// elapses) instead of re-issuing try_wait, which takes issue slots from the warps that share its SM
-// sub-partition (attention at C2: 11.54 -> 11.13 ms, profiles/r01_ab_mbar_suspend_r3z.txt).
+// kSuspendNs > 0: suspend-time hint on try_wait (attention at C2: 11.54 -> 11.13 ms,
+// profiles/r01_ab_mbar_suspend_r3z.txt). The try_wait count per launch drops only ~10 %, so the gain is
+// more likely a faster wake-up on phase completion than fewer re-issued polls.
 template <uint32_t kSuspendNs = FPSA_MBAR_SUSPEND_NS>
 __device__ __forceinline__ bool mbar_try_wait(uint32_t addr, uint32_t parity) {
   uint32_t ok;
