@@ -56,6 +56,8 @@ def parse():
     ap.add_argument("--ulysses", action="store_true", help="sequence-sharded inputs + all-to-all (C3)")
     ap.add_argument("--ulysses-chunk", type=int, default=1,
                     help="heads per pipelined all-to-all chunk (0: one all-to-all per tensor, no overlap)")
+    ap.add_argument("--dump-out", default=None,
+                    help="directory: each rank writes sha256 of its heads' outputs (head-parallel runs)")
     return ap.parse_args()
 
 
@@ -64,6 +66,54 @@ def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return world, rank, local
+
+
+def relaunch(n: int) -> int:
+    """--gpus N > 1 without a torchrun environment: start N ranks of this script (one process per GPU)
+    under torch.distributed.run on 127.0.0.1 and return their exit status (rank 0 prints the line)."""
+    import socket
+    import subprocess
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.run(cmd).returncode
+
+
+class Group:
+    """Process group for the timing collectives (barrier, max over ranks).  NCCL when every rank has its
+    own GPU; gloo when ranks share one (the CPU-side multi-rank test: NCCL refuses two ranks on a device)."""
+
+    def __init__(self, world: int, local: int, torch, dist):
+        self.world, self.dist, self.torch = world, dist, torch
+        n_dev = torch.cuda.device_count()
+        self.device = torch.device("cuda", local % n_dev)
+        torch.cuda.set_device(self.device)
+        self.backend = None
+        if world > 1:
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            local_world = int(os.environ.get("LOCAL_WORLD_SIZE", world))
+            self.backend = "nccl" if n_dev >= local_world else "gloo"
+            kw = {"device_id": self.device} if self.backend == "nccl" else {}
+            dist.init_process_group(self.backend, **kw)
+
+    def barrier(self):
+        if self.world > 1:
+            self.dist.barrier()
+
+    def max(self, values):
+        if self.world == 1:
+            return list(values)
+        dev = self.device if self.backend == "nccl" else "cpu"
+        t = self.torch.tensor(list(values), device=dev, dtype=self.torch.float64)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return t.tolist()
+
+    def close(self):
+        if self.world > 1:
+            self.dist.destroy_process_group()
 
 
 # ---------------------------------------------------------------------------- clocks
@@ -230,6 +280,11 @@ def run_reference(args):
 # ---------------------------------------------------------------------------- GPU leg
 def main():
     args = parse()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        return relaunch(args.gpus)
+    world, rank, local = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but the launcher started {world} rank(s)")
     if args.impl == "reference":
         return run_reference(args)
     import torch
@@ -237,14 +292,8 @@ def main():
 
     import paper_2506_04648_b200 as fpsa
 
-    world, rank, local = dist_env()
-    if world > 1:
-        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    else:
-        torch.cuda.set_device(0)
-    dev = torch.device("cuda", torch.cuda.current_device())
+    group = Group(world, local, torch, dist)
+    dev = group.device
     grid, H, d, tile, win = CONFIGS[args.config]
     L = grid[0] * grid[1] * grid[2]
     from paper_2506_04648_b200.sharding import UlyssesAttention, head_range
@@ -252,15 +301,24 @@ def main():
     if args.ulysses:
         if world < 2 or H % world or L % world:
             raise SystemExit("--ulysses needs >= 2 ranks dividing both the heads and the tokens")
+        if group.backend != "nccl":
+            raise SystemExit("--ulysses needs one GPU per rank (NCCL all-to-all)")
         h0, h1 = 0, H  # every rank holds all heads of its token shard
         Lr, Hr = L // world, H
     else:
         h0, h1 = head_range(rank, world, H)
         Lr, Hr = L, h1 - h0
-    gen = torch.Generator(device=dev).manual_seed(1234 + rank)
-    q = torch.randn((Lr, Hr, d), generator=gen, device=dev).to(torch.bfloat16)
-    k = torch.randn((Lr, Hr, d), generator=gen, device=dev).to(torch.bfloat16)
-    v = torch.randn((Lr, Hr, d), generator=gen, device=dev).to(torch.bfloat16)
+    gen = torch.Generator(device=dev)
+    if args.ulysses:
+        gen.manual_seed(1234 + rank)
+        q, k, v = (torch.randn((Lr, Hr, d), generator=gen, device=dev).to(torch.bfloat16) for _ in range(3))
+    else:
+        # per-head seeds: head h gets the same q, k, v whatever the rank count (--dump-out compares them)
+        q, k, v = (torch.empty((Lr, Hr, d), dtype=torch.bfloat16, device=dev) for _ in range(3))
+        for j in range(Hr):
+            gen.manual_seed(1234 + h0 + j)
+            for x in (q, k, v):
+                x[:, j].copy_(torch.randn((Lr, d), generator=gen, device=dev))
     out = torch.empty_like(q)
     if args.ulysses:
         uly = UlyssesAttention(grid, tile, win, H, d, device=dev, tau=args.tau,
@@ -278,9 +336,7 @@ def main():
     flops = plan.flops  # this rank's heads
     flops_total = plan.flops // plan.heads * H if not args.ulysses else plan.flops * world
 
-    def barrier():
-        if world > 1:
-            dist.barrier()
+    barrier = group.barrier
 
     stream = torch.cuda.current_stream()
     for _ in range(args.warmup):
@@ -314,10 +370,7 @@ def main():
     ms_quant = sum(a.elapsed_time(b) for a, b, _ in ev) / args.steps
     ms_attn = sum(b.elapsed_time(c) for _, b, c in ev) / args.steps
     ms_step = ms_total / args.steps
-    if world > 1:
-        tt = torch.tensor([ms_step, ms_attn, ms_quant], device=dev, dtype=torch.float64)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        ms_step, ms_attn, ms_quant = tt.tolist()
+    ms_step, ms_attn, ms_quant = group.max([ms_step, ms_attn, ms_quant])
     total_flops = flops_total
     value = total_flops / (ms_step * 1e-3) / 1e12
 
@@ -353,10 +406,7 @@ def main():
         torch.cuda.synchronize()
         barrier()
         ms_e2e = s.elapsed_time(e) / steps_e2e
-        if world > 1:
-            tt = torch.tensor([ms_e2e], device=dev, dtype=torch.float64)
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            ms_e2e = tt.item()
+        (ms_e2e,) = group.max([ms_e2e])
         e2e = {"value": total_flops / (ms_e2e * 1e-3) / 1e12, "unit": "TFLOPS", "ms_per_step": ms_e2e,
                "h2d_bytes_per_step": 3 * q.numel() * q.element_size(),
                "d2h_bytes_per_step": out.numel() * out.element_size(),
@@ -364,9 +414,18 @@ def main():
                        "paper_2506_04648_b200.HostStreamer.__call__ (FpsaPlan.quantize + .attention per head chunk, "
                        "fpsa_copy2d transfers overlapped)") + " via the C ABI, pinned host"}
 
+    if args.dump_out and not args.ulysses:
+        import hashlib
+
+        step(q, k, v, out)
+        torch.cuda.synchronize()
+        os.makedirs(args.dump_out, exist_ok=True)
+        digests = {str(h0 + j): hashlib.sha256(out[:, j].contiguous().cpu().numpy().tobytes()).hexdigest()
+                   for j in range(Hr)}
+        with open(os.path.join(args.dump_out, f"rank{rank}.json"), "w") as f:
+            json.dump(digests, f)
     if rank != 0:
-        if world > 1:
-            dist.destroy_process_group()
+        group.close()
         return 0
 
     peaks = measured_peaks()
@@ -430,8 +489,7 @@ def main():
                       f"fp8sta.fp8_sparse_forward, numpy, thread pool over tiles), {cb['seconds']:.1f} s",
         }
     print(json.dumps(line))
-    if world > 1:
-        dist.destroy_process_group()
+    group.close()
     return 0
 
 

@@ -45,6 +45,9 @@ typedef enum {
 typedef enum { FPSA_F32 = 0, FPSA_BF16 = 1, FPSA_F16 = 2 } fpsa_dtype;
 typedef enum { FPSA_E4M3 = 0, FPSA_E5M2 = 1 } fpsa_fmt;
 typedef enum { FPSA_ORDER_TILE = 0, FPSA_ORDER_NATURAL = 1 } fpsa_order;
+/* Softmax-weight semantics of fpsa_attn_fwd: one-pass (unnormalised weights re-quantised per key block,
+ * the fast path) or normalised (the reference's exact P = e4m3(448 * p), attention.py:133-145). */
+typedef enum { FPSA_P_ONEPASS = 0, FPSA_P_NORMALIZED = 1 } fpsa_p_mode;
 
 typedef struct {
   int32_t t, h, w;
@@ -135,13 +138,17 @@ int fpsa_attn_workspace_bytes(int32_t n_items, int64_t* bytes);
  *   out: element (token, head, c) at out + token*out_token_stride +
  *        head*out_head_stride + c, tokens in out_order, dtype out_dtype
  *   tau_log2: headroom of the one-pass softmax above the first block's row max (0..8)
+ *   p_mode: FPSA_P_ONEPASS, or FPSA_P_NORMALIZED: three passes per item (exact row max, f64 row sum,
+ *           then P = e4m3(448 * exp(s - m) / f32(l)) with a correctly rounded exp) and
+ *           out = O * f32(v_scale / 448): the reference's arithmetic step for step; f32 output only,
+ *           no redo launch (tau_log2 unused)
  *   workspace: device, >= fpsa_attn_workspace_bytes(n_items); word 0 = number of
  *              items recomputed exactly by this call (readable after the stream syncs)
  * Replaces fp8_sparse_forward / _engine (fp8sta/attention.py:91-149, :179-208). */
 int fpsa_attn_fwd(const uint8_t* q_codes, const uint8_t* k_codes, const uint8_t* v_codes, const double* q_scales,
                   const double* k_scales, const double* v_scales, int32_t heads, fpsa_dims3 grid, fpsa_dims3 tile,
                   int32_t d, int32_t tile_pitch, const int32_t* offs, const int32_t* ids, const int32_t* items,
-                  int32_t n_items, float softmax_scale, int fmt, float tau_log2, void* out, int out_dtype,
+                  int32_t n_items, float softmax_scale, int fmt, float tau_log2, int p_mode, void* out, int out_dtype,
                   int64_t out_token_stride, int64_t out_head_stride, int out_order, void* workspace,
                   int64_t workspace_bytes, void* stream);
 

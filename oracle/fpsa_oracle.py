@@ -24,6 +24,7 @@ __all__ = [
     "axis_interval", "window_lists", "density_of", "flops_sparse_of",
     "regime_of", "schedule_valid",
     "fp8_sparse_forward", "sparse_forward_f32", "onepass_forward", "bf16_round", "passthrough_emulation",
+    "normalized_rows", "p_flip_budget",
     "cosine", "max_abs", "gen_inputs",
 ]
 
@@ -320,6 +321,57 @@ def fp8_sparse_forward(q, k, v, tv, offs, ids, fmt: Fmt = E4M3, softmax_scale=No
         scale, quant_p=True,
     )
     return out, dict(q_codes=qc, q_scales=qs, k_codes=kc, k_scales=ks, v_codes=vc, v_scales=vs)
+
+
+def normalized_rows(q, k, v, tv, offs, ids, rows, fmt: Fmt = E4M3, softmax_scale=None):
+    """Per-row intermediates of the reference's quantised forward for selected rows (attention.py:179-208,
+    _engine :118-149): yields (row, x = f32(p) * 448 before rounding, decoded V rows of its keys, v_fac).
+    The same arithmetic as _tile_attention restricted to single rows (the f32 GEMM of one row)."""
+    q = np.ascontiguousarray(q, dtype=np.float32)
+    scale = _softmax_scale(q.shape[1], softmax_scale)
+    qc, qs = quantize_qk_tilewise(q, tv, fmt)
+    kc, ks = quantize_qk_tilewise(np.asarray(k, np.float32), tv, fmt)
+    vc, vs = quantize_v_channelwise(np.asarray(v, np.float32), fmt)
+    qv, kv, vv = decode(qc, fmt), decode(kc, fmt), decode(vc, fmt)
+    q_fac, k_fac = qs.astype(np.float32), ks.astype(np.float32)
+    v_fac = (vs * (1.0 / 448.0)).astype(np.float32)
+    lanes = np.arange(tv, dtype=np.int64)
+    for r in rows:
+        u = int(r) // tv
+        keys = ids[offs[u]:offs[u + 1]].astype(np.int64)
+        kr = (keys[:, None] * tv + lanes[None, :]).reshape(-1)
+        s = qv[r:r + 1] @ kv[kr].T
+        s *= (np.repeat(k_fac[keys], tv) * (q_fac[u] * scale))[None, :]
+        s -= s.max(axis=1, keepdims=True)
+        np.exp(s, out=s)
+        s /= s.sum(axis=1, dtype=np.float64, keepdims=True).astype(np.float32)
+        s *= np.float32(448.0)
+        yield int(r), s[0], vv[kr], v_fac
+
+
+def p_flip_budget(q, k, v, tv, offs, ids, rows, fmt: Fmt = E4M3, softmax_scale=None, rel: float = 2.0 ** -19):
+    """Bound on how far a correct implementation of the normalised-P forward may move each output element
+    of `rows` away from the reference through P-code flips.
+
+    The reference rounds x = 448 p onto the E4M3 grid (attention.py:143-145).  x itself depends on a float32
+    GEMM, exp and division whose last bits differ between numpy builds and a GPU (numpy's f32 exp is not
+    correctly rounded: up to 2 ulp), so an x within `rel` (relative) of a rounding midpoint may round to
+    either neighbour.  Each such weight can move output channel c by (hi - lo) |V_j,c| v_fac[c].  Returns
+    (budget [len(rows), d] float64, number of ambiguous weights)."""
+    grid = _VALUES["e4m3"][:0x7F].astype(np.float64)  # non-negative finite E4M3 values, ascending
+    d = np.asarray(q).shape[1]
+    budget = np.zeros((len(rows), d), dtype=np.float64)
+    n_amb = 0
+    for i, (_, x, vrows, v_fac) in enumerate(normalized_rows(q, k, v, tv, offs, ids, rows, fmt, softmax_scale)):
+        xd = x.astype(np.float64)
+        hi_i = np.clip(np.searchsorted(grid, xd, side="left"), 1, len(grid) - 1)
+        lo, hi = grid[hi_i - 1], grid[hi_i]
+        amb = np.abs(xd - 0.5 * (lo + hi)) <= rel * np.maximum(xd, 2.0 ** -6)
+        amb &= xd < grid[-1]
+        if amb.any():
+            n_amb += int(amb.sum())
+            budget[i] = ((hi - lo)[amb][:, None] * np.abs(vrows[amb].astype(np.float64))).sum(0) * v_fac
+    return budget, n_amb
 
 
 def sparse_forward_f32(q, k, v, tv, offs, ids, softmax_scale=None):

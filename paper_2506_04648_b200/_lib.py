@@ -26,6 +26,7 @@ FPSA_ECAPACITY = 7
 F32, BF16, F16 = 0, 1, 2
 E4M3_ID, E5M2_ID = 0, 1
 ORDER_TILE, ORDER_NATURAL = 0, 1
+P_ONEPASS, P_NORMALIZED = 0, 1  # fpsa_p_mode
 
 
 class Dims3(ctypes.Structure):
@@ -61,7 +62,8 @@ SIGNATURES = {
     "fpsa_attn_worklist": (_c.c_int, [_i32, Dims3, _i32, _pi32, _pi32, _i64, _pi64]),
     "fpsa_attn_workspace_bytes": (_c.c_int, [_i32, _pi64]),
     "fpsa_attn_fwd": (_c.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _i32, Dims3, Dims3, _i32, _i32, _vp, _vp, _vp, _i32,
-                                 _f32, _c.c_int, _f32, _vp, _c.c_int, _i64, _i64, _c.c_int, _vp, _i64, _vp]),
+                                 _f32, _c.c_int, _f32, _c.c_int, _vp, _c.c_int, _i64, _i64, _c.c_int, _vp, _i64,
+                                 _vp]),
     "fpsa_tile_gather_bf16": (_c.c_int, [_vp, _c.c_int, _i64, _i64, _i32, Dims3, Dims3, _i32, _i32, _c.c_int, _vp,
                                          _vp]),
     "fpsa_attn_bf16_fwd": (_c.c_int, [_vp, _vp, _vp, _i32, Dims3, Dims3, _i32, _i32, _vp, _vp, _vp, _i32, _f32, _vp,

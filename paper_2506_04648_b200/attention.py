@@ -8,11 +8,22 @@ path); CUDA tensor inputs give a CUDA tensor.  ``passthrough`` (the
 full-precision branch, attention.py:192-194) runs the bf16 tcgen05 kernel
 (``PassthroughPlan``): operands rounded to bf16, softmax and accumulation in
 f32.  There is no CPU fallback.
+
+``ForwardConfig.p_mode`` (extension) selects the softmax-weight semantics:
+``"normalized"`` (default) is the reference's arithmetic -- exact row max, f64
+row sum, P = e4m3(448 * p) of the normalised weights (attention.py:133-145) --
+in a three-pass kernel; ``"onepass"`` is the fast path of the batched API
+(unnormalised weights re-quantised per key block).  Plans are
+cached per (shape, window, format, mode, device, stream, thread).  Head dims
+other than 64 / 128 (the tcgen05 operand widths) are zero-padded to the next
+one: zero columns change no tile or channel amax, no logit and no kept output
+column, so codes and scales of the real columns are unchanged.
 """
 
 from __future__ import annotations
 
 import math
+import threading
 from dataclasses import dataclass
 
 import numpy as np
@@ -68,10 +79,13 @@ class ForwardConfig:
     softmax_scale: float | None = None
     passthrough: bool = False
     tau: float = 8.0
+    p_mode: str = "normalized"
 
     def __post_init__(self) -> None:
         if self.softmax_scale is not None and not self.softmax_scale > 0:
             raise ValueError("softmax_scale must be > 0")
+        if self.p_mode not in ("normalized", "onepass"):
+            raise ValueError(f"p_mode must be 'normalized' or 'onepass', got {self.p_mode!r}")
 
 
 def _is_torch(x) -> bool:
@@ -90,33 +104,67 @@ def _resolve_scale(scale, d: int) -> np.float32:
     return np.float32(scale)
 
 
+_PLAN_CACHE: dict = {}
+_PLAN_LOCK = threading.Lock()
+MAX_HEAD_DIM = 128
+
+
+def _padded_dim(d: int) -> int:
+    """Operand width of the tcgen05 kernels for head dim d (64 or 128)."""
+    if d > MAX_HEAD_DIM:
+        raise NotImplementedError(f"head dim {d} > {MAX_HEAD_DIM} is not supported by the sm_100a kernels")
+    return 64 if d <= 64 else 128
+
+
+def _cached_plan(kind: str, tmap: TileMap, config: ForwardConfig, dp: int, device):
+    import torch
+
+    from .ops import FpsaPlan, PassthroughPlan
+
+    stream = torch.cuda.current_stream(device).cuda_stream
+    key = (kind, tmap.grid.dims, tmap.scheme.dims, config.window.dims, dp, config.fmt.name, config.p_mode,
+           float(config.tau), str(device), stream, threading.get_ident())
+    with _PLAN_LOCK:
+        plan = _PLAN_CACHE.get(key)
+        if plan is None:
+            if kind == "passthrough":
+                plan = PassthroughPlan(tmap.grid.dims, tmap.scheme.dims, config.window, 1, dp, device=device)
+            else:
+                plan = FpsaPlan(tmap.grid.dims, tmap.scheme.dims, config.window, 1, dp, config.fmt, device=device,
+                                tau=config.tau, p_mode=config.p_mode)
+            _PLAN_CACHE[key] = plan
+    return plan
+
+
 def fp8_sparse_forward(inputs: AttentionInputs, config: ForwardConfig):
     """Joint tile-wise FP8 quantisation with sliding-tile sparse attention (attention.py:179-208)."""
     import torch
 
-    from .ops import FpsaPlan
-
     tmap = inputs.tile_map
-    scale = _resolve_scale(config.softmax_scale, inputs.d_model)
+    d = inputs.d_model
+    scale = _resolve_scale(config.softmax_scale, d)  # of the real head dim, before any padding
+    dp = _padded_dim(d)
     host = not _is_torch(inputs.q)
 
     def dev(x):
         t = torch.from_numpy(x) if host else x
         t = t.cuda()
-        return t if t.dtype in (torch.float32, torch.bfloat16) else t.float()
+        t = t if t.dtype in (torch.float32, torch.bfloat16) else t.float()
+        if dp != d:
+            t = torch.nn.functional.pad(t, (0, dp - d))
+        return t
 
     q, k, v = dev(inputs.q), dev(inputs.k), dev(inputs.v)
-    out = torch.empty((tmap.grid.tokens, inputs.d_model), dtype=torch.float32, device=q.device)
+    out = torch.empty((tmap.grid.tokens, dp), dtype=torch.float32, device=q.device)
     if config.passthrough:
-        from .ops import PassthroughPlan
-
-        pplan = PassthroughPlan(tmap.grid.dims, tmap.scheme.dims, config.window, 1, inputs.d_model, device=q.device)
+        pplan = _cached_plan("passthrough", tmap, config, dp, q.device)
         pplan.gather(q, k, v, layout="ld", tile_order=True)
         pplan.attention(out, layout="ld", tile_order=True, softmax_scale=float(scale))
-        return out.cpu().numpy() if host else out
-    plan = FpsaPlan(tmap.grid.dims, tmap.scheme.dims, config.window, 1, inputs.d_model, config.fmt,
-                    device=q.device, tau=config.tau)
-    plan.quantize(q, k, v, layout="ld", tile_order=True)
-    plan.attention(out, layout="ld", tile_order=True, softmax_scale=float(scale))
-    plan.check_finite()
+    else:
+        plan = _cached_plan("fp8", tmap, config, dp, q.device)
+        plan.quantize(q, k, v, layout="ld", tile_order=True)
+        plan.attention(out, layout="ld", tile_order=True, softmax_scale=float(scale))
+        plan.check_finite()
+    if dp != d:
+        out = out[:, :d].contiguous()
     return out.cpu().numpy() if host else out

@@ -40,7 +40,17 @@
 // writing their P~ over the first 32 columns of the step's S buffer, so one
 // warp's TMEM traffic and hand-off overlap the other's exp work.  Warp 8 is
 // the TMA producer (and TMEM allocator), warp 9 the MMA issuer, warp 10
-// prefetches per-item metadata, warp 11 is idle.
+// claims work items (a global atomic counter: CTAs take the next item of the
+// longest-first list when they are ready for it, so no CTA is left with a
+// longer share) and prefetches their metadata, warp 11 is idle.  The claimed
+// (head, tile, block) triples reach the other roles through a 4-deep ring in
+// shared memory.
+//
+// Normalised-P mode (template NORM, the reference's exact semantics,
+// attention.py:133-145): three passes over the keys of an item -- exact row
+// max m, row sum l = sum exp(s - m) in f64, then P~ = e4m3(448 * exp(s - m) / f32(l))
+// with s = S * f32(k_scale * f32(q_scale * softmax_scale)) and exp correctly
+// rounded to f32 -- and out = O * f32(v_scale / 448), no division by l.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -69,6 +79,14 @@ namespace {
 
 using namespace sm100;
 
+#ifndef FPSA_MBAR_SUSPEND_NS
+#define FPSA_MBAR_SUSPEND_NS 100000
+#endif
+// every wait of this kernel carries the suspend-time hint (sm100.cuh mbar_try_wait)
+__device__ __forceinline__ void attn_wait(uint64_t* bar, uint32_t parity) {
+  mbar_wait<FPSA_MBAR_SUSPEND_NS>(bar, parity);
+}
+
 constexpr int kParts = 2;                       // softmax warps sharing one TMEM lane quarter (row)
 [[maybe_unused]] constexpr int kPartCols = 128 / kParts;  // S columns per softmax thread in the FPSA_PINGPONG=0 variant
 constexpr int kSoftmaxWarps = 4 * kParts;
@@ -84,7 +102,9 @@ constexpr int kBlk = 128;      // rows per query block = keys per key block
 constexpr float kLog2_448 = 8.807354922057604f;
 constexpr int kRedoHeader = 4;  // int32 words before the redo items in the workspace
 constexpr int kFacCap = 512;    // key-tile factors per item kept in shared memory (more: read from L2)
-constexpr int kHelperWarp = kSoftmaxWarps + 2;  // producer-warpgroup warp that prefetches item metadata
+constexpr int kHelperWarp = kSoftmaxWarps + 2;  // producer-warpgroup warp that claims items, prefetches metadata
+constexpr int kItemRing = 4;                    // claimed items in flight between the helper and the other roles
+constexpr int kItemReaders = 2 + kSoftmaxWarps;  // TMA warp, MMA warp, softmax warps
 // Ping-pong softmax: the warps w and w+4 of an SMSP (same TMEM lane quarter) take alternate key blocks,
 // each computing whole 128-key rows.  FPSA_PINGPONG=0 builds the earlier variant in which the two warps
 // take the two 64-column halves of every block (slower: 12.65 vs 12.1 ms at C2).
@@ -103,11 +123,13 @@ struct AttnParams {
   const int32_t* items;  // (head, tile, query block) triples
   int32_t n_items;
   int32_t* redo;         // [0]: count, [kRedoHeader..]: triples of items to recompute exactly
+  int32_t* claim;        // work-item counter of this launch (zeroed before the launch)
   int32_t exact;         // 1: this launch recomputes the redo list with the exact row max
   int32_t M, tv, pitch, nb;  // nb: 128-key blocks per tile
   int32_t n_tail;     // valid keys of the last key block of a tile: tv - 128 (nb-1); the
                       // QK MMA still runs N = 128 over zero K rows, whose S = 0 the softmax drops
   float softmax_log2;  // f32(softmax_scale * log2 e)
+  float softmax_scale;  // f32 softmax scale (normalised-P factors)
   float tau;
   void* out;
   int64_t out_ts, out_hs;
@@ -155,7 +177,36 @@ __device__ __forceinline__ uint64_t desc_mnmajor(uint32_t addr) {
 //   [4] softmax: S load (tcgen05.ld + wait) cycles   [7] MMA: cycles waiting for K/V
 #endif
 
-template <int D, int FMT, int OUT>
+// Correctly rounded f32 exp (through f64): the normalised-P mode's exp.  Not inlined: it is called per
+// element of a fully unrolled row and would otherwise multiply the code size.
+__device__ __noinline__ float exp_f32_cr(float x) { return __double2float_rn(exp((double)x)); }
+
+// Normalised-P pass 2: f64 sum of exp(S * c - m) over the first ncol of NC S columns.
+template <int NC>
+__device__ __forceinline__ double expsum_norm(const uint32_t* s, int ncol, float c, float m) {
+  double acc = 0.0;
+#pragma unroll
+  for (int i = 0; i < NC; ++i)
+    if (i < ncol) acc += (double)exp_f32_cr(__fsub_rn(__fmul_rn(__uint_as_float(s[i]), c), m));
+  return acc;
+}
+// Normalised-P pass 3: P~ = e4m3(448 * (exp(S * c - m) / l)), packed 4 per word; columns >= ncol are 0.
+template <int NC>
+__device__ __forceinline__ void compute_p_norm(const uint32_t* s, int ncol, float c, float m, float l,
+                                               uint32_t* w) {
+#pragma unroll
+  for (int i = 0; i < NC; i += 4) {
+    float pv[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float e = exp_f32_cr(__fsub_rn(__fmul_rn(__uint_as_float(s[i + k]), c), m));
+      pv[k] = i + k < ncol ? __fmul_rn(__fdiv_rn(e, l), 448.0f) : 0.0f;
+    }
+    w[i / 4] = e4m3x4(f2{pv[0], pv[1]}, f2{pv[2], pv[3]});
+  }
+}
+
+template <int D, int FMT, int OUT, bool NORM>
 __global__ void __launch_bounds__(kThreads, 1)
     fpsa_attn_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                      const __grid_constant__ CUtensorMap tm_v, const AttnParams p) {
@@ -174,14 +225,35 @@ __global__ void __launch_bounds__(kThreads, 1)
   __shared__ int32_t s_hdr[2][4];      // kt0, n_kt, unused, unused
   __shared__ uint64_t bar_meta_full[2], bar_meta_empty[2];
   __shared__ uint32_t s_ovf[2];      // per item parity: some row overflowed
+  // claimed work items (helper warp -> TMA, MMA, softmax): head (-1: no more items), tile, query block
+  __shared__ int32_t s_item[kItemRing][4];
+  __shared__ uint64_t bar_item_full[kItemRing], bar_item_empty[kItemRing];
+  __shared__ double s_xchg_d[NORM ? kParts : 1][kBlk];  // normalised-P row-sum exchange
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // re-read from the parameter bank at each use (a long-lived pointer is spilled across the role switch)
   auto item_at = [&p](int32_t i) { return (p.exact ? p.redo + kRedoHeader : p.items)[i]; };
   const int32_t count = p.exact ? *reinterpret_cast<volatile int32_t*>(p.redo) : p.n_items;
-  if ((int32_t)blockIdx.x >= count) return;
+  if ((int32_t)blockIdx.x >= count) return;  // at most `count` CTAs can claim an item
+  constexpr int32_t kNormPasses = 3;
+  const int32_t passes = NORM ? kNormPasses : (p.exact ? 2 : 1);  // key sweeps per item; the last one runs PV
+  // next claimed item of this role's `iter`-th loop trip; false when the list is exhausted
+  auto next_item = [&](int32_t iter, int32_t& h, int32_t& u, int32_t& qb) {
+    const int r = iter % kItemRing;
+    attn_wait(&bar_item_full[r], (iter / kItemRing) & 1);
+    h = s_item[r][0];
+    u = s_item[r][1];
+    qb = s_item[r][2];
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&bar_item_empty[r]);
+    return h >= 0;
+  };
 
   if (threadIdx.x == 0) {
+    for (int i = 0; i < kItemRing; ++i) {
+      mbar_init(&bar_item_full[i], 1);
+      mbar_init(&bar_item_empty[i], kItemReaders);
+    }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&bar_q[i], 1);
       mbar_init(&bar_qfree[i], 1);
@@ -230,26 +302,25 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     __syncwarp();
     uint32_t g = 0;  // K/V block counter over all items of this CTA
-    int32_t iter = 0;
-    for (int32_t it = blockIdx.x; it < count; it += gridDim.x, ++iter) {
-      const int32_t h = item_at(3 * it), u = item_at(3 * it + 1), qb = item_at(3 * it + 2);
+    int32_t h, u, qb;
+    for (int32_t iter = 0; next_item(iter, h, u, qb); ++iter) {
       const int32_t kt0 = __ldg(p.offs + u), n_kt = __ldg(p.offs + u + 1) - kt0;
-      const int32_t n_kv = n_kt * p.nb, steps = p.exact ? 2 * n_kv : n_kv;
+      const int32_t n_kv = n_kt * p.nb, steps = passes * n_kv;
       const int qbuf = iter & 1;
-      if (iter >= 2) mbar_wait(&bar_qfree[qbuf], ((iter >> 1) - 1) & 1);
+      if (iter >= 2) attn_wait(&bar_qfree[qbuf], ((iter >> 1) - 1) & 1);
       mbar_arrive_expect_tx_w(&bar_q[qbuf], S::kTile);
       tma_load_2d_w(smem + S::kQ + qbuf * S::kTile, &tm_q, 0, (h * p.M + u) * p.pitch + qb * kBlk, &bar_q[qbuf]);
       int32_t kt = 0, b = 0;
       int32_t krow = (h * p.M + __ldg(p.ids + kt0)) * p.pitch;
       for (int32_t s = 0; s < steps; ++s, ++g) {
         const uint32_t st = g % kStages;
-        if (g >= (uint32_t)kStages) mbar_wait(&bar_kv_empty[st], ((g / kStages) - 1) & 1);
+        if (g >= (uint32_t)kStages) attn_wait(&bar_kv_empty[st], ((g / kStages) - 1) & 1);
         mbar_arrive_expect_tx_w(&bar_kv_full[st], 2 * S::kTile);
         tma_load_2d_w(smem + S::kK + st * S::kTile, &tm_k, 0, krow + b * kBlk, &bar_kv_full[st]);
         tma_load_2d_w(smem + S::kV + st * S::kTile, &tm_v, 0, krow + b * kBlk, &bar_kv_full[st]);
         if (++b == p.nb) {
           b = 0;
-          if (++kt == n_kt) kt = 0;  // exact mode streams the keys twice
+          if (++kt == n_kt) kt = 0;  // exact / normalised modes stream the keys 2 / 3 times
           krow = (h * p.M + __ldg(p.ids + kt0 + kt)) * p.pitch;
         }
       }
@@ -271,23 +342,22 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint64_t dvt0 = desc_mnmajor_ones<D>(sv0, smem_u32(smem + S::kOnesTail) - sv0);
     constexpr uint64_t kVStageStep = kTileU - (kTileU << 16);
     uint32_t g = 0;
-    int32_t iter = 0;
     uint32_t qk_st = 0, qk_ph = 0;  // K/V stage + full-barrier phase of the next QK
     uint32_t pv_st = 0;             // K/V stage of the next PV
-    for (int32_t it = blockIdx.x; it < count; it += gridDim.x, ++iter) {
-      const int32_t u = item_at(3 * it + 1);
+    int32_t h, u, qb;
+    for (int32_t iter = 0; next_item(iter, h, u, qb); ++iter) {
       const int32_t n_kt = __ldg(p.offs + u + 1) - __ldg(p.offs + u);
-      const int32_t n_kv = n_kt * p.nb, steps = p.exact ? 2 * n_kv : n_kv;
-      const int32_t pv0 = p.exact ? n_kv : 0;  // first step with a PV
+      const int32_t n_kv = n_kt * p.nb, steps = passes * n_kv;
+      const int32_t pv0 = (passes - 1) * n_kv;  // first step with a PV
       const int qbuf = iter & 1;
       const uint64_t dq = dq0 + (uint64_t)qbuf * kTileU;
-      mbar_wait(&bar_q[qbuf], (iter >> 1) & 1);
+      attn_wait(&bar_q[qbuf], (iter >> 1) & 1);
       tc_fence_after();
       int32_t b2 = 0;  // in-tile block of the next QK
       int32_t bp = 0;  // in-tile block of the current step (both passes cycle through whole tiles)
       // S(step gg) = Q K^T into TMEM buffer gg % 2
       auto issue_qk = [&](uint32_t gg) {
-        mbar_wait(&bar_kv_full[qk_st], qk_ph);
+        attn_wait(&bar_kv_full[qk_st], qk_ph);
         tc_fence_after();
         const uint64_t dk = dk0 + qk_st * kTileU;
         // N = 128 for every block: a tile's last block reads zero K rows past tv (S = 0 there,
@@ -321,7 +391,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const bool do_qk = s + 2 < steps;
           uint64_t dk = 0;
           if (do_qk) {
-            mbar_wait(&bar_kv_full[qk_st], qk_ph);
+            attn_wait(&bar_kv_full[qk_st], qk_ph);
             dk = dk0 + qk_st * kTileU;
           }
           constexpr uint64_t kVk = 32 * D / 16;
@@ -336,9 +406,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             dqq[k] = dq + 2 * k;
             ta[k] = ts + 8 * k;
           }
-          if (s == pv0 && iter > 0) mbar_wait(&bar_ofree, (iter - 1) & 1);  // the previous item's epilogue read O
+          if (s == pv0 && iter > 0) attn_wait(&bar_ofree, (iter - 1) & 1);  // the previous item's epilogue read O
           FPSA_TL(9, 0, gs);
-          mbar_wait(&bar_p_ready[gs & 1], (gs >> 1) & 1);
+          attn_wait(&bar_p_ready[gs & 1], (gs >> 1) & 1);
           FPSA_TL(9, 1, gs);
           tc_fence_after();
 #if FPSA_MMA_ONE_ELECT
@@ -382,7 +452,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const long long tp0 = clock64();
   #endif
           FPSA_TL(9, 0, gs);
-          mbar_wait(&bar_p_ready[gs & 1], (gs >> 1) & 1);
+          attn_wait(&bar_p_ready[gs & 1], (gs >> 1) & 1);
           FPSA_TL(9, 1, gs);
   #ifdef FPSA_TRACE
           if (lane == 0) atomicAdd(&g_trace[3], (unsigned long long)(clock64() - tp0));
@@ -392,7 +462,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             // [O|l] += P~ [V|1]: P~ of the keys of row part c sits in the first columns of that part's
             // S columns; the B descriptor's leading byte offset points from V at the ones atom
             if (s == pv0 && iter > 0) {
-              mbar_wait(&bar_ofree, (iter - 1) & 1);  // the previous item's epilogue has read O
+              attn_wait(&bar_ofree, (iter - 1) & 1);  // the previous item's epilogue has read O
               tc_fence_after();
             }
             const uint64_t dv = (bp == p.nb - 1 ? dvt0 : dv0) + pv_st * kVStageStep;
@@ -428,18 +498,40 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == kHelperWarp) {
     // ------------------------------------------------------------ metadata prefetch (one item ahead)
     const float sl = p.softmax_log2;
-    int32_t iter = 0;
-    for (int32_t it = blockIdx.x; it < count; it += gridDim.x, ++iter) {
+    for (int32_t iter = 0;; ++iter) {
+      // claim the next item and post it to the ring (the claim's latency is hidden: the ring runs ahead)
+      const int r = iter % kItemRing;
+      if (iter >= kItemRing) attn_wait(&bar_item_empty[r], ((iter / kItemRing) - 1) & 1);
+      int32_t idx = 0;
+      if (lane == 0) idx = atomicAdd(p.claim, 1);
+      idx = __shfl_sync(0xffffffffu, idx, 0);
+      const bool more = idx < count;
+      const int32_t h = more ? item_at(3 * idx) : -1;
+      const int32_t u = more ? item_at(3 * idx + 1) : 0;
+      if (lane == 0) {
+        s_item[r][0] = h;
+        s_item[r][1] = u;
+        s_item[r][2] = more ? item_at(3 * idx + 2) : 0;
+        mbar_arrive(&bar_item_full[r]);  // release: the item words above are visible to waiters
+      }
+      if (!more) break;
       const int slot = iter & 1;
-      if (iter >= 2) mbar_wait(&bar_meta_empty[slot], ((iter >> 1) - 1) & 1);
-      const int32_t h = item_at(3 * it), u = item_at(3 * it + 1);
+      if (iter >= 2) attn_wait(&bar_meta_empty[slot], ((iter >> 1) - 1) & 1);
       const int32_t kt0 = __ldg(p.offs + u), n_kt = __ldg(p.offs + u + 1) - kt0;
       const float qs = (float)__ldg(p.q_scales + h * p.M + u);
       const double* ks = p.k_scales + (int64_t)h * p.M;
-      // c(kt) = f32(f32(sq) * f32(sk)) * f32(scale log2 e), the oracle's factor order
-      for (int32_t i = lane; i < min(n_kt, kFacCap); i += 32)
-        s_fac[slot][i] = (qs * (float)__ldg(ks + __ldg(p.ids + kt0 + i))) * sl;
-      for (int i = lane; i < D; i += 32) s_vsc[slot][i] = (float)__ldg(p.v_scales + (int64_t)h * D + i);
+      // c(kt) = f32(f32(sq) * f32(sk)) * f32(scale log2 e), the oracle's factor order; normalised-P mode:
+      // the reference's f32(f32(sk) * f32(f32(sq) * scale)) (attention.py:122)
+      const float qsc = qs * p.softmax_scale;
+      for (int32_t i = lane; i < min(n_kt, kFacCap); i += 32) {
+        const float kf = (float)__ldg(ks + __ldg(p.ids + kt0 + i));
+        s_fac[slot][i] = NORM ? kf * qsc : (qs * kf) * sl;
+      }
+      // v factors: f32(sv), or f32(sv / 448) in normalised-P mode (attention.py:206-207)
+      for (int i = lane; i < D; i += 32) {
+        const double sv = __ldg(p.v_scales + (int64_t)h * D + i);
+        s_vsc[slot][i] = NORM ? (float)(sv * (1.0 / 448.0)) : (float)sv;
+      }
       if (lane == 0) {
         s_hdr[slot][0] = kt0;
         s_hdr[slot][1] = n_kt;
@@ -466,22 +558,22 @@ __global__ void __launch_bounds__(kThreads, 1)
       return r;
     };
     uint32_t g = 0;
-    int32_t iter = 0;
 #ifdef FPSA_TRACE
     long long w_s = 0, w_c = 0, t_loop = 0;
     int64_t n_steps = 0;
 #endif
-    for (int32_t it = blockIdx.x; it < count; it += gridDim.x, ++iter) {
-      const int32_t h = item_at(3 * it), u = item_at(3 * it + 1), qb = item_at(3 * it + 2);
+    int32_t h, u, qb;
+    for (int32_t iter = 0; next_item(iter, h, u, qb); ++iter) {
       const int slot = iter & 1;
-      mbar_wait(&bar_meta_full[slot], (iter >> 1) & 1);
+      attn_wait(&bar_meta_full[slot], (iter >> 1) & 1);
       const int32_t kt0 = s_hdr[slot][0], n_kt = s_hdr[slot][1];
       const int32_t n_kv = n_kt * p.nb;
       const float* fac = s_fac[slot];
       auto factor_at = [&](int32_t kt) {
         if (kt < kFacCap) return fac[kt];
         const float qs = (float)__ldg(p.q_scales + h * p.M + u);  // windows beyond kFacCap tiles: from L2
-        return (qs * (float)__ldg(p.k_scales + (int64_t)h * p.M + __ldg(p.ids + kt0 + kt))) * sl;
+        const float kf = (float)__ldg(p.k_scales + (int64_t)h * p.M + __ldg(p.ids + kt0 + kt));
+        return NORM ? kf * (qs * p.softmax_scale) : (qs * kf) * sl;
       };
       float m_ref = 0.0f;
       uint32_t sat = 0u;
@@ -495,14 +587,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t s_row = tm_s((uint32_t)part) + lane_off;
         auto owned = [&](uint32_t gg) { return (int)(gg & 1u) == part; };
         auto ncol_blk = [&](int32_t bb) { return bb == p.nb - 1 ? p.n_tail : kBlk; };
-        if (p.exact) {
-          // pass 0 (exact mode only): running max over this warp's key blocks, then over the pair
+        float l_norm = 1.0f;  // normalised-P mode: f32 of the f64 row sum
+        if (NORM || p.exact) {
+          // pass 0 (exact and normalised modes): running max over this warp's key blocks, then over the pair
           float m_acc = -INFINITY;
           int32_t kt = 0, b = 0;
           for (int32_t j = 0; j < n_kv; ++j, ++g) {
             if (owned(g)) {
               const float c = factor_at(kt);
-              mbar_wait(&bar_s_full[g & 1], (g >> 1) & 1);
+              attn_wait(&bar_s_full[g & 1], (g >> 1) & 1);
               tc_fence_after();
               m_acc = fmaxf(m_acc, block_max<kBlk>(s_row, ncol_blk(b), false) * c);
               tc_fence_before();
@@ -517,11 +610,47 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
           m_ref = row_max(m_acc);
+          if constexpr (NORM) {
+            // pass 1: l = sum exp(s - m) in f64 over this warp's blocks, then over the pair
+            double l_acc = 0.0;
+            int32_t kt = 0, b = 0;
+            for (int32_t j = 0; j < n_kv; ++j, ++g) {
+              if (owned(g)) {
+                const float c = factor_at(kt);
+                const int n = ncol_blk(b);
+                attn_wait(&bar_s_full[g & 1], (g >> 1) & 1);
+                tc_fence_after();
+#pragma unroll
+                for (int hb = 0; hb < 2; ++hb) {
+                  uint32_t sreg[64];
+                  load_s_all<64>(s_row + 64 * hb, sreg);
+                  tmem_wait_ld();
+                  l_acc += expsum_norm<64>(sreg, n - 64 * hb, c, m_ref);
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&bar_p_ready[g & 1]);  // S consumed
+              }
+              if (b == p.nb - 1) {
+                b = 0;
+                ++kt;
+              } else {
+                ++b;
+              }
+            }
+            s_xchg_d[part][row] = l_acc;
+            row_sync();
+            double l_row = s_xchg_d[0][row];
+#pragma unroll
+            for (int i = 1; i < kParts; ++i) l_row += s_xchg_d[i][row];
+            row_sync();
+            l_norm = (float)l_row;  // f32(denominator), attention.py:137-138
+          }
         } else {
           // reference max = row max of the item's first key block, taken by the warp that owns it
           float m0 = -INFINITY;
           if (owned(g)) {
-            mbar_wait(&bar_s_full[g & 1], (g >> 1) & 1);
+            attn_wait(&bar_s_full[g & 1], (g >> 1) & 1);
             tc_fence_after();
             m0 = block_max<kBlk>(s_row, ncol_blk(0), false) * factor_at(0);
           }
@@ -535,7 +664,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const long long ts0 = clock64();
 #endif
             FPSA_TL(warp, 0, g);
-            mbar_wait(&bar_s_full[g & 1], (g >> 1) & 1);
+            attn_wait(&bar_s_full[g & 1], (g >> 1) & 1);
             FPSA_TL(warp, 1, g);
 #ifdef FPSA_TRACE
             w_s += clock64() - ts0;
@@ -546,17 +675,27 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int n = ncol_blk(b);
             const float bias = kLog2_448 - m_ref - tau;
             uint32_t w[kBlk / 4];
-            {
-              uint32_t sreg[64];
-              load_s_all<64>(s_row, sreg);
-              tmem_wait_ld();
-              sat |= compute_p_regs<64>(sreg, min(n, 64), c, bias, w);
-            }
-            {
-              uint32_t sreg[64];
-              load_s_all<64>(s_row + 64, sreg);
-              tmem_wait_ld();
-              sat |= compute_p_regs<64>(sreg, max(n - 64, 0), c, bias, w + 16);
+            if constexpr (NORM) {
+#pragma unroll
+              for (int hb = 0; hb < 2; ++hb) {
+                uint32_t sreg[64];
+                load_s_all<64>(s_row + 64 * hb, sreg);
+                tmem_wait_ld();
+                compute_p_norm<64>(sreg, n - 64 * hb, c, m_ref, l_norm, w + 16 * hb);
+              }
+            } else {
+              {
+                uint32_t sreg[64];
+                load_s_all<64>(s_row, sreg);
+                tmem_wait_ld();
+                sat |= compute_p_regs<64>(sreg, min(n, 64), c, bias, w);
+              }
+              {
+                uint32_t sreg[64];
+                load_s_all<64>(s_row + 64, sreg);
+                tmem_wait_ld();
+                sat |= compute_p_regs<64>(sreg, max(n - 64, 0), c, bias, w + 16);
+              }
             }
 #ifdef FPSA_TRACE
             w_c += clock64() - tc0;
@@ -586,7 +725,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int ncol = (tail ? p.n_tail : kBlk) - kPartCols * part;
           const int ncol_h = min(max(ncol, 0), kPartCols);
           const float c = factor_at(kt);
-          mbar_wait(&bar_s_full[g & 1], (g >> 1) & 1);
+          attn_wait(&bar_s_full[g & 1], (g >> 1) & 1);
           tc_fence_after();
           m_acc = fmaxf(m_acc, block_max<kPartCols>(tm_s(g) + lane_off + part * kPartCols, ncol_h, false) * c);
           tc_fence_before();
@@ -610,7 +749,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         auto ncol_of = [&](int32_t bb) {
           return min(max((bb == p.nb - 1 ? p.n_tail : kBlk) - kPartCols * part, 0), kPartCols);
         };
-        mbar_wait(&bar_s_full[g & 1], (g >> 1) & 1);
+        attn_wait(&bar_s_full[g & 1], (g >> 1) & 1);
         tc_fence_after();
         if (!p.exact) {
           // reference max = row max of the first key block (a tail block only when nb == 1)
@@ -645,7 +784,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const long long ts0 = clock64();
 #endif
             FPSA_TL(warp, 0, g + 1);
-            mbar_wait(&bar_s_full[(g + 1) & 1], ((g + 1) >> 1) & 1);
+            attn_wait(&bar_s_full[(g + 1) & 1], ((g + 1) >> 1) & 1);
             FPSA_TL(warp, 1, g + 1);
 #ifdef FPSA_TRACE
             w_s += clock64() - ts0;
@@ -666,10 +805,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       t_loop += clock64() - tl0;
 #endif
       // ---------------------------------------------------------- epilogue
-      mbar_wait(&bar_o, iter & 1);
+      attn_wait(&bar_o, iter & 1);
       tc_fence_after();
-      float inv_l;
-      {
+      float inv_l = 1.0f;  // normalised-P mode: P~ is already normalised (out = O * v_fac)
+      if constexpr (!NORM) {
         uint32_t lw[16];
         tmem_ld16(tm_o + lane_off + D, lw);  // row sum of P~ (the ones columns, all equal)
         tmem_wait_ld();
@@ -723,7 +862,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&bar_ofree);
       mbar_arrive(&bar_meta_empty[slot]);  // this item's metadata slot may be refilled
-      if (!p.exact) {
+      if (!NORM && !p.exact) {
         // items with a possibly saturated P~ are recomputed exactly by the redo launch
         if (__any_sync(0xffffffffu, sat != 0u) && lane == 0) atomicOr(&s_ovf[iter & 1], 1u);
         named_bar_sync(5, kSoftmaxWarps * 32);
@@ -781,35 +920,25 @@ int make_code_map(CUtensorMap* m, const uint8_t* base, int64_t rows, int32_t d, 
   return FPSA_OK;
 }
 
-int g_num_sms = 0;
-int num_sms() {
-  if (!g_num_sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-    if (g_num_sms <= 0) g_num_sms = 148;
-  }
-  return g_num_sms;
-}
-
-// Main persistent launch, then the exact-mode launch over the redo list
-// (its CTAs exit at once when the list is empty).
-template <int D, int FMT, int OUT>
+// Main persistent launch, then the exact-mode launch over the redo list (its CTAs exit at once when the list
+// is empty).  Normalised-P mode: one three-pass launch, nothing to redo.  Workspace words 0..2 (redo count,
+// the two launches' claim counters) are zeroed first.
+template <int D, int FMT, int OUT, bool NORM>
 int launch(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, AttnParams p, cudaStream_t st) {
-  auto kern = fpsa_attn_kernel<D, FMT, OUT>;
+  auto kern = fpsa_attn_kernel<D, FMT, OUT, NORM>;
   constexpr int smem = Smem<D>::kBytes + 1024;
-  static bool configured = false;
-  if (!configured) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
-      return fail(FPSA_ECUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(cudaGetLastError()));
-    configured = true;
-  }
-  if (cudaMemsetAsync(p.redo, 0, sizeof(int32_t), st) != cudaSuccess)
-    return fail(FPSA_ECUDA, std::string("fpsa_attn_fwd redo reset: ") + cudaGetErrorString(cudaGetLastError()));
+  if (int s = ensure_smem_attr(reinterpret_cast<const void*>(kern), smem, "fpsa_attn_fwd")) return s;
+  if (cudaMemsetAsync(p.redo, 0, kRedoHeader * sizeof(int32_t), st) != cudaSuccess)
+    return fail(FPSA_ECUDA, std::string("fpsa_attn_fwd workspace reset: ") + cudaGetErrorString(cudaGetLastError()));
+  const int grid = std::min(p.n_items, device_sm_count());
   p.exact = 0;
-  kern<<<std::min(p.n_items, num_sms()), kThreads, smem, st>>>(tq, tk, tv, p);
-  p.exact = 1;
-  kern<<<std::min(p.n_items, num_sms()), kThreads, smem, st>>>(tq, tk, tv, p);
+  p.claim = p.redo + 1;
+  kern<<<grid, kThreads, smem, st>>>(tq, tk, tv, p);
+  if constexpr (!NORM) {
+    p.exact = 1;
+    p.claim = p.redo + 2;
+    kern<<<grid, kThreads, smem, st>>>(tq, tk, tv, p);
+  }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(FPSA_ECUDA, std::string("fpsa_attn_fwd launch: ") + cudaGetErrorString(e));
   return FPSA_OK;
@@ -820,24 +949,18 @@ int launch(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, 
 
 using namespace fpsa;
 
-#ifdef FPSA_ATTN2
-extern "C" int fpsa_attn2_fwd(const uint8_t* q_codes, const uint8_t* k_codes, const uint8_t* v_codes,
-                              const double* q_scales, const double* k_scales, const double* v_scales, int32_t heads,
-                              fpsa_dims3 grid, fpsa_dims3 tile, int32_t d, int32_t tile_pitch, const int32_t* offs,
-                              const int32_t* ids, const int32_t* items, int32_t n_items, float softmax_scale,
-                              int fmt, float tau_log2, void* out, int out_dtype, int64_t out_token_stride,
-                              int64_t out_head_stride, int out_order, void* workspace, int64_t workspace_bytes,
-                              void* stream);
-#endif
-
 extern "C" int fpsa_attn_fwd(const uint8_t* q_codes, const uint8_t* k_codes, const uint8_t* v_codes,
                              const double* q_scales, const double* k_scales, const double* v_scales, int32_t heads,
                              fpsa_dims3 grid, fpsa_dims3 tile, int32_t d, int32_t tile_pitch, const int32_t* offs,
                              const int32_t* ids, const int32_t* items, int32_t n_items, float softmax_scale, int fmt,
-                             float tau_log2, void* out, int out_dtype, int64_t out_token_stride,
+                             float tau_log2, int p_mode, void* out, int out_dtype, int64_t out_token_stride,
                              int64_t out_head_stride, int out_order, void* workspace, int64_t workspace_bytes,
                              void* stream) {
   clear_error();
+  if (p_mode != FPSA_P_ONEPASS && p_mode != FPSA_P_NORMALIZED) return fail(FPSA_EINVAL, "p_mode must be 0 or 1");
+  const bool norm = p_mode == FPSA_P_NORMALIZED;
+  if (norm && out_dtype != FPSA_F32)
+    return fail(FPSA_EUNSUPPORTED, "the normalised-P mode writes f32 output (the reference's dtype)");
   fpsa_dims3 td;
   if (int s = fpsa_tile_grid(grid, tile, &td)) return s;
   if (!q_codes || !k_codes || !v_codes || !q_scales || !k_scales || !v_scales || !offs || !ids || !items || !out)
@@ -854,12 +977,6 @@ extern "C" int fpsa_attn_fwd(const uint8_t* q_codes, const uint8_t* k_codes, con
   fpsa_attn_workspace_bytes(n_items, &need);
   if (!workspace || workspace_bytes < need)
     return fail(FPSA_ECAPACITY, "attention workspace must hold " + std::to_string(need) + " bytes");
-#ifdef FPSA_ATTN2
-  if (d == 128 && tv > kBlk && getenv("FPSA_ATTN_1CTA") == nullptr)
-    return fpsa_attn2_fwd(q_codes, k_codes, v_codes, q_scales, k_scales, v_scales, heads, grid, tile, d, tile_pitch,
-                          offs, ids, items, n_items, softmax_scale, fmt, tau_log2, out, out_dtype, out_token_stride,
-                          out_head_stride, out_order, workspace, workspace_bytes, stream);
-#endif
   const int32_t M = td.t * td.h * td.w;
   const int64_t rows = (int64_t)heads * M * tile_pitch;
   CUtensorMap tq, tk, tvm;
@@ -881,6 +998,7 @@ extern "C" int fpsa_attn_fwd(const uint8_t* q_codes, const uint8_t* k_codes, con
   p.nb = (tv + kBlk - 1) / kBlk;
   p.n_tail = tv - kBlk * (p.nb - 1);  // valid keys of a tile's last 128-key block
   p.softmax_log2 = softmax_scale * 1.4426950408889634f;
+  p.softmax_scale = softmax_scale;
   p.tau = tau_log2;
   p.out = out;
   p.out_ts = out_token_stride;
@@ -894,7 +1012,15 @@ extern "C" int fpsa_attn_fwd(const uint8_t* q_codes, const uint8_t* k_codes, con
   p.dh = td.h;
   p.dw = td.w;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-#define FPSA_LAUNCH(D_, F_, O_) return launch<D_, F_, O_>(tq, tk, tvm, p, st)
+#define FPSA_LAUNCH(D_, F_, O_) return launch<D_, F_, O_, false>(tq, tk, tvm, p, st)
+  if (norm) {  // f32 output only
+    if (d == 128) {
+      if (fmt == FPSA_E4M3) return launch<128, FPSA_E4M3, FPSA_F32, true>(tq, tk, tvm, p, st);
+      return launch<128, FPSA_E5M2, FPSA_F32, true>(tq, tk, tvm, p, st);
+    }
+    if (fmt == FPSA_E4M3) return launch<64, FPSA_E4M3, FPSA_F32, true>(tq, tk, tvm, p, st);
+    return launch<64, FPSA_E5M2, FPSA_F32, true>(tq, tk, tvm, p, st);
+  }
   if (d == 128) {
     if (fmt == FPSA_E4M3) {
       if (out_dtype == FPSA_F32) FPSA_LAUNCH(128, FPSA_E4M3, FPSA_F32); else FPSA_LAUNCH(128, FPSA_E4M3, FPSA_BF16);

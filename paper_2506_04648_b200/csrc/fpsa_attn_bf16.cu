@@ -494,30 +494,15 @@ int make_bf16_map(CUtensorMap* m, const void* base, int64_t rows, int32_t d) {
   return FPSA_OK;
 }
 
-int sm_count() {
-  static int n = 0;
-  if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
-  }
-  return n;
-}
 
 template <int D, int OUT>
 int launch(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, Params p, cudaStream_t st) {
   auto kern = attn_bf16_kernel<D, OUT>;
   constexpr int smem = Smem<D>::kBytes + 1024;
-  static bool configured = false;
-  if (!configured) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
-      return fail(FPSA_ECUDA, std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(cudaGetLastError()));
-    configured = true;
-  }
+  if (int s = ensure_smem_attr(reinterpret_cast<const void*>(kern), smem, "fpsa_attn_bf16_fwd")) return s;
   if (cudaMemsetAsync(p.redo, 0, sizeof(int32_t), st) != cudaSuccess)
     return fail(FPSA_ECUDA, std::string("fpsa_attn_bf16_fwd redo reset: ") + cudaGetErrorString(cudaGetLastError()));
-  const int grid = std::min(p.n_items, sm_count());
+  const int grid = std::min(p.n_items, device_sm_count());
   p.exact = 0;
   kern<<<grid, kThreads, smem, st>>>(tq, tk, tv, p);
   p.exact = 1;
@@ -551,7 +536,7 @@ extern "C" int fpsa_tile_gather_bf16(const void* x, int dtype, int64_t token_str
   const int64_t rows = (int64_t)heads * M * tile_pitch;
   if (rows >= (int64_t)1 << 31) return fail(FPSA_EUNSUPPORTED, "too many rows for one gather");
   const int32_t rows_per_block = 256 / (d / 8);
-  const int blocks = (int)std::min<int64_t>((rows + rows_per_block - 1) / rows_per_block, (int64_t)pt::sm_count() * 16);
+  const int blocks = (int)std::min<int64_t>((rows + rows_per_block - 1) / rows_per_block, (int64_t)device_sm_count() * 16);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int nat = in_order == FPSA_ORDER_NATURAL;
   auto* o = static_cast<__nv_bfloat16*>(out);

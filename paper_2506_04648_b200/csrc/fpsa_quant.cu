@@ -631,16 +631,6 @@ bool make_input_map(CUtensorMap* m, const void* x, int64_t L, int32_t heads, int
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-int g_num_sms = 0;
-int num_sms() {
-  if (!g_num_sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-    if (g_num_sms <= 0) g_num_sms = 148;
-  }
-  return g_num_sms;
-}
 
 // Launch the TMA quantiser if the request fits it; returns false to fall back.
 bool try_tma_quant(const void* const* xs, int njobs, int dtype, int64_t ts, int64_t hs, int32_t heads,
@@ -654,13 +644,9 @@ bool try_tma_quant(const void* const* xs, int njobs, int dtype, int64_t ts, int6
     if (!make_input_map(&tm[i], xs[i < njobs ? i : 0], L, heads, ts, hs, g.sw)) return false;
   const int smem = kTmaStages * kTmaStageBytes;
   auto kern = fmt == FPSA_E4M3 ? quant_tma_kernel<FPSA_E4M3> : quant_tma_kernel<FPSA_E5M2>;
-  static bool configured[2] = {false, false};
-  if (!configured[fmt]) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) return false;
-    configured[fmt] = true;
-  }
+  if (ensure_smem_attr(reinterpret_cast<const void*>(kern), smem, "quant_tma_kernel") != FPSA_OK) return false;
   const int64_t items = (int64_t)njobs * heads * g.M;
-  const int grid = (int)std::min<int64_t>(items, num_sms());
+  const int grid = (int)std::min<int64_t>(items, device_sm_count());
   kern<<<grid, kTmaThreads, smem, st>>>(tm[0], tm[1], tm[2], g, a);
   return true;
 }

@@ -38,13 +38,11 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                : "memory");
 }
-#ifndef FPSA_MBAR_SUSPEND_NS
-#define FPSA_MBAR_SUSPEND_NS 100000
-#endif
-// kSuspendNs > 0: suspend-time hint on try_wait (attention at C2: 11.54 -> 11.13 ms,
-// profiles/r01_ab_mbar_suspend_r3z.txt). The try_wait count per launch drops only ~10 %, so the gain is
-// more likely a faster wake-up on phase completion than fewer re-issued polls.
-template <uint32_t kSuspendNs = FPSA_MBAR_SUSPEND_NS>
+// kSuspendNs > 0: suspend-time hint on try_wait.  Only the FP8 attention kernel uses it (its A/B:
+// 11.54 -> 11.13 ms at C2, profiles/r01_ab_mbar_suspend_r3z.txt); every other kernel waits without a hint.
+// The try_wait count per launch drops only ~10 %, so the gain is more likely a faster wake-up on phase
+// completion than fewer re-issued polls.
+template <uint32_t kSuspendNs = 0>
 __device__ __forceinline__ bool mbar_try_wait(uint32_t addr, uint32_t parity) {
   uint32_t ok;
   if constexpr (kSuspendNs > 0) {
@@ -66,7 +64,7 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t addr, uint32_t parity) {
   }
   return ok != 0;
 }
-template <uint32_t kSuspendNs = FPSA_MBAR_SUSPEND_NS>
+template <uint32_t kSuspendNs = 0>
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t addr = smem_u32(bar);
   while (!mbar_try_wait<kSuspendNs>(addr, parity)) {

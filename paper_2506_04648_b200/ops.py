@@ -11,6 +11,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import threading
 
 import numpy as np
 
@@ -31,8 +32,11 @@ def _ptr(t) -> int:
     return t.data_ptr()
 
 
-def _stream():
-    return _torch().cuda.current_stream().cuda_stream
+def _stream(device=None):
+    return _torch().cuda.current_stream(device).cuda_stream
+
+
+P_MODES = {"onepass": _lib.P_ONEPASS, "normalized": _lib.P_NORMALIZED}
 
 
 def _dtype_id(t) -> int:
@@ -82,6 +86,8 @@ class _TilePlan:
         self.pitch = tile_pitch(self.tv) if pitch is None else int(pitch)
         self.mask = build_block_mask(self.window, self.tile_dims)
         self.device = torch.device(device)
+        if self.device.type == "cuda" and self.device.index is None:
+            self.device = torch.device("cuda", torch.cuda.current_device())
         dev = self.device
         self.offs = torch.from_numpy(self.mask.offsets.astype(np.int32)).to(dev)
         self.ids = torch.from_numpy(np.ascontiguousarray(self.mask.ids, dtype=np.int32)).to(dev)
@@ -91,6 +97,10 @@ class _TilePlan:
         need = ctypes.c_int64(0)
         _lib.check(_lib.lib().fpsa_attn_workspace_bytes(self.n_items, ctypes.byref(need)))
         self.attn_ws = torch.zeros(-(-need.value // 4), dtype=torch.int32, device=dev)
+
+    def _guard(self):
+        """Make the plan's device current for a call: its buffers, TMA maps and streams live there."""
+        return _torch().cuda.device(self.device)
 
     # ------------------------------------------------------------------ accounting
     @property
@@ -150,10 +160,12 @@ class FpsaPlan(_TilePlan):
     """
 
     def __init__(self, grid, tile, window, heads: int, d: int, fmt: Fp8Format = E4M3, *,
-                 device="cuda", tau: float = 8.0, pitch: int | None = None):
+                 device="cuda", tau: float = 8.0, pitch: int | None = None, p_mode: str = "onepass"):
+        if p_mode not in P_MODES:
+            raise ValueError(f"p_mode must be one of {sorted(P_MODES)}, got {p_mode!r}")
         super().__init__(grid, tile, window, heads, d, device, pitch)
         torch = _torch()
-        self.fmt, self.tau = fmt, float(tau)
+        self.fmt, self.tau, self.p_mode = fmt, float(tau), p_mode
         dev = self.device
         rows = self.heads * self.M * self.pitch
         self.q_codes = torch.empty(rows * self.d, dtype=torch.uint8, device=dev)
@@ -168,8 +180,11 @@ class FpsaPlan(_TilePlan):
     # ------------------------------------------------------------------ kernels
     def quantize(self, q, k, v, layout: str = "lhd", tile_order: bool = False, stream=None) -> None:
         """K1/K2: per-tile Q/K and per-channel V codes into the plan's buffers."""
+        with self._guard():
+            self._quantize(q, k, v, layout, tile_order, _stream(self.device) if stream is None else stream)
+
+    def _quantize(self, q, k, v, layout, tile_order, st) -> None:
         L = _lib.lib()
-        st = _stream() if stream is None else stream
         order = _lib.ORDER_TILE if tile_order else _lib.ORDER_NATURAL
         g, t = _lib.dims3(self.grid), _lib.dims3(self.tile)
         f = self.fmt.abi_id
@@ -192,15 +207,17 @@ class FpsaPlan(_TilePlan):
 
     def attention(self, out, layout: str = "lhd", tile_order: bool = False, softmax_scale: float | None = None,
                   stream=None) -> None:
-        """K4 over the quantised buffers; writes `out` (f32 or bf16)."""
+        """K4 over the quantised buffers; writes `out` (f32 or bf16; f32 in the normalised-P mode)."""
         scale, odt, ts, hs = self._out_args(out, layout, softmax_scale)
-        st = _stream() if stream is None else stream
-        _lib.check(_lib.lib().fpsa_attn_fwd(
-            _ptr(self.q_codes), _ptr(self.k_codes), _ptr(self.v_codes), _ptr(self.q_scales), _ptr(self.k_scales),
-            _ptr(self.v_scales), self.heads, _lib.dims3(self.grid), _lib.dims3(self.tile), self.d, self.pitch,
-            _ptr(self.offs), _ptr(self.ids), _ptr(self.items), self.n_items, scale, self.fmt.abi_id,
-            self.tau, _ptr(out), odt, ts, hs, _lib.ORDER_TILE if tile_order else _lib.ORDER_NATURAL,
-            _ptr(self.attn_ws), self.attn_ws.numel() * 4, st))
+        with self._guard():
+            st = _stream(self.device) if stream is None else stream
+            _lib.check(_lib.lib().fpsa_attn_fwd(
+                _ptr(self.q_codes), _ptr(self.k_codes), _ptr(self.v_codes), _ptr(self.q_scales),
+                _ptr(self.k_scales), _ptr(self.v_scales), self.heads, _lib.dims3(self.grid), _lib.dims3(self.tile),
+                self.d, self.pitch, _ptr(self.offs), _ptr(self.ids), _ptr(self.items), self.n_items, scale,
+                self.fmt.abi_id, self.tau, P_MODES[self.p_mode], _ptr(out), odt, ts, hs,
+                _lib.ORDER_TILE if tile_order else _lib.ORDER_NATURAL, _ptr(self.attn_ws), self.attn_ws.numel() * 4,
+                st))
 
     def check_finite(self) -> None:
         """Raise ValueError if a quantised input held a non-finite value (synchronises)."""
@@ -255,6 +272,10 @@ class HostStreamer:
         return p.flops // p.heads * self.heads
 
     def __call__(self, q_host, k_host, v_host, out_host) -> None:
+        with _torch().cuda.device(self.device):
+            self._run(q_host, k_host, v_host, out_host)
+
+    def _run(self, q_host, k_host, v_host, out_host) -> None:
         torch = _torch()
         for x in (q_host, k_host, v_host, out_host):
             if x.device.type != "cpu" or not x.is_pinned() or not x.is_contiguous() or x.dtype != torch.bfloat16:
@@ -322,24 +343,26 @@ class PassthroughPlan(_TilePlan):
     def gather(self, q, k, v, layout: str = "lhd", tile_order: bool = False, stream=None) -> None:
         """q, k, v -> tile-major padded bf16 (f32 inputs rounded to nearest even)."""
         L = _lib.lib()
-        st = _stream() if stream is None else stream
         order = _lib.ORDER_TILE if tile_order else _lib.ORDER_NATURAL
         g, t = _lib.dims3(self.grid), _lib.dims3(self.tile)
-        for x, dst in ((q, self.q_tiles), (k, self.k_tiles), (v, self.v_tiles)):
-            ts, hs = self._strides(x, layout)
-            _lib.check(L.fpsa_tile_gather_bf16(_ptr(x), _dtype_id(x), ts, hs, self.heads, g, t, self.d, self.pitch,
-                                               order, _ptr(dst), st))
+        with self._guard():
+            st = _stream(self.device) if stream is None else stream
+            for x, dst in ((q, self.q_tiles), (k, self.k_tiles), (v, self.v_tiles)):
+                ts, hs = self._strides(x, layout)
+                _lib.check(L.fpsa_tile_gather_bf16(_ptr(x), _dtype_id(x), ts, hs, self.heads, g, t, self.d,
+                                                   self.pitch, order, _ptr(dst), st))
 
     def attention(self, out, layout: str = "lhd", tile_order: bool = False, softmax_scale: float | None = None,
                   stream=None) -> None:
         """Passthrough attention over the gathered tiles; writes `out` (f32 or bf16)."""
         scale, odt, ts, hs = self._out_args(out, layout, softmax_scale)
-        st = _stream() if stream is None else stream
-        _lib.check(_lib.lib().fpsa_attn_bf16_fwd(
-            _ptr(self.q_tiles), _ptr(self.k_tiles), _ptr(self.v_tiles), self.heads, _lib.dims3(self.grid),
-            _lib.dims3(self.tile), self.d, self.pitch, _ptr(self.offs), _ptr(self.ids), _ptr(self.items),
-            self.n_items, scale, _ptr(out), odt, ts, hs, _lib.ORDER_TILE if tile_order else _lib.ORDER_NATURAL,
-            _ptr(self.attn_ws), self.attn_ws.numel() * 4, st))
+        with self._guard():
+            st = _stream(self.device) if stream is None else stream
+            _lib.check(_lib.lib().fpsa_attn_bf16_fwd(
+                _ptr(self.q_tiles), _ptr(self.k_tiles), _ptr(self.v_tiles), self.heads, _lib.dims3(self.grid),
+                _lib.dims3(self.tile), self.d, self.pitch, _ptr(self.offs), _ptr(self.ids), _ptr(self.items),
+                self.n_items, scale, _ptr(out), odt, ts, hs, _lib.ORDER_TILE if tile_order else _lib.ORDER_NATURAL,
+                _ptr(self.attn_ws), self.attn_ws.numel() * 4, st))
 
     def __call__(self, q, k, v, layout: str = "lhd", out=None, out_dtype=None, tile_order: bool = False,
                  softmax_scale: float | None = None):
@@ -376,9 +399,10 @@ def device_fidelity(ref, approx, layout: str = "lhd", stream=None) -> list[tuple
     else:
         raise ValueError(f"unknown layout {layout!r}")
     sums = torch.empty((heads, 6), dtype=torch.float64, device=ref.device)
-    st = _stream() if stream is None else stream
-    _lib.check(_lib.lib().fpsa_fidelity(_ptr(ref), _dtype_id(ref), _ptr(approx), _dtype_id(approx), tokens, heads, d,
-                                        ts, hs, _ptr(sums), st))
+    with torch.cuda.device(ref.device):
+        st = _stream(ref.device) if stream is None else stream
+        _lib.check(_lib.lib().fpsa_fidelity(_ptr(ref), _dtype_id(ref), _ptr(approx), _dtype_id(approx), tokens, heads,
+                                            d, ts, hs, _ptr(sums), st))
     from .metrics import fidelity_from_sums
 
     return [fidelity_from_sums(*row, n=tokens * d) for row in sums.cpu().tolist()]
@@ -403,12 +427,16 @@ def fps_attention(q, k, v, grid, tile, window, *, fmt: Fp8Format = E4M3, softmax
     else:
         raise ValueError(f"unknown layout {layout!r}")
     win = window if isinstance(window, WindowSpec) else WindowSpec(*window)
-    key = (tuple(grid), tuple(tile), win.dims, H, d, fmt.name, str(q.device), tau)
+    torch = _torch()
+    # one plan (code buffers + workspace) per device, stream and thread: calls that could overlap never share
+    # buffers, calls on one stream are ordered by it
+    stream = torch.cuda.current_stream(q.device)
+    key = (tuple(grid), tuple(tile), win.dims, H, d, fmt.name, str(q.device), tau, stream.cuda_stream,
+           threading.get_ident())
     plan = _PLANS.get(key)
     if plan is None:
         plan = FpsaPlan(grid, tile, win, H, d, fmt, device=q.device, tau=tau)
         _PLANS[key] = plan
-    torch = _torch()
     out = torch.empty(q.shape, dtype=out_dtype or q.dtype, device=q.device)
     for b in range(B):
         sl = (lambda x: x[b]) if batched else (lambda x: x)

@@ -56,3 +56,32 @@ def test_gpu_arm_contract():
     assert set(d["clocks"]) >= {"sm_mhz", "sm_max_mhz", "reasons"}
     e2e = d["e2e"]
     assert e2e["h2d_bytes_per_step"] > 0 and e2e["d2h_bytes_per_step"] > 0 and 0 < e2e["value"] < d["value"]
+
+
+def test_reference_arm_two_ranks():
+    """--gpus 2 without torchrun: bench.py starts two ranks itself; the reference arm runs on rank 0 only and
+    reports n_gpus = 2 (the other rank exits 0 without work)."""
+    d = _run(["--impl", "reference", "--gpus", "2", "--steps", "1", "--warmup", "0", "--config", "wan13b_480p"],
+             600)
+    assert d["impl"] == "reference" and d["n_gpus"] == 2
+
+
+@pytest.mark.gpu
+def test_gpu_arm_two_ranks(tmp_path):
+    """--gpus 2 self-launches two ranks (sharing cuda:0 on a 1-GPU box: gloo for the timing collectives),
+    heads split 6/6 at C1, max-over-ranks timing; every head's output is bit-identical to the 1-rank run."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    one, two = tmp_path / "n1", tmp_path / "n2"
+    d1 = _run(["--steps", "3", "--warmup", "3", "--no-cpu", "--no-e2e", "--config", "wan13b_480p",
+               "--dump-out", str(one)], 900)
+    d2 = _run(["--gpus", "2", "--steps", "3", "--warmup", "3", "--no-cpu", "--no-e2e", "--config", "wan13b_480p",
+               "--dump-out", str(two)], 900)
+    _common(d2)
+    assert d1["n_gpus"] == 1 and d2["n_gpus"] == 2
+    assert d2["config"]["heads_per_gpu"] == 6
+    h1 = json.load(open(one / "rank0.json"))
+    h2 = {**json.load(open(two / "rank0.json")), **json.load(open(two / "rank1.json"))}
+    assert sorted(h1, key=int) == sorted(h2, key=int) == [str(h) for h in range(12)]
+    assert h1 == h2

@@ -247,9 +247,16 @@ def test_device_calls_reject_bad_arguments_before_cuda(lib):
                               None, None, None, None)
     assert st in (_lib.FPSA_EINVAL, _lib.FPSA_EINDIVISIBLE)
     st = lib.fpsa_attn_fwd(None, None, None, None, None, None, 1, g, t, 64, 128, None, None, None, 1, 0.125, 0, 8.0,
-                           None, _lib.F32, 64, 0, _lib.ORDER_TILE, None, 0, None)
+                           _lib.P_ONEPASS, None, _lib.F32, 64, 0, _lib.ORDER_TILE, None, 0, None)
     assert st == _lib.FPSA_EINVAL
     assert lib.fpsa_last_error()
+    st = lib.fpsa_attn_fwd(None, None, None, None, None, None, 1, g, t, 64, 128, None, None, None, 1, 0.125, 0, 8.0,
+                           7, None, _lib.F32, 64, 0, _lib.ORDER_TILE, None, 0, None)
+    assert st == _lib.FPSA_EINVAL and b"p_mode" in lib.fpsa_last_error()
+    # the normalised-P mode writes f32 only
+    st = lib.fpsa_attn_fwd(None, None, None, None, None, None, 1, g, t, 64, 128, None, None, None, 1, 0.125, 0, 8.0,
+                           _lib.P_NORMALIZED, None, _lib.BF16, 64, 0, _lib.ORDER_TILE, None, 0, None)
+    assert st == _lib.FPSA_EUNSUPPORTED
     # passthrough entry points
     st = lib.fpsa_tile_gather_bf16(None, _lib.F32, 64, 0, 1, g, t, 64, 128, _lib.ORDER_TILE, None, None)
     assert st == _lib.FPSA_EINVAL
