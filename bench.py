@@ -420,7 +420,7 @@ def main():
         step(q, k, v, out)
         torch.cuda.synchronize()
         os.makedirs(args.dump_out, exist_ok=True)
-        digests = {str(h0 + j): hashlib.sha256(out[:, j].contiguous().cpu().numpy().tobytes()).hexdigest()
+        digests = {str(h0 + j): hashlib.sha256(out[:, j].contiguous().view(torch.int16).cpu().numpy().tobytes()).hexdigest()
                    for j in range(Hr)}
         with open(os.path.join(args.dump_out, f"rank{rank}.json"), "w") as f:
             json.dump(digests, f)
