@@ -105,15 +105,37 @@ int fpsa_quantize_v(const void* x, int dtype, int64_t token_stride, int64_t head
                     fpsa_dims3 grid, fpsa_dims3 tile, int32_t d, int32_t tile_pitch, int in_order, int fmt,
                     uint8_t* codes, double* scales, void* workspace, int32_t* err_flag, void* stream);
 
+/* Device workspace bytes of fpsa_quantize_qkv / fpsa_quantize_qkv_amax:
+ * (heads*(d+1) + 1) * 4 (v channel maxima, per-head completion counters, an
+ * item counter; zeroed by the call itself). */
+int fpsa_quantize_workspace_bytes(int32_t heads, int32_t d, int64_t* bytes);
+
 /* Fused form of fpsa_quantize_qk(q) + fpsa_quantize_qk(k) + fpsa_quantize_v(v)
- * for three tensors with the same dtype and strides: one channel-amax pass
- * over v, then a single launch that quantises all three (bit-identical to the
- * separate calls).  workspace: device, >= heads*d*4 bytes. */
+ * for three tensors with the same dtype and strides, bit-identical to the
+ * separate calls.  bf16, d = 128, tile volume <= 256: ONE persistent launch
+ * (per head: v channel-amax tiles, then q and k tiles, then v code tiles that
+ * wait for the head's channel maxima); otherwise a channel-amax pass over v
+ * and one launch over all tiles.  workspace: device,
+ * >= fpsa_quantize_workspace_bytes(heads, d). */
 int fpsa_quantize_qkv(const void* q, const void* k, const void* v, int dtype, int64_t token_stride,
                       int64_t head_stride, int32_t heads, fpsa_dims3 grid, fpsa_dims3 tile, int32_t d,
                       int32_t tile_pitch, int in_order, int fmt, uint8_t* q_codes, uint8_t* k_codes,
                       uint8_t* v_codes, double* q_scales, double* k_scales, double* v_scales, void* workspace,
                       int32_t* err_flag, void* stream);
+
+/* fpsa_quantize_qkv with the absolute maxima supplied by the producer of q, k, v
+ * (the upstream-fusion hook, Alg. 1 steps 2-3: a QKV-projection
+ * epilogue reduces |x| while it writes): q_tile_amax / k_tile_amax f32
+ * [heads*M] (tile order), v_channel_amax f32 [heads*d]; any may be NULL
+ * (computed here).  They must equal max|x| over the tile / channel, so the
+ * codes and scales stay those of the reference.  With v_channel_amax the
+ * extra read of v disappears; with the tile maxima the per-tile reductions. */
+int fpsa_quantize_qkv_amax(const void* q, const void* k, const void* v, int dtype, int64_t token_stride,
+                           int64_t head_stride, int32_t heads, fpsa_dims3 grid, fpsa_dims3 tile, int32_t d,
+                           int32_t tile_pitch, int in_order, int fmt, const float* q_tile_amax,
+                           const float* k_tile_amax, const float* v_channel_amax, uint8_t* q_codes,
+                           uint8_t* k_codes, uint8_t* v_codes, double* q_scales, double* k_scales, double* v_scales,
+                           void* workspace, int32_t* err_flag, void* stream);
 
 /* Work list for fpsa_attn_fwd: one entry per (head, query tile, 128-row
  * query block), tiles with the most key tiles first within each head, the

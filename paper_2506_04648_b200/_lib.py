@@ -59,6 +59,10 @@ SIGNATURES = {
                                    _vp, _vp, _vp, _vp, _vp]),
     "fpsa_quantize_qkv": (_c.c_int, [_vp, _vp, _vp, _c.c_int, _i64, _i64, _i32, Dims3, Dims3, _i32, _i32,
                                      _c.c_int, _c.c_int, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "fpsa_quantize_workspace_bytes": (_c.c_int, [_i32, _i32, _pi64]),
+    "fpsa_quantize_qkv_amax": (_c.c_int, [_vp, _vp, _vp, _c.c_int, _i64, _i64, _i32, Dims3, Dims3, _i32, _i32,
+                                          _c.c_int, _c.c_int, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
+                                          _vp]),
     "fpsa_attn_worklist": (_c.c_int, [_i32, Dims3, _i32, _pi32, _pi32, _i64, _pi64]),
     "fpsa_attn_workspace_bytes": (_c.c_int, [_i32, _pi64]),
     "fpsa_attn_fwd": (_c.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _i32, Dims3, Dims3, _i32, _i32, _vp, _vp, _vp, _i32,

@@ -174,7 +174,9 @@ class FpsaPlan(_TilePlan):
         self.q_scales = torch.empty(self.heads * self.M, dtype=torch.float64, device=dev)
         self.k_scales = torch.empty_like(self.q_scales)
         self.v_scales = torch.empty(self.heads * self.d, dtype=torch.float64, device=dev)
-        self.workspace = torch.empty(self.heads * self.d, dtype=torch.int32, device=dev)
+        ws = ctypes.c_int64(0)
+        _lib.check(_lib.lib().fpsa_quantize_workspace_bytes(self.heads, self.d, ctypes.byref(ws)))
+        self.workspace = torch.empty(-(-ws.value // 4), dtype=torch.int32, device=dev)
         self.err = torch.zeros(1, dtype=torch.int32, device=dev)
 
     # ------------------------------------------------------------------ kernels
@@ -204,6 +206,37 @@ class FpsaPlan(_TilePlan):
         _lib.check(L.fpsa_quantize_v(_ptr(v), _dtype_id(v), ts, hs, self.heads, g, t, self.d, self.pitch, order,
                                      f, _ptr(self.v_codes), _ptr(self.v_scales), _ptr(self.workspace),
                                      _ptr(self.err), st))
+
+    def quantize_with_amax(self, q, k, v, q_tile_amax=None, k_tile_amax=None, v_channel_amax=None,
+                           layout: str = "lhd", tile_order: bool = False, stream=None) -> None:
+        """The upstream-fusion hook (Alg. 1 steps 2-3): like :meth:`quantize`, with the absolute
+        maxima supplied by the producer of q, k, v -- f32 CUDA tensors [H, M] (tile order) for q / k,
+        [H, d] for v; any may be None.  They must equal the true maxima; the codes are then identical to
+        :meth:`quantize`'s, and a supplied v maximum removes the extra read of v."""
+        torch = _torch()
+        strides = [self._strides(x, layout) for x in (q, k, v)]
+        if not (strides[0] == strides[1] == strides[2] and q.dtype == k.dtype == v.dtype):
+            raise ValueError("q, k, v must share dtype and strides")
+
+        def amax_arg(t, shape):
+            if t is None:
+                return None
+            if t.dtype != torch.float32 or t.device != self.device or tuple(t.shape) != shape or not t.is_contiguous():
+                raise ValueError(f"amax must be a contiguous float32 {shape} tensor on {self.device}")
+            return _ptr(t)
+
+        qa = amax_arg(q_tile_amax, (self.heads, self.M))
+        ka = amax_arg(k_tile_amax, (self.heads, self.M))
+        va = amax_arg(v_channel_amax, (self.heads, self.d))
+        ts, hs = strides[0]
+        order = _lib.ORDER_TILE if tile_order else _lib.ORDER_NATURAL
+        with self._guard():
+            st = _stream(self.device) if stream is None else stream
+            _lib.check(_lib.lib().fpsa_quantize_qkv_amax(
+                _ptr(q), _ptr(k), _ptr(v), _dtype_id(q), ts, hs, self.heads, _lib.dims3(self.grid),
+                _lib.dims3(self.tile), self.d, self.pitch, order, self.fmt.abi_id, qa, ka, va, _ptr(self.q_codes),
+                _ptr(self.k_codes), _ptr(self.v_codes), _ptr(self.q_scales), _ptr(self.k_scales),
+                _ptr(self.v_scales), _ptr(self.workspace), _ptr(self.err), st))
 
     def attention(self, out, layout: str = "lhd", tile_order: bool = False, softmax_scale: float | None = None,
                   stream=None) -> None:

@@ -164,3 +164,58 @@ def test_bf16_exact_ties_natural_order(fpsa, tie_rich):
         c, s = O.quantize_v_channelwise(xt)
         assert np.array_equal(plan.v_scales.view(H, d)[h].cpu().numpy(), s)
         assert np.array_equal(vc[h, :, :tv, :].reshape(L, d), c)
+
+
+def _check_plan_codes(plan, xs, perm):
+    """Every head's q, k, v codes and scales in `plan` against the oracle (bit-exact)."""
+    H, M, tv, d, L = plan.heads, plan.M, plan.tv, plan.d, plan.L
+    bufs = [(plan.q_codes, plan.q_scales, False), (plan.k_codes, plan.k_scales, False),
+            (plan.v_codes, plan.v_scales, True)]
+    for x, (codes, scales, chan) in zip(xs, bufs):
+        cc = codes.view(H, M, plan.pitch, d).cpu().numpy()
+        sc = scales.cpu().numpy()
+        xf = x.float().cpu().numpy()
+        for h in range(H):
+            xt = xf[perm, h, :]
+            c, s = O.quantize_v_channelwise(xt) if chan else O.quantize_qk_tilewise(xt, tv)
+            assert np.array_equal(sc.reshape(H, -1)[h], s)
+            assert np.array_equal(cc[h, :, :tv, :].reshape(L, d), c)
+            assert (cc[h, :, tv:, :] == 0).all()
+
+
+def test_fused_quantiser_distinct_qkv_many_heads(fpsa):
+    """The fused one-launch quantiser (v channel-amax tiles -> q, k tiles -> v code tiles waiting on the
+    head's maxima) with distinct q, k, v over 6 heads of the C2 grid: all codes / scales bit-exact."""
+    grid, tile, H, d = (21, 45, 80), (3, 5, 16), 6, 128
+    L = grid[0] * grid[1] * grid[2]
+    gen = torch.Generator(device="cuda").manual_seed(11)
+    xs = [(torch.randn((L, H, d), generator=gen, device="cuda") * s).to(torch.bfloat16) for s in (1.0, 3.0, 0.5)]
+    plan = fpsa.FpsaPlan(grid, tile, (3, 3, 3), H, d)
+    for _ in range(2):  # the second call reuses the workspace (counters re-zeroed by the call)
+        plan.quantize(*xs, "lhd")
+    torch.cuda.synchronize()
+    plan.check_finite()
+    _check_plan_codes(plan, xs, O.tile_perm(grid, tile))
+
+
+@pytest.mark.parametrize("given", ["qkv", "v", "qk"])
+def test_quantize_with_amax_hook(fpsa, given):
+    """f3 fusion hook: caller-supplied tile / channel maxima give the same codes and scales as the
+    self-reducing quantiser (and those are the reference's)."""
+    grid, tile, H, d = (6, 10, 32), (3, 5, 16), 3, 128
+    L = grid[0] * grid[1] * grid[2]
+    gen = torch.Generator(device="cuda").manual_seed(5)
+    xs = [torch.randn((L, H, d), generator=gen, device="cuda").to(torch.bfloat16) for _ in range(3)]
+    plan = fpsa.FpsaPlan(grid, tile, (3, 3, 3), H, d)
+    perm = torch.from_numpy(O.tile_perm(grid, tile)).cuda()
+    tv, M = plan.tv, plan.M
+
+    def tile_amax(x):  # [L, H, d] natural order -> [H, M] f32 max|x| per tile
+        return x.float()[perm].abs().view(M, tv, H, d).amax(dim=(1, 3)).t().contiguous()
+
+    qa = tile_amax(xs[0]) if "q" in given else None
+    ka = tile_amax(xs[1]) if "k" in given else None
+    va = xs[2].float().abs().amax(dim=0).contiguous() if "v" in given else None
+    plan.quantize_with_amax(*xs, qa, ka, va, layout="lhd")
+    torch.cuda.synchronize()
+    _check_plan_codes(plan, xs, O.tile_perm(grid, tile))
