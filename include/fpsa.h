@@ -105,17 +105,15 @@ int fpsa_quantize_v(const void* x, int dtype, int64_t token_stride, int64_t head
                     fpsa_dims3 grid, fpsa_dims3 tile, int32_t d, int32_t tile_pitch, int in_order, int fmt,
                     uint8_t* codes, double* scales, void* workspace, int32_t* err_flag, void* stream);
 
-/* Device workspace bytes of fpsa_quantize_qkv / fpsa_quantize_qkv_amax:
- * (heads*(d+1) + 1) * 4 (v channel maxima, per-head completion counters, an
- * item counter; zeroed by the call itself). */
+/* Device workspace bytes of fpsa_quantize_qkv / fpsa_quantize_qkv_amax
+ * ((heads*(d+1) + 1) * 4: v channel maxima plus spare words; zeroed by the call). */
 int fpsa_quantize_workspace_bytes(int32_t heads, int32_t d, int64_t* bytes);
 
 /* Fused form of fpsa_quantize_qk(q) + fpsa_quantize_qk(k) + fpsa_quantize_v(v)
  * for three tensors with the same dtype and strides, bit-identical to the
- * separate calls.  bf16, d = 128, tile volume <= 256: ONE persistent launch
- * (per head: v channel-amax tiles, then q and k tiles, then v code tiles that
- * wait for the head's channel maxima); otherwise a channel-amax pass over v
- * and one launch over all tiles.  workspace: device,
+ * separate calls: one channel-amax pass over v, then a single persistent
+ * TMA-fed launch over all q, k and v tiles (bf16, d = 128, tile volume <= 256;
+ * otherwise one grid over all tiles).  workspace: device,
  * >= fpsa_quantize_workspace_bytes(heads, d). */
 int fpsa_quantize_qkv(const void* q, const void* k, const void* v, int dtype, int64_t token_stride,
                       int64_t head_stride, int32_t heads, fpsa_dims3 grid, fpsa_dims3 tile, int32_t d,
@@ -129,7 +127,8 @@ int fpsa_quantize_qkv(const void* q, const void* k, const void* v, int dtype, in
  * [heads*M] (tile order), v_channel_amax f32 [heads*d]; any may be NULL
  * (computed here).  They must equal max|x| over the tile / channel, so the
  * codes and scales stay those of the reference.  With v_channel_amax the
- * extra read of v disappears; with the tile maxima the per-tile reductions. */
+ * channel-amax pass (an extra read of v) disappears; the tile maxima are
+ * reduced from the tile in shared memory anyway. */
 int fpsa_quantize_qkv_amax(const void* q, const void* k, const void* v, int dtype, int64_t token_stride,
                            int64_t head_stride, int32_t heads, fpsa_dims3 grid, fpsa_dims3 tile, int32_t d,
                            int32_t tile_pitch, int in_order, int fmt, const float* q_tile_amax,

@@ -418,207 +418,120 @@ __global__ void __launch_bounds__(kQuantThreads)
 }
 
 // ---------------------------------------------------------------------------
-// Fused TMA-fed persistent quantiser of q, k and v (bf16 input, d = 128, tile
-// volume <= 256): one launch, every byte of q, k, v read from HBM once for
-// the codes plus one extra read of v for its channel amax.
+// TMA-fed persistent quantiser (bf16 input, d = 128, tile volume <= 256).
 //
-// Work items, claimed in order from a global counter, per head h:
-//   VA(h, u)  v tile u: per-channel |x| max of the tile -> atomicMax into
-//             amax[h][c]; then done[h] += 1
-//   Q(h, u), K(h, u)   q / k tile u: tile amax -> f64 scale -> codes
-//   VE(h, u)  v tile u: waits for done[h] == M (all VA items of the head,
-//             claimed M..3M items earlier, so the wait is almost never
-//             taken), then codes with the per-channel scales.
-// VE(h, .) follows VA(h, .) by the 2M q/k tiles of the head (39 MB of bf16
-// at C2), so most of v's second read is served by L2.  With caller-provided
-// amax (fpsa_quantize_qkv_amax, the f3 fusion hook) there are no VA items
-// and no tile amax reductions.
-//
-// CTA: one producer warp (claims items, TMA-loads each tile into one of
-// kFqStages shared-memory stages, one box per run of tile_w tokens) and two
-// consumer groups of kFqGroupWarps warps that take alternate items.  A group
-// copies its tile from shared memory into registers (each warp holds rows
-// w, w + 8, ... : 4 channels per lane) and releases the stage at once, so
-// the producer's next loads overlap the group's reductions and stores; the
-// group's named barriers never stall the other group.  Elements whose
-// bracketed fast code is ambiguous (mostly exact ties of bf16 data) are
-// queued per group and re-encoded exactly after the tile.
-#ifndef FPSA_FQ_GROUPS
-#define FPSA_FQ_GROUPS 1  // consumer groups taking alternate tiles (2 groups of 8 warps spill at 96 registers)
+// One CTA per SM loops over (tensor, head, tile) items.  A producer warp
+// streams each tile into shared memory with 3D TMA loads (one box per run
+// of tile_w consecutive tokens, strided by the token stride, so the gather
+// to tile-major order is done by the copy engine), kTmaStages tiles ahead;
+// 24 consumer warps reduce the tile amax from shared memory and write the
+// codes.  HBM traffic is one read of q/k/v and one write of the codes.
+#ifndef FPSA_QUANT_WARPS
+#define FPSA_QUANT_WARPS 24  // measured best: 1.26 ms at C2 vs 1.31 (20), 1.28 (28), 1.37 (16), 1.56 (12)
 #endif
-constexpr int kFqGroups = FPSA_FQ_GROUPS;
-constexpr int kFqGroupWarps = 16 / kFqGroups;
-constexpr int kFqThreads = (kFqGroups * kFqGroupWarps + 1) * 32;
-constexpr int kFqStages = 3;
-constexpr int kFqMaxRows = 256;
-constexpr int kFqRowsPerWarp = kFqMaxRows / kFqGroupWarps;
-constexpr int kFqD = 128;
-constexpr int kFqStageBytes = kFqMaxRows * kFqD * 2;
-constexpr uint32_t kFqQueueCap = 1024;
-constexpr int kFqProducerWarp = kFqGroups * kFqGroupWarps;
+constexpr int kTmaConsumerWarps = FPSA_QUANT_WARPS;
+constexpr int kTmaThreads = (kTmaConsumerWarps + 1) * 32;
+constexpr int kTmaStages = 3;
+constexpr int kTmaMaxRows = 256;
+constexpr int kTmaD = 128;
+constexpr int kTmaStageBytes = kTmaMaxRows * kTmaD * 2;
+constexpr uint32_t kTmaQueueCap = 2048;
 
-enum FqKind { kFqVA = 0, kFqQ = 1, kFqK = 2, kFqVE = 3 };
-
-struct FqArgs {
-  uint8_t* codes[3];        // q, k, v
+struct TmaQuantArgs {
+  uint8_t* codes[3];
   double* scales[3];
-  const float* given[3];    // caller amax (f32 |x| max): q/k per tile [heads*M], v per channel [heads*d]; or null
-  uint32_t* amax;           // v channel amax bits [heads][d] (zeroed), unused with given amax
-  int32_t* done;            // [heads] VA items finished (zeroed)
-  int32_t* claim;           // item counter (zeroed)
+  int32_t channel[3];
+  int32_t njobs, heads;
+  const uint32_t* amax;
   int32_t* err;
-  int32_t heads;
-  int32_t kinds;            // 4 (VA, Q, K, VE) or 3 (Q, K, VE: v amax given)
 };
 
 template <int FMT>
-__global__ void __launch_bounds__(kFqThreads, 1)
-    quant_fused_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
-                       const __grid_constant__ CUtensorMap tm_v, Geometry g, FqArgs a) {
+__global__ void __launch_bounds__(kTmaThreads, 1)
+    quant_tma_kernel(const __grid_constant__ CUtensorMap tm0, const __grid_constant__ CUtensorMap tm1,
+                     const __grid_constant__ CUtensorMap tm2, Geometry g, TmaQuantArgs a) {
   using namespace sm100;
   constexpr int VEC = 4;
   constexpr double kMax = FMT == FPSA_E4M3 ? 448.0 : 57344.0;
   using V = Vec<__nv_bfloat16, VEC>;
   extern __shared__ __align__(128) uint8_t smem[];
-  __shared__ uint64_t full[kFqStages], empty[kFqStages];
-  __shared__ int32_t s_item[kFqStages];
-  __shared__ uint32_t s_red[kFqGroups][kFqGroupWarps][kFqD];  // per-warp partial maxima (VA: channels, Q/K: [0])
-  __shared__ uint32_t s_queue[kFqGroups][2][kFqQueueCap];
-  __shared__ uint32_t s_count[kFqGroups][2];
+  __shared__ uint64_t full[kTmaStages], empty[kTmaStages];
+  __shared__ uint32_t s_peak[2];  // tile |x| max bits by tile parity (shared-memory atomicMax of the warps)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int32_t per_head = a.kinds * g.M;
-  const int32_t n_items = a.heads * per_head;
-  const int32_t first_kind = a.kinds == 4 ? kFqVA : kFqQ;
+  const int32_t per_job = a.heads * g.M;
+  const int32_t n_items = a.njobs * per_job;
+  const int32_t runs = g.tv / g.sw;
   if (threadIdx.x == 0) {
-    for (int i = 0; i < kFqStages; ++i) {
+    for (int i = 0; i < kTmaStages; ++i) {
       mbar_init(&full[i], 1);
-      mbar_init(&empty[i], kFqGroupWarps);
+      mbar_init(&empty[i], kTmaConsumerWarps);
     }
-    for (int i = 0; i < kFqGroups; ++i) s_count[i][0] = s_count[i][1] = 0;
     fence_barrier_init();
   }
   __syncthreads();
 
-  if (warp == kFqProducerWarp) {
-    // ------------------------------------------------------------ producer: claim, then TMA
+  if (warp == kTmaConsumerWarps) {
+    // ------------------------------------------------------------ producer
     if (lane == 0) {
-      prefetch_tmap(&tm_q);
-      prefetch_tmap(&tm_k);
-      prefetch_tmap(&tm_v);
-      const int32_t runs = g.tv / g.sw;
-      int32_t k = 0;
-      for (;; ++k) {
-        const int st = k % kFqStages;
-        if (k >= kFqStages) mbar_wait(&empty[st], ((k / kFqStages) - 1) & 1);
-        const int32_t it = atomicAdd(a.claim, 1);
-        if (it >= n_items) break;
-        s_item[st] = it;
-        const int32_t h = it / per_head, r = it - h * per_head;
-        const int32_t kind = first_kind + r / g.M, u = r % g.M;
-        const void* tm = kind == kFqQ ? (const void*)&tm_q : (kind == kFqK ? (const void*)&tm_k : (const void*)&tm_v);
-        uint8_t* dst = smem + st * kFqStageBytes;
-        mbar_arrive_expect_tx(&full[st], (uint32_t)g.tv * kFqD * 2);
+      prefetch_tmap(&tm0);
+      prefetch_tmap(&tm1);
+      prefetch_tmap(&tm2);
+      int k = 0;
+      for (int32_t it = blockIdx.x; it < n_items; it += gridDim.x, ++k) {
+        const int st = k % kTmaStages;
+        if (k >= kTmaStages) mbar_wait(&empty[st], ((k / kTmaStages) - 1) & 1);
+        const int32_t z = it / per_job, rem = it - z * per_job, h = rem / g.M, u = rem - h * g.M;
+        const void* tm = z == 0 ? (const void*)&tm0 : (z == 1 ? (const void*)&tm1 : (const void*)&tm2);
+        uint8_t* dst = smem + st * kTmaStageBytes;
+        mbar_arrive_expect_tx(&full[st], (uint32_t)g.tv * kTmaD * 2);
         const int32_t base = tile_base(g, u);
-        for (int32_t rr = 0; rr < runs; ++rr) {
-          const int32_t lt = rr / g.sh, lh = rr - lt * g.sh;
-          const int32_t tok = g.natural ? base + (lt * g.gh + lh) * g.gw : base + rr * g.sw;
-          tma_load_3d(dst + rr * g.sw * kFqD * 2, tm, 0, tok, h, &full[st]);
+        for (int32_t r = 0; r < runs; ++r) {
+          // run r = (lt, lh) of the tile; in tile order runs are consecutive rows
+          const int32_t lt = r / g.sh, lh = r - lt * g.sh;
+          const int32_t tok = g.natural ? base + (lt * g.gh + lh) * g.gw : base + r * g.sw;
+          tma_load_3d(dst + r * g.sw * kTmaD * 2, tm, 0, tok, h, &full[st]);
         }
-      }
-      // one end marker per consumer group (items k and k + 1 go to different groups)
-      for (int e = 0; e < kFqGroups; ++e, ++k) {
-        const int st = k % kFqStages;
-        if (k >= kFqStages) mbar_wait(&empty[st], ((k / kFqStages) - 1) & 1);
-        s_item[st] = -1;
-        mbar_arrive(&full[st]);
       }
     }
     return;
   }
-  // -------------------------------------------------------------- consumer groups
-  // Per tile: [reductions] barrier A [codes, ambiguous bytes queued] barrier B [queue re-encoded exactly].
-  // Queue counters alternate by tile parity: count[p ^ 1] is reset between A and B, after every thread has
-  // read it (before A) and before any thread enqueues into it (after the next tile's A).
-  const int grp = warp / kFqGroupWarps, gw = warp % kFqGroupWarps;
-  const uint32_t bar_id = 1 + grp, bar_n = kFqGroupWarps * 32;
-  const int tid = gw * 32 + lane;
-  int qp = 0;
-  for (int32_t k = grp;; k += kFqGroups, qp ^= 1) {
-    const int st = k % kFqStages;
-    mbar_wait(&full[st], (k / kFqStages) & 1);
-    const int32_t it = s_item[st];
-    // registers <- this warp's rows (w, w + 8, ...), then the stage is free for the producer
-    typename V::raw raw[kFqRowsPerWarp];
-    const uint2* tile = reinterpret_cast<const uint2*>(smem + st * kFqStageBytes) + lane;
+  // -------------------------------------------------------------- consumers
+  // Ambiguous elements (the bracket straddles a rounding boundary: mostly
+  // exact ties of bf16 data, ~0.4% of elements) are queued in shared memory
+  // and re-encoded exactly by all consumer threads after the tile.
+  __shared__ uint16_t s_queue[2][kTmaQueueCap];
+  __shared__ uint32_t s_count[2];
+  if (threadIdx.x == 0) s_count[0] = s_peak[0] = 0;
+  named_bar_sync(1, kTmaConsumerWarps * 32);
+  int k = 0;
+  for (int32_t it = blockIdx.x; it < n_items; it += gridDim.x, ++k) {
+    const int st = k % kTmaStages;
+    const int32_t z = it / per_job, rem = it - z * per_job, h = rem / g.M, u = rem - h * g.M;
+    // select, do not index: a dynamically indexed parameter array is copied to local memory
+    const bool channel = (z == 0 ? a.channel[0] : z == 1 ? a.channel[1] : a.channel[2]) != 0;
+    uint8_t* const codes = z == 0 ? a.codes[0] : z == 1 ? a.codes[1] : a.codes[2];
+    double* const scales = z == 0 ? a.scales[0] : z == 1 ? a.scales[1] : a.scales[2];
+    uint8_t* out_tile = codes + ((int64_t)h * g.M + u) * g.pitch * kTmaD;
+    uint8_t* out = out_tile + lane * VEC;
+    const uint2* tile = reinterpret_cast<const uint2*>(smem + st * kTmaStageBytes) + lane;
+    mbar_wait(&full[st], (k / kTmaStages) & 1);
+    uint32_t m = 0;
+    if (!channel) {
+#pragma unroll 8
+      for (int32_t r = warp; r < g.tv; r += kTmaConsumerWarps) m = absmax_bits<__nv_bfloat16, VEC>(tile[r * 32], m);
+      m = __float_as_uint(bits_to_peak<__nv_bfloat16>(m));
 #pragma unroll
-    for (int i = 0; i < kFqRowsPerWarp; ++i) {
-      const int32_t row = gw + i * kFqGroupWarps;
-      raw[i] = (it >= 0 && row < g.tv) ? tile[row * 32] : make_uint2(0u, 0u);
+      for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+      if (lane == 0) atomicMax(&s_peak[k & 1], m);
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[st]);
-    if (it < 0) break;
-    const int32_t h = it / per_head, r = it - h * per_head;
-    const int32_t kind = first_kind + r / g.M, u = r % g.M;
-    const int z = kind == kFqQ ? 0 : (kind == kFqK ? 1 : 2);
-
-    if (kind == kFqVA) {
-      // per-channel maxima of the tile (4 channels per lane, two packed bf16 maxima per word)
-      uint32_t m01 = 0, m23 = 0;
-#pragma unroll
-      for (int i = 0; i < kFqRowsPerWarp; ++i) {
-        m01 = __vmaxu2(m01, raw[i].x & 0x7FFF7FFFu);
-        m23 = __vmaxu2(m23, raw[i].y & 0x7FFF7FFFu);
-      }
-      s_red[grp][gw][4 * lane + 0] = (m01 & 0xFFFFu) << 16;
-      s_red[grp][gw][4 * lane + 1] = m01 & 0xFFFF0000u;
-      s_red[grp][gw][4 * lane + 2] = (m23 & 0xFFFFu) << 16;
-      s_red[grp][gw][4 * lane + 3] = m23 & 0xFFFF0000u;
-      named_bar_sync(bar_id, bar_n);  // A
-      if (tid == 0) s_count[grp][qp ^ 1] = 0;
-      if (gw == 0) {
-#pragma unroll
-        for (int e = 0; e < VEC; ++e) {
-          const int c = 4 * lane + e;
-          uint32_t mm = s_red[grp][0][c];
-#pragma unroll
-          for (int w = 1; w < kFqGroupWarps; ++w) mm = max(mm, s_red[grp][w][c]);
-          if (mm > 0x7F7FFFFFu && a.err) atomicOr(a.err, 1);
-          atomicMax(a.amax + (int64_t)h * kFqD + c, mm);
-        }
-        __threadfence();  // release the maxima before the count that publishes them
-        __syncwarp();
-        if (lane == 0) atomicAdd(a.done + h, 1);
-      }
-      named_bar_sync(bar_id, bar_n);  // B (s_red is rewritten by the group's next tile)
-      continue;
-    }
-
-    // ---- scales and fast-path brackets
+    named_bar_sync(1, kTmaConsumerWarps * 32);
+    if (threadIdx.x == 0) s_count[(k + 1) & 1] = s_peak[(k + 1) & 1] = 0;
     float pk[VEC];
     Bracket b[VEC];
-    if (z < 2) {
-      uint32_t m = 0;
-      if (!a.given[z]) {
-#pragma unroll
-        for (int i = 0; i < kFqRowsPerWarp; ++i) m = absmax_bits<__nv_bfloat16, VEC>(raw[i], m);
-        m = __float_as_uint(bits_to_peak<__nv_bfloat16>(m));
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
-        if (lane == 0) s_red[grp][gw][0] = m;
-      }
-      named_bar_sync(bar_id, bar_n);  // A
-      float peak;
-      if (a.given[z]) {
-        peak = __ldg(a.given[z] + (int64_t)h * g.M + u);
-      } else {
-        m = s_red[grp][0][0];
-#pragma unroll
-        for (int w = 1; w < kFqGroupWarps; ++w) m = max(m, s_red[grp][w][0]);
-        peak = __uint_as_float(m);
-      }
+    if (!channel) {
+      float peak = __uint_as_float(s_peak[k & 1]);
       if (!(peak <= FLT_MAX)) {
-        if (tid == 0 && a.err) atomicOr(a.err, 1);
+        if (warp == 0 && lane == 0 && a.err) atomicOr(a.err, 1);
         peak = 0.0f;
       }
       const Bracket bb = bracket_f32<FMT>(peak);
@@ -627,93 +540,65 @@ __global__ void __launch_bounds__(kFqThreads, 1)
         pk[e] = peak;
         b[e] = bb;
       }
-      if (tid == 0) a.scales[z][(int64_t)h * g.M + u] = scale_of(peak, kMax);
+      if (warp == 0 && lane == 0) scales[(int64_t)h * g.M + u] = scale_of(peak, kMax);
     } else {
-      if (!a.given[2]) {
-        // VE: wait until every VA item of this head has published its channel maxima
-        if (lane == 0) {
-          const volatile int32_t* dn = a.done + h;
-          while (*dn < g.M) __nanosleep(256);
-        }
-        __syncwarp();
-        __threadfence();  // acquire
-      }
 #pragma unroll
       for (int e = 0; e < VEC; ++e) {
-        const int c = 4 * lane + e;
-        const float peak = a.given[2] ? __ldg(a.given[2] + (int64_t)h * kFqD + c)
-                                      : __uint_as_float(__ldcg(a.amax + (int64_t)h * kFqD + c));
+        const float peak = __uint_as_float(a.amax[(int64_t)h * kTmaD + lane * VEC + e]);
         pk[e] = peak <= FLT_MAX ? peak : 0.0f;
         b[e] = bracket_f32<FMT>(pk[e]);
-        if (u == 0 && gw == 0) a.scales[2][(int64_t)h * kFqD + c] = scale_of(pk[e], kMax);
+        if (u == 0 && warp == 0) scales[(int64_t)h * kTmaD + lane * VEC + e] = scale_of(pk[e], kMax);
       }
-      named_bar_sync(bar_id, bar_n);  // A
     }
-    if (tid == 0) s_count[grp][qp ^ 1] = 0;
     bool fast_ok = true;
 #pragma unroll
     for (int e = 0; e < VEC; ++e) fast_ok &= b[e].ok;
-
-    // ---- fast codes from registers; ambiguous bytes queued as (row, column, bf16 bits)
-    uint8_t* const out_tile = a.codes[z] + ((int64_t)h * g.M + u) * g.pitch * kFqD;
-    uint8_t* const out = out_tile + lane * VEC;
-    uint32_t* count = &s_count[grp][qp];
-    uint32_t* queue = s_queue[grp][qp];
+    uint32_t* count = &s_count[k & 1];
+    uint16_t* queue = s_queue[k & 1];
+#pragma unroll 4
+    for (int32_t r = warp; r < g.tv; r += kTmaConsumerWarps) {
+      float v[VEC];
+      V::unpack(tile[r * 32], v);
+      uint32_t clo = 0, chi = 0;
 #pragma unroll
-    for (int i = 0; i < kFqRowsPerWarp; ++i) {
-      const int32_t row = gw + i * kFqGroupWarps;
-      if (row < g.tv) {
-        float v[VEC];
-        V::unpack(raw[i], v);
-        uint32_t clo = 0, chi = 0;
-#pragma unroll
-        for (int e = 0; e < VEC; e += 2) {
-          float l0, l1, h0, h1;
-          mul2(v[e], v[e + 1], b[e].lo, b[e + 1].lo, l0, l1);
-          mul2(v[e], v[e + 1], b[e].hi, b[e + 1].hi, h0, h1);
-          clo |= cvt_pair<FMT>(l1, l0) << (8 * e);
-          chi |= cvt_pair<FMT>(h1, h0) << (8 * e);
-        }
-        store_codes<VEC>(out + (int64_t)row * kFqD, clo);
-        uint32_t diff = fast_ok ? (clo ^ chi) : 0xFFFFFFFFu;
-        while (diff) {
-          const int e = (__ffs(diff) - 1) >> 3;
-          diff &= ~(0xFFu << (8 * e));
-          const uint32_t slot = atomicAdd(count, 1u);
-          const uint32_t bits = (e & 1) ? ((e < 2 ? raw[i].x : raw[i].y) >> 16) : ((e < 2 ? raw[i].x : raw[i].y) & 0xFFFFu);
-          if (slot < kFqQueueCap) queue[slot] = ((uint32_t)((row << 7) | (lane * VEC + e)) << 16) | bits;
-        }
-      } else if (row < g.pitch) {
-        store_codes<VEC>(out + (int64_t)row * kFqD, 0u);  // padding rows of the tile slot
+      for (int e = 0; e < VEC; e += 2) {
+        float l0, l1, h0, h1;
+        mul2(v[e], v[e + 1], b[e].lo, b[e + 1].lo, l0, l1);
+        mul2(v[e], v[e + 1], b[e].hi, b[e + 1].hi, h0, h1);
+        clo |= cvt_pair<FMT>(l1, l0) << (8 * e);
+        chi |= cvt_pair<FMT>(h1, h0) << (8 * e);
+      }
+      store_codes<VEC>(out + (int64_t)r * kTmaD, clo);
+      uint32_t diff = fast_ok ? (clo ^ chi) : 0xFFFFFFFFu;
+      while (diff) {  // rare: enqueue each ambiguous byte as (row, column)
+        const int e = (__ffs(diff) - 1) >> 3;
+        diff &= ~(0xFFu << (8 * e));
+        const uint32_t slot = atomicAdd(count, 1u);
+        if (slot < kTmaQueueCap) queue[slot] = (uint16_t)((r << 7) | (lane * VEC + e));
       }
     }
-    named_bar_sync(bar_id, bar_n);  // B
+    named_bar_sync(1, kTmaConsumerWarps * 32);
     const uint32_t n = *count;
-    if (n <= kFqQueueCap) {
-      for (uint32_t i = tid; i < n; i += bar_n) {
-        const uint32_t ent = queue[i];
-        const int32_t row = ent >> 23, c = (ent >> 16) & 127;
-        const float xv = __uint_as_float((ent & 0xFFFFu) << 16);
-        float peak = pk[0];
-        if (z == 2) {
-          peak = a.given[2] ? __ldg(a.given[2] + (int64_t)h * kFqD + c)
-                            : __uint_as_float(__ldcg(a.amax + (int64_t)h * kFqD + c));
-          peak = peak <= FLT_MAX ? peak : 0.0f;
-        }
-        out_tile[(int64_t)row * kFqD + c] = (uint8_t)encode_exact<FMT>(xv, scale_of(peak, kMax));
+    if (n <= kTmaQueueCap) {
+      for (uint32_t i = threadIdx.x; i < n; i += kTmaConsumerWarps * 32) {
+        const uint32_t rc = queue[i];
+        const int32_t r = rc >> 7, c = rc & 127;
+        const uint16_t bits = reinterpret_cast<const uint16_t*>(smem + st * kTmaStageBytes)[r * kTmaD + c];
+        const float xv = __uint_as_float((uint32_t)bits << 16);
+        const float peak = channel ? __uint_as_float(a.amax[(int64_t)h * kTmaD + c]) : pk[0];
+        out_tile[(int64_t)r * kTmaD + c] = (uint8_t)encode_exact<FMT>(xv, scale_of(peak <= FLT_MAX ? peak : 0.0f, kMax));
       }
     } else {
-      // queue overflow (adversarial data): exact pass over this warp's rows (unrolled: raw stays in registers)
-#pragma unroll
-      for (int i = 0; i < kFqRowsPerWarp; ++i) {
-        const int32_t row = gw + i * kFqGroupWarps;
-        if (row < g.tv) {
-          float v[VEC];
-          V::unpack(raw[i], v);
-          store_codes<VEC>(out + (int64_t)row * kFqD, encode_slow<FMT, VEC>(v, pk));
-        }
+      // queue overflow (adversarial data): exact pass over the whole tile
+      for (int32_t r = warp; r < g.tv; r += kTmaConsumerWarps) {
+        float v[VEC];
+        V::unpack(tile[r * 32], v);
+        store_codes<VEC>(out + (int64_t)r * kTmaD, encode_slow<FMT, VEC>(v, pk));
       }
     }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[st]);
+    for (int32_t r = g.tv + warp; r < g.pitch; r += kTmaConsumerWarps) store_codes<VEC>(out + (int64_t)r * kTmaD, 0u);
   }
 }
 
@@ -734,9 +619,9 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 bool make_input_map(CUtensorMap* m, const void* x, int64_t L, int32_t heads, int64_t ts, int64_t hs, int32_t sw) {
   auto fn = encode_fn();
   if (!fn) return false;
-  cuuint64_t dims[3] = {(cuuint64_t)kFqD, (cuuint64_t)L, (cuuint64_t)heads};
+  cuuint64_t dims[3] = {(cuuint64_t)kTmaD, (cuuint64_t)L, (cuuint64_t)heads};
   cuuint64_t strides[2] = {(cuuint64_t)ts * 2, (cuuint64_t)(hs > 0 ? hs : ts) * 2};
-  cuuint32_t box[3] = {(cuuint32_t)kFqD, (cuuint32_t)sw, 1};
+  cuuint32_t box[3] = {(cuuint32_t)kTmaD, (cuuint32_t)sw, 1};
   cuuint32_t es[3] = {1, 1, 1};
   return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(x), dims, strides, box, es,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -744,23 +629,22 @@ bool make_input_map(CUtensorMap* m, const void* x, int64_t L, int32_t heads, int
 }
 
 
-// Launch the fused TMA quantiser if the request fits it; returns false to fall back.
-bool try_fused_quant(const void* const* xs, int dtype, int64_t ts, int64_t hs, int32_t heads, const Geometry& g,
-                     int32_t d, int fmt, const FqArgs& a, cudaStream_t st) {
-  if (dtype != FPSA_BF16 || d != kFqD || g.tv > kFqMaxRows || g.sw > 256 || g.tv % g.sw || (ts * 2) % 16 ||
-      (hs * 2) % 16)
+// Launch the TMA quantiser if the request fits it; returns false to fall back.
+bool try_tma_quant(const void* const* xs, int njobs, int dtype, int64_t ts, int64_t hs, int32_t heads,
+                   const Geometry& g, int32_t d, int fmt, const TmaQuantArgs& a, cudaStream_t st) {
+  if (dtype != FPSA_BF16 || d != kTmaD || g.tv > kTmaMaxRows || g.sw > 256 || (ts * 2) % 16 || (hs * 2) % 16)
     return false;
   if (heads > 1 && hs == 0) return false;
   const int64_t L = (int64_t)g.gt * g.gh * g.gw;
   CUtensorMap tm[3];
   for (int i = 0; i < 3; ++i)
-    if (!make_input_map(&tm[i], xs[i], L, heads, ts, hs, g.sw)) return false;
-  const int smem = kFqStages * kFqStageBytes;
-  auto kern = fmt == FPSA_E4M3 ? quant_fused_kernel<FPSA_E4M3> : quant_fused_kernel<FPSA_E5M2>;
-  if (ensure_smem_attr(reinterpret_cast<const void*>(kern), smem, "quant_fused_kernel") != FPSA_OK) return false;
-  const int64_t items = (int64_t)a.kinds * heads * g.M;
+    if (!make_input_map(&tm[i], xs[i < njobs ? i : 0], L, heads, ts, hs, g.sw)) return false;
+  const int smem = kTmaStages * kTmaStageBytes;
+  auto kern = fmt == FPSA_E4M3 ? quant_tma_kernel<FPSA_E4M3> : quant_tma_kernel<FPSA_E5M2>;
+  if (ensure_smem_attr(reinterpret_cast<const void*>(kern), smem, "quant_tma_kernel") != FPSA_OK) return false;
+  const int64_t items = (int64_t)njobs * heads * g.M;
   const int grid = (int)std::min<int64_t>(items, device_sm_count());
-  kern<<<grid, kFqThreads, smem, st>>>(tm[0], tm[1], tm[2], g, a);
+  kern<<<grid, kTmaThreads, smem, st>>>(tm[0], tm[1], tm[2], g, a);
   return true;
 }
 
@@ -894,32 +778,31 @@ int quantize_qkv(const void* q, const void* k, const void* v, int dtype, int64_t
   Geometry g;
   if (int s = make_geometry(grid, tile, d, tile_pitch, in_order, &g)) return s;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  // workspace: v channel amax bits [heads*d], VA-done counters [heads], item counter
+  // workspace: v channel amax bits [heads*d] (+ spare words kept for ABI stability)
   uint32_t* amax = static_cast<uint32_t*>(workspace);
-  int32_t* done = reinterpret_cast<int32_t*>(amax + (int64_t)heads * d);
   if (cudaMemsetAsync(workspace, 0, (size_t)qkv_workspace_words(heads, d) * 4, st) != cudaSuccess)
     return cuda_status(name);
-  static const bool no_fused = getenv("FPSA_QUANT_NO_FUSED") != nullptr;  // measurement switch
-  if (!no_fused) {
-    FqArgs fa{};
-    fa.codes[0] = q_codes; fa.codes[1] = k_codes; fa.codes[2] = v_codes;
-    fa.scales[0] = q_scales; fa.scales[1] = k_scales; fa.scales[2] = v_scales;
-    fa.given[0] = q_amax; fa.given[1] = k_amax; fa.given[2] = v_amax;
-    fa.amax = amax;
-    fa.done = done;
-    fa.claim = done + heads;
-    fa.err = err_flag;
-    fa.heads = heads;
-    fa.kinds = v_amax ? 3 : 4;
-    const void* xs[3] = {q, k, v};
-    if (try_fused_quant(xs, dtype, token_stride, head_stride, heads, g, d, fmt, fa, st)) return cuda_status(name);
-  }
-  // general path (other dtypes / head dims / strides): channel-amax pass, then one grid over all tiles; the
-  // q / k tile maxima are computed (a caller's maxima must equal them), a caller's v maxima are used
-  const uint32_t* vmax = reinterpret_cast<const uint32_t*>(v_amax);  // f32 |x| max bits compare as u32
+  // v channel maxima: the caller's (f32 |x| max bits compare as u32), else one pass over v
+  const uint32_t* vmax = reinterpret_cast<const uint32_t*>(v_amax);
   if (!v_amax) {
     dispatch<RunAmax>(dtype, d, fmt, v, token_stride, head_stride, heads, g, amax, err_flag, st);
     vmax = amax;
+  }
+  (void)q_amax;  // tile maxima are reduced from the tile in shared memory anyway (the caller's must equal them)
+  (void)k_amax;
+  {
+    TmaQuantArgs ta{};
+    ta.codes[0] = q_codes; ta.codes[1] = k_codes; ta.codes[2] = v_codes;
+    ta.scales[0] = q_scales; ta.scales[1] = k_scales; ta.scales[2] = v_scales;
+    ta.channel[2] = 1;
+    ta.njobs = 3;
+    ta.heads = heads;
+    ta.amax = vmax;
+    ta.err = err_flag;
+    const void* xs[3] = {q, k, v};
+    static const bool no_tma = getenv("FPSA_QUANT_NO_TMA") != nullptr;  // measurement switch
+    if (!no_tma && try_tma_quant(xs, 3, dtype, token_stride, head_stride, heads, g, d, fmt, ta, st))
+      return cuda_status(name);
   }
   QuantArgs a{};
   a.job[0] = QuantJob{q, token_stride, head_stride, q_codes, q_scales, 0};
