@@ -42,7 +42,7 @@ typedef enum {
   FPSA_ECAPACITY = 7      /* caller buffer too small */
 } fpsa_status;
 
-typedef enum { FPSA_F32 = 0, FPSA_BF16 = 1, FPSA_F16 = 2 } fpsa_dtype;
+typedef enum { FPSA_F32 = 0, FPSA_BF16 = 1, FPSA_F16 = 2, FPSA_F64 = 3 } fpsa_dtype;
 typedef enum { FPSA_E4M3 = 0, FPSA_E5M2 = 1 } fpsa_fmt;
 typedef enum { FPSA_ORDER_TILE = 0, FPSA_ORDER_NATURAL = 1 } fpsa_order;
 /* Softmax-weight semantics of fpsa_attn_fwd: one-pass (unnormalised weights re-quantised per key block,
@@ -99,14 +99,20 @@ int fpsa_quantize_qk(const void* x, int dtype, int64_t token_stride, int64_t hea
 
 /* Per-channel FP8 quantisation of v: column amax over all L tokens of each
  * head, f64 scale per (head, channel), codes in the same tile-major padded
- * layout as fpsa_quantize_qk.  workspace: device, >= heads*d*4 bytes.
+ * layout as fpsa_quantize_qk.  workspace: device, >= heads*d*8 bytes.
+ *
+ * Both quantisers accept any head dim d >= 1 and f32 / bf16 / f64 input
+ * (the reference quantises any L x d float64 matrix): d in {64, 128} with
+ * f32 / bf16 runs the fast kernels; f64 or other d runs general kernels
+ * that take every element through the exact f64 path (f64 maxima).
  * Replaces quantize_v_channelwise (fp8sta/quantize.py:127-134). */
 int fpsa_quantize_v(const void* x, int dtype, int64_t token_stride, int64_t head_stride, int32_t heads,
                     fpsa_dims3 grid, fpsa_dims3 tile, int32_t d, int32_t tile_pitch, int in_order, int fmt,
                     uint8_t* codes, double* scales, void* workspace, int32_t* err_flag, void* stream);
 
 /* Device workspace bytes of fpsa_quantize_qkv / fpsa_quantize_qkv_amax
- * ((heads*(d+1) + 1) * 4: v channel maxima plus spare words; zeroed by the call). */
+ * ((2*heads*d + heads + 1) * 4: v channel maxima (8-byte on the general
+ * path) plus spare words; zeroed by the call). */
 int fpsa_quantize_workspace_bytes(int32_t heads, int32_t d, int64_t* bytes);
 
 /* Fused form of fpsa_quantize_qk(q) + fpsa_quantize_qk(k) + fpsa_quantize_v(v)
@@ -135,6 +141,25 @@ int fpsa_quantize_qkv_amax(const void* q, const void* k, const void* v, int dtyp
                            const float* k_tile_amax, const float* v_channel_amax, uint8_t* q_codes,
                            uint8_t* k_codes, uint8_t* v_codes, double* q_scales, double* k_scales, double* v_scales,
                            void* workspace, int32_t* err_flag, void* stream);
+
+/* Element codec.  fpsa_encode: codes[i] = RNE(x[i]) (scale == NULL) or
+ * RNE(x[i] / scale[i]) with the quotient in f64 (scale: device f64 [n]),
+ * onto e4m3 / e5m2, saturating finite magnitudes, sign kept on zero;
+ * x dtype f32 / bf16 / f64 (an unscaled f32 is rounded as f32, everything else
+ * through f64).  err_flag (device int32): bit 0 NaN input, bit 1 infinity in
+ * a format without one (E5M2 infinities get the inf code).  Replaces
+ * fp8.encode (fp8sta/fp8.py:153-188) and the division of quantize_dequantize
+ * (:219-234). */
+int fpsa_encode(const void* x, int dtype, const double* scale, int64_t n, int fmt, uint8_t* codes, int32_t* err_flag,
+                void* stream);
+
+/* fpsa_decode: out[i] = value(codes[i]) (* scale[i] in f64 when scale != NULL),
+ * out dtype f32 / f64; a NaN code pattern sets err_flag bit 0.  Replaces
+ * fp8.decode (fp8.py:191-205), QuantizedTensor.dequantize /
+ * dequantize_tensor (quantize.py:95-98, :183-185) and the reconstruction of
+ * quantize_dequantize. */
+int fpsa_decode(const uint8_t* codes, int64_t n, int fmt, const double* scale, void* out, int out_dtype,
+                int32_t* err_flag, void* stream);
 
 /* Work list for fpsa_attn_fwd: one entry per (head, query tile, 128-row
  * query block), tiles with the most key tiles first within each head, the

@@ -23,7 +23,7 @@ FPSA_EUNSUPPORTED = 5
 FPSA_ERANGE = 6
 FPSA_ECAPACITY = 7
 
-F32, BF16, F16 = 0, 1, 2
+F32, BF16, F16, F64 = 0, 1, 2, 3
 E4M3_ID, E5M2_ID = 0, 1
 ORDER_TILE, ORDER_NATURAL = 0, 1
 P_ONEPASS, P_NORMALIZED = 0, 1  # fpsa_p_mode
@@ -63,6 +63,8 @@ SIGNATURES = {
     "fpsa_quantize_qkv_amax": (_c.c_int, [_vp, _vp, _vp, _c.c_int, _i64, _i64, _i32, Dims3, Dims3, _i32, _i32,
                                           _c.c_int, _c.c_int, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                                           _vp]),
+    "fpsa_encode": (_c.c_int, [_vp, _c.c_int, _vp, _i64, _c.c_int, _vp, _vp, _vp]),
+    "fpsa_decode": (_c.c_int, [_vp, _i64, _c.c_int, _vp, _vp, _c.c_int, _vp, _vp]),
     "fpsa_attn_worklist": (_c.c_int, [_i32, Dims3, _i32, _pi32, _pi32, _i64, _pi64]),
     "fpsa_attn_workspace_bytes": (_c.c_int, [_i32, _pi64]),
     "fpsa_attn_fwd": (_c.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _i32, Dims3, Dims3, _i32, _i32, _vp, _vp, _vp, _i32,

@@ -67,12 +67,14 @@ __device__ __forceinline__ int32_t local_offset(const Geometry& g, int32_t r) {
 constexpr int kMaxTableRows = 2048;
 __device__ __forceinline__ void build_row_table(const Geometry& g, int64_t token_stride, int64_t* table) {
   if (g.natural)
-    for (int32_t r = threadIdx.x; r < g.tv; r += blockDim.x) table[r] = (int64_t)local_offset(g, r) * token_stride;
+    for (int32_t r = threadIdx.x; r < min(g.tv, kMaxTableRows); r += blockDim.x)
+      table[r] = (int64_t)local_offset(g, r) * token_stride;
   __syncthreads();
 }
-// Element offset of local row r from the tile's first token.
+// Element offset of local row r from the tile's first token (tiles above kMaxTableRows tokens: computed).
 __device__ __forceinline__ int64_t row_offset(const Geometry& g, const int64_t* table, int32_t r, int64_t ts) {
-  return g.natural ? table[r] : (int64_t)r * ts;
+  if (!g.natural) return (int64_t)r * ts;
+  return r < kMaxTableRows ? table[r] : (int64_t)local_offset(g, r) * ts;
 }
 
 // Raw vector of VEC consecutive channels (16-bit inputs stay packed in registers).
@@ -418,6 +420,105 @@ __global__ void __launch_bounds__(kQuantThreads)
 }
 
 // ---------------------------------------------------------------------------
+// General quantisers: any head dim, f32 / bf16 / f64 input, every element
+// through the exact path (f64 quotient -> round-to-odd f32 -> RNE cvt), f64
+// maxima.  The reference's standalone quantize_qk_tilewise /
+// quantize_v_channelwise accept any L x d float64 matrix (quantize.py:111-134);
+// these kernels serve the requests the fast kernels do not (d not in {64,128},
+// f64 data), off the attention hot path.
+template <typename T>
+__device__ __forceinline__ double load_elem(const T* p) {
+  if constexpr (sizeof(T) == 2) return (double)__uint_as_float((uint32_t)__ldg(reinterpret_cast<const unsigned short*>(p)) << 16);
+  else return (double)__ldg(p);
+}
+template <int FMT>
+__device__ __forceinline__ uint32_t encode_exact_d(double x, double s) {
+  const double q = __ddiv_rn(x, s);
+  float f = __double2float_rz(q);
+  if ((double)f != q) f = __uint_as_float(__float_as_uint(f) | 1u);  // round to odd
+  return cvt_pair<FMT>(0.0f, f) & 0xFFu;
+}
+__device__ __forceinline__ double scale_of_d(double peak, double maxv) {
+  if (peak == 0.0) return 1.0;
+  const double s = __ddiv_rn(peak, maxv);
+  return s > DBL_MIN ? s : DBL_MIN;
+}
+constexpr int kGenThreads = 256;
+
+// one CTA per (tile, head): f64 tile max -> scale -> exact codes; padding rows zero
+template <typename T, int FMT>
+__global__ void __launch_bounds__(kGenThreads) quant_tile_generic_kernel(const T* x, int64_t ts, int64_t hs, Geometry g,
+                                                                          int32_t d, uint8_t* codes, double* scales,
+                                                                          int32_t* err) {
+  constexpr double kMax = FMT == FPSA_E4M3 ? 448.0 : 57344.0;
+  __shared__ unsigned long long s_max;
+  const int32_t u = blockIdx.x, h = blockIdx.y;
+  const T* xt = x + (int64_t)h * hs + (int64_t)tile_base(g, u) * ts;
+  auto off = [&](int32_t r) { return g.natural ? (int64_t)local_offset(g, r) * ts : (int64_t)r * ts; };
+  if (threadIdx.x == 0) s_max = 0ull;
+  __syncthreads();
+  unsigned long long m = 0ull;  // |x| bits: non-negative doubles order as integers, NaN / inf above all
+  const int64_t n = (int64_t)g.tv * d;
+  for (int64_t i = threadIdx.x; i < n; i += kGenThreads) {
+    const double v = load_elem(xt + off((int32_t)(i / d)) + i % d);
+    m = max(m, (unsigned long long)__double_as_longlong(fabs(v)));
+  }
+  atomicMax(&s_max, m);
+  __syncthreads();
+  double peak = __longlong_as_double((long long)s_max);
+  if (!(peak <= DBL_MAX)) {
+    if (threadIdx.x == 0 && err) atomicOr(err, 1);
+    peak = 0.0;
+  }
+  const double sc = scale_of_d(peak, kMax);
+  if (threadIdx.x == 0) scales[(int64_t)h * g.M + u] = sc;
+  uint8_t* out = codes + ((int64_t)h * g.M + u) * g.pitch * d;
+  for (int64_t i = threadIdx.x; i < (int64_t)g.pitch * d; i += kGenThreads) {
+    const int32_t r = (int32_t)(i / d);
+    out[i] = r < g.tv ? (uint8_t)encode_exact_d<FMT>(load_elem(xt + off(r) + i % d), sc) : (uint8_t)0;
+  }
+}
+
+// v: per-(head, channel) f64 |x| max over all tokens (atomicMax on the bits)
+template <typename T>
+__global__ void __launch_bounds__(kGenThreads) chan_amax_generic_kernel(const T* x, int64_t ts, int64_t hs, int64_t L,
+                                                                         int32_t d, unsigned long long* amax) {
+  const int32_t h = blockIdx.y;
+  const int64_t n = L * d;
+  for (int64_t i = (int64_t)blockIdx.x * kGenThreads + threadIdx.x; i < n; i += (int64_t)gridDim.x * kGenThreads) {
+    const double v = load_elem(x + (int64_t)h * hs + (i / d) * ts + i % d);
+    atomicMax(amax + (int64_t)h * d + i % d, (unsigned long long)__double_as_longlong(fabs(v)));
+  }
+}
+
+// v codes with the channel scales, in the tile-major padded layout; one CTA per (tile, head)
+template <typename T, int FMT>
+__global__ void __launch_bounds__(kGenThreads) quant_chan_generic_kernel(const T* x, int64_t ts, int64_t hs, Geometry g,
+                                                                          int32_t d, const unsigned long long* amax,
+                                                                          uint8_t* codes, double* scales,
+                                                                          int32_t* err) {
+  constexpr double kMax = FMT == FPSA_E4M3 ? 448.0 : 57344.0;
+  const int32_t u = blockIdx.x, h = blockIdx.y;
+  const T* xt = x + (int64_t)h * hs + (int64_t)tile_base(g, u) * ts;
+  auto off = [&](int32_t r) { return g.natural ? (int64_t)local_offset(g, r) * ts : (int64_t)r * ts; };
+  auto scale_c = [&](int32_t c) {
+    double peak = __longlong_as_double((long long)amax[(int64_t)h * d + c]);
+    return scale_of_d(peak <= DBL_MAX ? peak : 0.0, kMax);
+  };
+  if (u == 0)
+    for (int32_t c = threadIdx.x; c < d; c += kGenThreads) {
+      const double peak = __longlong_as_double((long long)amax[(int64_t)h * d + c]);
+      if (!(peak <= DBL_MAX) && err) atomicOr(err, 1);
+      scales[(int64_t)h * d + c] = scale_c(c);
+    }
+  uint8_t* out = codes + ((int64_t)h * g.M + u) * g.pitch * d;
+  for (int64_t i = threadIdx.x; i < (int64_t)g.pitch * d; i += kGenThreads) {
+    const int32_t r = (int32_t)(i / d), c = (int32_t)(i % d);
+    out[i] = r < g.tv ? (uint8_t)encode_exact_d<FMT>(load_elem(xt + off(r) + c), scale_c(c)) : (uint8_t)0;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // TMA-fed persistent quantiser (bf16 input, d = 128, tile volume <= 256).
 //
 // One CTA per SM loops over (tensor, head, tile) items.  A producer warp
@@ -651,11 +752,9 @@ bool try_tma_quant(const void* const* xs, int njobs, int dtype, int64_t ts, int6
 int make_geometry(fpsa_dims3 grid, fpsa_dims3 tile, int32_t d, int32_t pitch, int in_order, Geometry* g) {
   fpsa_dims3 td;
   if (int st = fpsa_tile_grid(grid, tile, &td)) return st;
-  if (d != 64 && d != 128) return fail(FPSA_EUNSUPPORTED, "head dim must be 64 or 128, got " + std::to_string(d));
+  if (d < 1) return fail(FPSA_EINVAL, "head dim must be >= 1, got " + std::to_string(d));
   const int32_t tv = tile.t * tile.h * tile.w;
   if (pitch < tv) return fail(FPSA_EINVAL, "tile_pitch smaller than the tile volume");
-  if (in_order == FPSA_ORDER_NATURAL && tv > kMaxTableRows)
-    return fail(FPSA_EUNSUPPORTED, "tile volume above " + std::to_string(kMaxTableRows) + " tokens");
   if (in_order != FPSA_ORDER_TILE && in_order != FPSA_ORDER_NATURAL) return fail(FPSA_EINVAL, "bad token order");
   *g = Geometry{grid.t, grid.h, grid.w, tile.t, tile.h, tile.w, td.t, td.h, td.w,
                 tv,     td.t * td.h * td.w, pitch, in_order == FPSA_ORDER_NATURAL};
@@ -665,7 +764,8 @@ int make_geometry(fpsa_dims3 grid, fpsa_dims3 tile, int32_t d, int32_t pitch, in
 int check_common(const void* x, int dtype, int32_t heads, int fmt, const void* codes, const void* scales) {
   if (!x || !codes || !scales) return fail(FPSA_EINVAL, "null buffer");
   if (heads < 1) return fail(FPSA_EINVAL, "heads must be >= 1");
-  if (dtype != FPSA_F32 && dtype != FPSA_BF16) return fail(FPSA_EUNSUPPORTED, "input dtype must be f32 or bf16");
+  if (dtype != FPSA_F32 && dtype != FPSA_BF16 && dtype != FPSA_F64)
+    return fail(FPSA_EUNSUPPORTED, "input dtype must be f32, bf16 or f64");
   if (fmt != FPSA_E4M3 && fmt != FPSA_E5M2) return fail(FPSA_EINVAL, "fmt must be e4m3 or e5m2");
   return FPSA_OK;
 }
@@ -722,6 +822,46 @@ struct RunAmax {
   }
 };
 
+// the general (exact, any d, f64) quantisers; true when the request needs them
+bool needs_general(int dtype, int32_t d) { return dtype == FPSA_F64 || (d != 64 && d != 128); }
+
+template <typename T, int FMT>
+void launch_general_tile(const void* x, int64_t ts, int64_t hs, int32_t heads, const Geometry& g, int32_t d,
+                         uint8_t* codes, double* scales, int32_t* err, cudaStream_t st) {
+  quant_tile_generic_kernel<T, FMT><<<dim3(g.M, heads), kGenThreads, 0, st>>>(static_cast<const T*>(x), ts, hs, g, d,
+                                                                              codes, scales, err);
+}
+template <typename T, int FMT>
+void launch_general_chan(const void* x, int64_t ts, int64_t hs, int32_t heads, const Geometry& g, int32_t d,
+                         unsigned long long* amax, uint8_t* codes, double* scales, int32_t* err, cudaStream_t st) {
+  const int64_t L = (int64_t)g.gt * g.gh * g.gw;
+  const int64_t blocks = std::min<int64_t>((L * d + kGenThreads - 1) / kGenThreads, 4096);
+  chan_amax_generic_kernel<T><<<dim3((unsigned)blocks, heads), kGenThreads, 0, st>>>(static_cast<const T*>(x), ts, hs, L,
+                                                                                      d, amax);
+  quant_chan_generic_kernel<T, FMT><<<dim3(g.M, heads), kGenThreads, 0, st>>>(static_cast<const T*>(x), ts, hs, g, d,
+                                                                              amax, codes, scales, err);
+}
+template <template <typename, int> class F, typename... Args>
+void dispatch_general(int dtype, int fmt, Args&&... args) {
+  if (dtype == FPSA_F64) {
+    if (fmt == FPSA_E4M3) F<double, FPSA_E4M3>::run(args...); else F<double, FPSA_E5M2>::run(args...);
+  } else if (dtype == FPSA_F32) {
+    if (fmt == FPSA_E4M3) F<float, FPSA_E4M3>::run(args...); else F<float, FPSA_E5M2>::run(args...);
+  } else {
+    if (fmt == FPSA_E4M3) F<__nv_bfloat16, FPSA_E4M3>::run(args...); else F<__nv_bfloat16, FPSA_E5M2>::run(args...);
+  }
+}
+template <typename T, int FMT>
+struct RunGeneralTile {
+  template <typename... A>
+  static void run(A... a) { launch_general_tile<T, FMT>(a...); }
+};
+template <typename T, int FMT>
+struct RunGeneralChan {
+  template <typename... A>
+  static void run(A... a) { launch_general_chan<T, FMT>(a...); }
+};
+
 }  // namespace
 }  // namespace fpsa
 
@@ -734,6 +874,11 @@ extern "C" int fpsa_quantize_qk(const void* x, int dtype, int64_t token_stride, 
   if (int s = check_common(x, dtype, heads, fmt, codes, scales)) return s;
   Geometry g;
   if (int s = make_geometry(grid, tile, d, tile_pitch, in_order, &g)) return s;
+  if (needs_general(dtype, d)) {
+    dispatch_general<RunGeneralTile>(dtype, fmt, x, token_stride, head_stride, heads, g, d, codes, scales, err_flag,
+                                     static_cast<cudaStream_t>(stream));
+    return cuda_status("fpsa_quantize_qk");
+  }
   QuantArgs a{};
   a.job[0] = QuantJob{x, token_stride, head_stride, codes, scales, 0};
   a.err = err_flag;
@@ -750,6 +895,13 @@ extern "C" int fpsa_quantize_v(const void* x, int dtype, int64_t token_stride, i
   Geometry g;
   if (int s = make_geometry(grid, tile, d, tile_pitch, in_order, &g)) return s;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (needs_general(dtype, d)) {  // f64 channel maxima: workspace >= heads*d*8 bytes
+    auto* amax64 = static_cast<unsigned long long*>(workspace);
+    if (cudaMemsetAsync(amax64, 0, (size_t)heads * d * 8, st) != cudaSuccess) return cuda_status("fpsa_quantize_v memset");
+    dispatch_general<RunGeneralChan>(dtype, fmt, x, token_stride, head_stride, heads, g, d, amax64, codes, scales,
+                                     err_flag, st);
+    return cuda_status("fpsa_quantize_v");
+  }
   uint32_t* amax = static_cast<uint32_t*>(workspace);
   if (cudaMemsetAsync(amax, 0, (size_t)heads * d * sizeof(uint32_t), st) != cudaSuccess)
     return cuda_status("fpsa_quantize_v memset");
@@ -764,7 +916,8 @@ extern "C" int fpsa_quantize_v(const void* x, int dtype, int64_t token_stride, i
 
 namespace fpsa {
 namespace {
-int64_t qkv_workspace_words(int32_t heads, int32_t d) { return (int64_t)heads * (d + 1) + 1; }
+// v channel maxima: 4-byte words on the fast paths, 8-byte on the general (f64 / any d) path
+int64_t qkv_workspace_words(int32_t heads, int32_t d) { return 2 * (int64_t)heads * d + heads + 1; }
 
 int quantize_qkv(const void* q, const void* k, const void* v, int dtype, int64_t token_stride, int64_t head_stride,
                  int32_t heads, fpsa_dims3 grid, fpsa_dims3 tile, int32_t d, int32_t tile_pitch, int in_order,
@@ -778,7 +931,18 @@ int quantize_qkv(const void* q, const void* k, const void* v, int dtype, int64_t
   Geometry g;
   if (int s = make_geometry(grid, tile, d, tile_pitch, in_order, &g)) return s;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  // workspace: v channel amax bits [heads*d] (+ spare words kept for ABI stability)
+  if (needs_general(dtype, d)) {
+    auto* amax64 = static_cast<unsigned long long*>(workspace);
+    if (cudaMemsetAsync(amax64, 0, (size_t)heads * d * 8, st) != cudaSuccess) return cuda_status(name);
+    dispatch_general<RunGeneralTile>(dtype, fmt, q, token_stride, head_stride, heads, g, d, q_codes, q_scales,
+                                     err_flag, st);
+    dispatch_general<RunGeneralTile>(dtype, fmt, k, token_stride, head_stride, heads, g, d, k_codes, k_scales,
+                                     err_flag, st);
+    dispatch_general<RunGeneralChan>(dtype, fmt, v, token_stride, head_stride, heads, g, d, amax64, v_codes, v_scales,
+                                     err_flag, st);
+    return cuda_status(name);
+  }
+  // workspace: v channel amax bits [heads*d] (+ spare words)
   uint32_t* amax = static_cast<uint32_t*>(workspace);
   if (cudaMemsetAsync(workspace, 0, (size_t)qkv_workspace_words(heads, d) * 4, st) != cudaSuccess)
     return cuda_status(name);
@@ -844,4 +1008,114 @@ extern "C" int fpsa_quantize_qkv_amax(const void* q, const void* k, const void* 
   return quantize_qkv(q, k, v, dtype, token_stride, head_stride, heads, grid, tile, d, tile_pitch, in_order, fmt,
                       q_codes, k_codes, v_codes, q_scales, k_scales, v_scales, q_tile_amax, k_tile_amax,
                       v_channel_amax, workspace, err_flag, stream, "fpsa_quantize_qkv_amax");
+}
+
+// ---------------------------------------------------------------------------
+// Element codec (fp8.encode / fp8.decode / quantize_dequantize, fp8.py:153-234)
+namespace fpsa {
+namespace {
+constexpr int kCodecThreads = 256;
+
+// RNE of x (or of the f64 quotient x / scale) onto the format: f32 without a scale rounds the f32 value
+// directly (the reference's bounds32 path), everything else goes through f64 (bounds64).  NaN -> err bit 0;
+// infinity -> the inf code (E5M2) or err bit 1 (E4M3); finite magnitudes above max_value saturate.
+template <typename T, int FMT>
+__global__ void __launch_bounds__(kCodecThreads) encode_kernel(const T* x, const double* scale, int64_t n,
+                                                               uint8_t* codes, int32_t* err) {
+  for (int64_t i = (int64_t)blockIdx.x * kCodecThreads + threadIdx.x; i < n; i += (int64_t)gridDim.x * kCodecThreads) {
+    const double v = load_elem(x + i);
+    uint32_t c;
+    if (isnan(v)) {
+      atomicOr(err, 1);
+      c = 0;
+    } else if (isinf(v)) {
+      if (FMT == FPSA_E5M2) c = signbit(v) ? 0xFCu : 0x7Cu;
+      else {
+        atomicOr(err, 2);
+        c = 0;
+      }
+    } else if (scale) {
+      c = encode_exact_d<FMT>(v, scale[i]);
+    } else if (sizeof(T) <= 4) {
+      c = cvt_pair<FMT>(0.0f, (float)v) & 0xFFu;  // f32 / bf16 value: exactly an f32
+    } else {
+      c = encode_exact_d<FMT>(v, 1.0);
+    }
+    codes[i] = (uint8_t)c;
+  }
+}
+
+// value(code) [* scale in f64]; a NaN pattern sets err bit 0 (the reference raises)
+template <int FMT, typename O>
+__global__ void __launch_bounds__(kCodecThreads) decode_kernel(const uint8_t* codes, const double* scale, int64_t n,
+                                                               O* out, int32_t* err) {
+  for (int64_t i = (int64_t)blockIdx.x * kCodecThreads + threadIdx.x; i < n; i += (int64_t)gridDim.x * kCodecThreads) {
+    const uint32_t c = codes[i];
+    const uint32_t e = FMT == FPSA_E4M3 ? (c >> 3) & 0xF : (c >> 2) & 0x1F;
+    const uint32_t m = FMT == FPSA_E4M3 ? c & 7 : c & 3;
+    constexpr int kMb = FMT == FPSA_E4M3 ? 3 : 2, kBias = FMT == FPSA_E4M3 ? 7 : 15, kTop = FMT == FPSA_E4M3 ? 15 : 31;
+    double mag;
+    bool nan = false;
+    if (e == 0) mag = ldexp((double)m, 1 - kBias - kMb);
+    else mag = ldexp((double)(m + (1u << kMb)), (int)e - kBias - kMb);
+    if (FMT == FPSA_E4M3 && e == kTop && m == 7) nan = true;
+    if (FMT == FPSA_E5M2 && e == kTop) {
+      if (m == 0) mag = INFINITY;
+      else nan = true;
+    }
+    if (nan) {
+      atomicOr(err, 1);
+      mag = NAN;
+    }
+    double val = (c & 0x80) ? -mag : mag;
+    if (scale) val *= scale[i];
+    out[i] = (O)val;
+  }
+}
+
+template <typename T>
+void launch_encode(const void* x, const double* scale, int64_t n, int fmt, uint8_t* codes, int32_t* err,
+                   cudaStream_t st) {
+  const int blocks = (int)std::min<int64_t>((n + kCodecThreads - 1) / kCodecThreads, device_sm_count() * 8);
+  if (fmt == FPSA_E4M3)
+    encode_kernel<T, FPSA_E4M3><<<blocks, kCodecThreads, 0, st>>>(static_cast<const T*>(x), scale, n, codes, err);
+  else
+    encode_kernel<T, FPSA_E5M2><<<blocks, kCodecThreads, 0, st>>>(static_cast<const T*>(x), scale, n, codes, err);
+}
+}  // namespace
+}  // namespace fpsa
+
+extern "C" int fpsa_encode(const void* x, int dtype, const double* scale, int64_t n, int fmt, uint8_t* codes,
+                           int32_t* err_flag, void* stream) {
+  clear_error();
+  if (n < 0) return fail(FPSA_EINVAL, "n must be >= 0");
+  if (n == 0) return FPSA_OK;
+  if (!x || !codes || !err_flag) return fail(FPSA_EINVAL, "null buffer");
+  if (fmt != FPSA_E4M3 && fmt != FPSA_E5M2) return fail(FPSA_EINVAL, "fmt must be e4m3 or e5m2");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (dtype == FPSA_F32) launch_encode<float>(x, scale, n, fmt, codes, err_flag, st);
+  else if (dtype == FPSA_F64) launch_encode<double>(x, scale, n, fmt, codes, err_flag, st);
+  else if (dtype == FPSA_BF16) launch_encode<__nv_bfloat16>(x, scale, n, fmt, codes, err_flag, st);
+  else return fail(FPSA_EUNSUPPORTED, "input dtype must be f32, bf16 or f64");
+  return cuda_status("fpsa_encode");
+}
+
+extern "C" int fpsa_decode(const uint8_t* codes, int64_t n, int fmt, const double* scale, void* out, int out_dtype,
+                           int32_t* err_flag, void* stream) {
+  clear_error();
+  if (n < 0) return fail(FPSA_EINVAL, "n must be >= 0");
+  if (n == 0) return FPSA_OK;
+  if (!codes || !out || !err_flag) return fail(FPSA_EINVAL, "null buffer");
+  if (fmt != FPSA_E4M3 && fmt != FPSA_E5M2) return fail(FPSA_EINVAL, "fmt must be e4m3 or e5m2");
+  if (out_dtype != FPSA_F32 && out_dtype != FPSA_F64) return fail(FPSA_EUNSUPPORTED, "out dtype must be f32 or f64");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int blocks = (int)std::min<int64_t>((n + kCodecThreads - 1) / kCodecThreads, device_sm_count() * 8);
+#define FPSA_DEC(F_, O_) decode_kernel<F_, O_><<<blocks, kCodecThreads, 0, st>>>(codes, scale, n, static_cast<O_*>(out), err_flag)
+  if (fmt == FPSA_E4M3) {
+    if (out_dtype == FPSA_F32) FPSA_DEC(FPSA_E4M3, float); else FPSA_DEC(FPSA_E4M3, double);
+  } else {
+    if (out_dtype == FPSA_F32) FPSA_DEC(FPSA_E5M2, float); else FPSA_DEC(FPSA_E5M2, double);
+  }
+#undef FPSA_DEC
+  return cuda_status("fpsa_decode");
 }

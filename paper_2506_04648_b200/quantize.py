@@ -3,7 +3,10 @@
 ``quantize_qk_tilewise`` and ``quantize_v_channelwise`` run the sm_100a
 kernels of libfpsa and return the reference's ``QuantizedTensor``: uint8
 codes in the input row order and float64 scales, bit-identical to the
-reference (fp8sta/quantize.py:111-134).
+reference (fp8sta/quantize.py:111-134) for f32, bf16 and f64 input of any
+width d (f64 data is quantised in f64, as the reference does; d other than
+64 / 128 and f64 run the general exact kernels).  ``dequantize`` /
+``dequantize_tensor`` reconstruct decode(code) * scale in float64 on the GPU.
 """
 
 from __future__ import annotations
@@ -52,27 +55,27 @@ class QuantizedTensor:
         if kind == "per_channel":
             return self.scales[None, :]
         if kind == "per_tile_3d":
-            return np.repeat(self.scales, self.block_rows)[:, None]
+            s = self.scales.cpu().numpy() if hasattr(self.scales, "cpu") else self.scales
+            return np.repeat(s, self.block_rows)[:, None]
         raise NotImplementedError(f"{kind} is a comparison granularity outside the hot path")
 
-    def dequantize(self) -> np.ndarray:
-        """decode(code) * scale in float64."""
-        return _code_table(self.fmt)[self.codes] * self.element_scales()
+    def dequantize(self):
+        """decode(code) * scale in float64 (quantize.py:95-98), on the GPU (fpsa_decode).  numpy codes give
+        numpy, CUDA codes a CUDA tensor."""
+        import torch
+
+        from .fp8 import _decode_dev, _scale_arg
+
+        host = not isinstance(self.codes, torch.Tensor)
+        codes = torch.from_numpy(np.ascontiguousarray(self.codes)) if host else self.codes
+        shape = tuple(codes.shape)
+        codes = codes.reshape(-1).contiguous().cuda()
+        es = self.element_scales()
+        scales = _scale_arg(es.cpu() if isinstance(es, torch.Tensor) else es, shape, codes.device)
+        out = _decode_dev(codes, self.fmt, torch.float64, scales).reshape(shape)
+        return out.cpu().numpy() if host else out
 
 
-def _code_table(fmt: Fp8Format) -> np.ndarray:
-    codes = np.arange(256)
-    mb, eb = fmt.mantissa_bits, fmt.exponent_bits
-    e = (codes >> mb) & ((1 << eb) - 1)
-    m = codes & ((1 << mb) - 1)
-    mag = np.where(e == 0, np.ldexp(m.astype(np.float64), 1 - fmt.exponent_bias - mb),
-                   np.ldexp((m + (1 << mb)).astype(np.float64), e - fmt.exponent_bias - mb))
-    top = (1 << eb) - 1
-    if fmt.has_inf:
-        mag = np.where(e == top, np.where(m == 0, np.inf, np.nan), mag)
-    else:
-        mag = np.where((e == top) & (m == (1 << mb) - 1), np.nan, mag)
-    return np.where(codes & 0x80, -mag, mag)
 
 
 def _device_matrix(matrix):
@@ -81,12 +84,12 @@ def _device_matrix(matrix):
 
     if isinstance(matrix, torch.Tensor):
         x = matrix
-        if x.dtype not in (torch.float32, torch.bfloat16):
-            x = x.float()
+        if x.dtype not in (torch.float32, torch.bfloat16, torch.float64):
+            x = x.double()
         return x.contiguous().cuda(), False
     arr = np.asarray(matrix)
     if arr.dtype != np.float32:
-        arr = arr.astype(np.float32)  # f64 inputs: see DESIGN.md (codes exact for f32-representable data)
+        arr = arr.astype(np.float64)  # the reference quantises in float64 (quantize.py:115, :128)
     return torch.from_numpy(np.ascontiguousarray(arr)).cuda(), True
 
 
@@ -101,7 +104,7 @@ def _run(kind: str, matrix, grid, tile, fmt: Fp8Format, n_scales: int):
     scales = torch.empty(n_scales, dtype=torch.float64, device=x.device)
     err = torch.zeros(1, dtype=torch.int32, device=x.device)
     st = torch.cuda.current_stream().cuda_stream
-    dt = _lib.F32 if x.dtype == torch.float32 else _lib.BF16
+    dt = {torch.float32: _lib.F32, torch.bfloat16: _lib.BF16, torch.float64: _lib.F64}[x.dtype]
     L = _lib.lib()
     tv = tile[0] * tile[1] * tile[2]
     if kind == "qk":
@@ -109,7 +112,7 @@ def _run(kind: str, matrix, grid, tile, fmt: Fp8Format, n_scales: int):
                                       _lib.ORDER_TILE, fmt.abi_id, codes.data_ptr(), scales.data_ptr(),
                                       err.data_ptr(), st))
     else:
-        ws = torch.empty(d, dtype=torch.int32, device=x.device)
+        ws = torch.empty(2 * d, dtype=torch.int32, device=x.device)  # f64 channel maxima on the general path
         _lib.check(L.fpsa_quantize_v(x.data_ptr(), dt, d, 0, 1, _lib.dims3(grid), _lib.dims3(tile), d, tv,
                                      _lib.ORDER_TILE, fmt.abi_id, codes.data_ptr(), scales.data_ptr(),
                                      ws.data_ptr(), err.data_ptr(), st))
@@ -138,3 +141,8 @@ def quantize_v_channelwise(matrix, fmt: Fp8Format) -> QuantizedTensor:
     R, d = shape
     codes, scales = _run("v", matrix, (1, 1, R), (1, 1, R), fmt, d)
     return QuantizedTensor(codes, scales, Granularity("per_channel"), fmt)
+
+
+def dequantize_tensor(q: QuantizedTensor):
+    """Elementwise decode(code) * scale(block) (quantize.py:183-185)."""
+    return q.dequantize()
