@@ -57,14 +57,14 @@ class ScheduleRunner:
 
     def __init__(self, grid: tuple[int, int, int], schedule: ScheduleConfig, heads: int, d: int,
                  fmt: Fp8Format = E4M3, device="cuda", use_graphs: bool = True, tau: float = 8.0,
-                 fidelity: bool = False):
+                 fidelity: bool = False, p_mode: str = "onepass"):
         problems = validate(schedule)
         if problems:
             raise ValueError("invalid schedule: " + "; ".join(problems))
         self.grid = tuple(int(x) for x in grid)
         self.schedule, self.heads, self.d = schedule, int(heads), int(d)
         self.fmt, self.device, self.use_graphs, self.tau = fmt, device, use_graphs, tau
-        self.fidelity = fidelity
+        self.fidelity, self.p_mode = fidelity, p_mode
         self._plans: dict = {}
         self._ref_plans: dict = {}
         self._ref_out = None
@@ -78,7 +78,7 @@ class ScheduleRunner:
         if p is None:
             rp = self.schedule.params(regime)
             p = FpsaPlan(self.grid, rp.tile.dims, rp.window, self.heads, self.d, self.fmt, device=self.device,
-                         tau=self.tau)
+                         tau=self.tau, p_mode=self.p_mode)
             self._plans[regime] = p
         return p
 

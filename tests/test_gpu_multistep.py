@@ -93,3 +93,52 @@ def test_host_streamer_matches_plan(fpsa):
         assert torch.equal(oh, ref.cpu())
     with pytest.raises(ValueError):
         streamer(q, k, v, oh)  # device tensors are rejected
+
+
+def _oracle_head(fpsa, grid, tile, win, x_nat, h):
+    """Oracle output of head h, natural-order [L, H, d] bf16 inputs -> natural order f32."""
+    import oracle as O
+
+    perm = O.tile_perm(grid, tile)
+    tv = tile[0] * tile[1] * tile[2]
+    q, k, v = (x[:, h, :].float().cpu().numpy()[perm] for x in x_nat)
+    offs, ids = O.window_lists(O.tile_grid_dims(grid, tile), win)
+    ref, _ = O.fp8_sparse_forward(q, k, v, tv, offs, ids)
+    out = np.empty_like(ref)
+    out[perm] = ref
+    return out
+
+
+@pytest.mark.parametrize("which", ["c4", "default"])
+def test_schedule_runner_regimes_vs_oracle(fpsa, which):
+    """One step of every regime through ScheduleRunner (CUDA graphs) against the oracle of that step's
+    (tile, window) (experiment.py:178-201, schedule.py:71-73): the BASELINE C4 schedule at the 14B 720p grid,
+    and the reference's own default_schedule (schedule.py:58-64: 24576-, 384- and 3072-token tiles) on a grid
+    its tiles divide."""
+    import oracle as O
+
+    if which == "c4":
+        grid, d, sc = (21, 45, 80), 128, fpsa.c4_schedule(50)
+    else:
+        grid, d, sc = (24, 32, 32), 64, fpsa.default_schedule(50)
+    H = 1
+    L = grid[0] * grid[1] * grid[2]
+    g = torch.Generator(device="cuda").manual_seed(4)
+    x = [torch.randn((L, H, d), generator=g, device="cuda").to(torch.bfloat16) for _ in range(3)]
+    runner = fpsa.ScheduleRunner(grid, sc, H, d, use_graphs=True)
+    seen = set()
+    for t in range(1, sc.total_steps + 1):
+        regime = sc.regime_of(t)
+        if regime in seen:
+            continue
+        seen.add(regime)
+        out = torch.empty_like(x[0])
+        assert runner.step(t, *x, out) == regime
+        torch.cuda.synchronize()
+        rp = fpsa.params_at(t, sc)
+        ref = _oracle_head(fpsa, grid, rp.tile.dims, rp.window.dims, x, 0)
+        got = out[:, 0].float().cpu().numpy()
+        cos, mabs = O.cosine(got, ref), O.max_abs(got, ref)
+        print(f"{which} t={t} {regime} tile {rp.tile.dims} window {rp.window.dims}: cos={cos:.6f} max-abs={mabs:.3e}")
+        assert cos >= 0.999 and mabs <= 2e-2
+    assert seen == {"early", "mid", "late"}
