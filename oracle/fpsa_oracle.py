@@ -24,7 +24,7 @@ __all__ = [
     "axis_interval", "window_lists", "density_of", "flops_sparse_of",
     "regime_of", "schedule_valid",
     "fp8_sparse_forward", "sparse_forward_f32", "onepass_forward", "bf16_round", "passthrough_emulation",
-    "normalized_rows", "p_flip_budget",
+    "normalized_rows", "p_flip_budget", "packed_keys",
     "cosine", "max_abs", "gen_inputs",
 ]
 
@@ -412,8 +412,14 @@ def _exp2_poly(x: np.ndarray) -> np.ndarray:
     return np.ldexp(y, j.astype(np.int64))
 
 
+def packed_keys(tv: int) -> bool:
+    """Whether the kernel runs packed key blocks for tile volume tv (fpsa_attn.cu fpsa_attn_fwd: 128
+    consecutive keys of the concatenated window tiles per block, no padding keys)."""
+    return tv % 16 == 0 and tv > 128 and tv % 128 != 0
+
+
 def onepass_forward(codes: dict, tv, offs, ids, fmt: Fmt = E4M3, softmax_scale=None, block=128, tau=0.0,
-                    poly=False, return_redo=False):
+                    poly=False, return_redo=False, packed=None):
     """Emulation of the GPU kernel's schedule (NOT the reference semantics).
 
     Work item = 128 query rows of a tile.  Keys are visited per key tile in
@@ -425,8 +431,12 @@ def onepass_forward(codes: dict, tv, offs, ids, fmt: Fmt = E4M3, softmax_scale=N
     item reaches 448 (possible saturation), the item is recomputed with the
     exact row max and tau = 0 (the kernel's redo launch).  Used to check the
     CUDA kernel tightly; the reference-facing check is against
-    ``fp8_sparse_forward``.
+    ``fp8_sparse_forward``.  With packed key blocks (``packed_keys(tv)``) a
+    key's column in its block -- which decides polynomial or MUFU exp2 -- is
+    its position in the concatenated key stream modulo 128.
     """
+    if packed is None:
+        packed = packed_keys(tv)
     qv = decode(codes["q_codes"], fmt).astype(np.float64)
     kv = decode(codes["k_codes"], fmt).astype(np.float64)
     vv = decode(codes["v_codes"], fmt).astype(np.float64)
@@ -443,22 +453,29 @@ def onepass_forward(codes: dict, tv, offs, ids, fmt: Fmt = E4M3, softmax_scale=N
             rows = slice(u * tv + r0, u * tv + min(r0 + 128, tv))
             qrows = qv[rows]
             blocks = []
-            for vt in ids[offs[u]:offs[u + 1]]:
+            for i, vt in enumerate(ids[offs[u]:offs[u + 1]]):
                 c = float(np.float32(np.float32(np.float32(qs[u]) * np.float32(ks[vt])) * np.float32(sl)))
-                for b0 in range(0, tv, block):
-                    b1 = min(b0 + block, tv)
-                    blocks.append((c, vt * tv + b0, vt * tv + b1))
+                if packed:
+                    # first block of the stream separate (it sets the reference max), then whole tiles
+                    starts = [0, block] if i == 0 else [0]
+                    ends = [block, tv] if i == 0 else [tv]
+                    for b0, b1 in zip(starts, ends):
+                        blocks.append((c, vt * tv + b0, vt * tv + b1, (i * tv + b0) % block))
+                else:
+                    for b0 in range(0, tv, block):
+                        b1 = min(b0 + block, tv)
+                        blocks.append((c, vt * tv + b0, vt * tv + b1, 0))
 
             def run(m, t):
                 lsum = np.zeros(qrows.shape[0])
                 acc = np.zeros((qrows.shape[0], d))
                 over = False
-                for c, k0, k1 in blocks:
+                for c, k0, k1, col0 in blocks:
                     x = (qrows @ kv[k0:k1].T) * c
                     xe = x - m[:, None] + (math.log2(448.0) - t)
                     p = np.exp2(xe)
                     if poly:
-                        pc = pc_all[: x.shape[1]]
+                        pc = pc_all[(col0 + np.arange(x.shape[1])) % block]
                         p[:, pc] = _exp2_poly(xe[:, pc])
                     pq = grid_round(p.astype(np.float32), E4M3).astype(np.float64)
                     over |= bool(np.any(pq >= 448.0))
@@ -466,10 +483,10 @@ def onepass_forward(codes: dict, tv, offs, ids, fmt: Fmt = E4M3, softmax_scale=N
                     acc += pq @ vv[k0:k1]
                 return acc / lsum[:, None] * vs[None, :], over
 
-            c0, k0, k1 = blocks[0]
+            c0, k0, k1, _ = blocks[0]
             o, over = run((qrows @ kv[k0:k1].T).max(axis=1) * c0, tau)
             if over:
-                m = np.max([((qrows @ kv[a:b].T) * c).max(axis=1) for c, a, b in blocks], axis=0)
+                m = np.max([((qrows @ kv[a:b].T) * c).max(axis=1) for c, a, b, _ in blocks], axis=0)
                 o, _ = run(m, 0.0)
                 redo.append((u, r0 // 128))
             out[rows] = o

@@ -135,7 +135,48 @@ struct AttnParams {
   int64_t out_ts, out_hs;
   int32_t natural;
   int32_t gh, gw, st, sh, sw, dh, dw;
+  int32_t packed;  // key blocks run over the concatenated valid keys of the window's tiles (no padding keys)
 };
+
+// Position in an item's key stream during one pass.  Unpacked: every tile is cut into nb 128-key blocks (the
+// last has n_tail valid keys); packed (tile volume a multiple of 16 and >= 128): blocks of 128 consecutive
+// keys of the concatenated tiles, so a block holds the tail of tile kt and the head of tile kt + 1.
+struct KeyWalk {
+  int32_t kt = 0;  // tile (index into the item's window list)
+  int32_t r = 0;   // packed: first row of the next block in tile kt; unpacked: block index in tile kt
+};
+// The next block: keys [0, split) come from tile kt_a (from row `row0` on), keys [split, nvalid) from tile
+// kt_a + 1 (from row 0), keys >= nvalid are absent (padding or past the stream end).
+__device__ __forceinline__ void next_block(const AttnParams& p, int32_t n_kt, KeyWalk& w, int32_t& kt_a,
+                                           int32_t& row0, int32_t& split, int32_t& nvalid) {
+  kt_a = w.kt;
+  if (p.packed) {
+    row0 = w.r;
+    const int32_t n1 = min(kBlk, p.tv - w.r);
+    split = nvalid = n1;
+    w.r += n1;
+    if (w.r == p.tv) {
+      ++w.kt;
+      w.r = 0;
+      if (n1 < kBlk && w.kt < n_kt) {
+        w.r = kBlk - n1;
+        nvalid = kBlk;
+      }
+    }
+  } else {
+    row0 = w.r * kBlk;
+    nvalid = w.r == p.nb - 1 ? p.n_tail : kBlk;
+    split = kBlk;
+    if (++w.r == p.nb) {
+      w.r = 0;
+      ++w.kt;
+    }
+  }
+}
+// 128-key blocks of one pass over an item's n_kt key tiles
+__device__ __forceinline__ int32_t blocks_per_pass(const AttnParams& p, int32_t n_kt) {
+  return p.packed ? (n_kt * p.tv + kBlk - 1) / kBlk : n_kt * p.nb;
+}
 
 template <int D>
 struct Smem {
@@ -181,24 +222,26 @@ __device__ __forceinline__ uint64_t desc_mnmajor(uint32_t addr) {
 // element of a fully unrolled row and would otherwise multiply the code size.
 __device__ __noinline__ float exp_f32_cr(float x) { return __double2float_rn(exp((double)x)); }
 
-// Normalised-P pass 2: f64 sum of exp(S * c - m) over the first ncol of NC S columns.
+// Normalised-P pass 2: f64 sum of exp(S * c - m) over the first ncol of NC S columns; columns < split use
+// factor ca, the others cb (a packed block's two key tiles).
 template <int NC>
-__device__ __forceinline__ double expsum_norm(const uint32_t* s, int ncol, float c, float m) {
+__device__ __forceinline__ double expsum_norm(const uint32_t* s, int split, int ncol, float ca, float cb, float m) {
   double acc = 0.0;
 #pragma unroll
   for (int i = 0; i < NC; ++i)
-    if (i < ncol) acc += (double)exp_f32_cr(__fsub_rn(__fmul_rn(__uint_as_float(s[i]), c), m));
+    if (i < ncol) acc += (double)exp_f32_cr(__fsub_rn(__fmul_rn(__uint_as_float(s[i]), i < split ? ca : cb), m));
   return acc;
 }
 // Normalised-P pass 3: P~ = e4m3(448 * (exp(S * c - m) / l)), packed 4 per word; columns >= ncol are 0.
 template <int NC>
-__device__ __forceinline__ void compute_p_norm(const uint32_t* s, int ncol, float c, float m, float l,
-                                               uint32_t* w) {
+__device__ __forceinline__ void compute_p_norm(const uint32_t* s, int split, int ncol, float ca, float cb, float m,
+                                               float l, uint32_t* w) {
 #pragma unroll
   for (int i = 0; i < NC; i += 4) {
     float pv[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
+      const float c = i + k < split ? ca : cb;
       const float e = exp_f32_cr(__fsub_rn(__fmul_rn(__uint_as_float(s[i + k]), c), m));
       pv[k] = i + k < ncol ? __fmul_rn(__fdiv_rn(e, l), 448.0f) : 0.0f;
     }
@@ -209,7 +252,8 @@ __device__ __forceinline__ void compute_p_norm(const uint32_t* s, int ncol, floa
 template <int D, int FMT, int OUT, bool NORM>
 __global__ void __launch_bounds__(kThreads, 1)
     fpsa_attn_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
-                     const __grid_constant__ CUtensorMap tm_v, const AttnParams p) {
+                     const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_k16,
+                     const __grid_constant__ CUtensorMap tm_v16, const AttnParams p) {
   using S = Smem<D>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -282,6 +326,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     reinterpret_cast<uint32_t*>(smem + S::kOnes)[i] = one;
     reinterpret_cast<uint32_t*>(smem + S::kOnesTail)[i] = (4 * i) / D < p.n_tail ? one : 0u;
   }
+  if (p.packed) {
+    // a stream's last block leaves stage rows unloaded: their P~ codes are zeroed, and zero-initialised
+    // stages guarantee that what those codes multiply is a finite e4m3 value, never a NaN pattern
+    for (int i = threadIdx.x; i < 2 * kStages * S::kTile / 16; i += kThreads)
+      reinterpret_cast<uint4*>(smem + S::kK)[i] = make_uint4(0u, 0u, 0u, 0u);
+  }
   fence_proxy_async_smem();  // generic-proxy writes read by the tensor core
   tc_fence_before();
   __syncthreads();
@@ -299,29 +349,53 @@ __global__ void __launch_bounds__(kThreads, 1)
       prefetch_tmap(&tm_q);
       prefetch_tmap(&tm_k);
       prefetch_tmap(&tm_v);
+      if (p.packed) {
+        prefetch_tmap(&tm_k16);
+        prefetch_tmap(&tm_v16);
+      }
     }
     __syncwarp();
     uint32_t g = 0;  // K/V block counter over all items of this CTA
     int32_t h, u, qb;
     for (int32_t iter = 0; next_item(iter, h, u, qb); ++iter) {
       const int32_t kt0 = __ldg(p.offs + u), n_kt = __ldg(p.offs + u + 1) - kt0;
-      const int32_t n_kv = n_kt * p.nb, steps = passes * n_kv;
+      const int32_t n_kv = blocks_per_pass(p, n_kt), steps = passes * n_kv;
       const int qbuf = iter & 1;
       if (iter >= 2) attn_wait(&bar_qfree[qbuf], ((iter >> 1) - 1) & 1);
       mbar_arrive_expect_tx_w(&bar_q[qbuf], S::kTile);
       tma_load_2d_w(smem + S::kQ + qbuf * S::kTile, &tm_q, 0, (h * p.M + u) * p.pitch + qb * kBlk, &bar_q[qbuf]);
-      int32_t kt = 0, b = 0;
-      int32_t krow = (h * p.M + __ldg(p.ids + kt0)) * p.pitch;
-      for (int32_t s = 0; s < steps; ++s, ++g) {
+      KeyWalk w;
+      for (int32_t s = 0, j = 0; s < steps; ++s, ++g) {
+        if (j == n_kv) {  // exact / normalised modes stream the keys 2 / 3 times
+          j = 0;
+          w = KeyWalk{};
+        }
+        ++j;
+        int32_t kt_a, row0, split, nvalid;
+        next_block(p, n_kt, w, kt_a, row0, split, nvalid);
+        const int32_t krow = (h * p.M + __ldg(p.ids + kt0 + kt_a)) * p.pitch + row0;
         const uint32_t st = g % kStages;
+        uint8_t* const ks = smem + S::kK + st * S::kTile;
+        uint8_t* const vs = smem + S::kV + st * S::kTile;
         if (g >= (uint32_t)kStages) attn_wait(&bar_kv_empty[st], ((g / kStages) - 1) & 1);
-        mbar_arrive_expect_tx_w(&bar_kv_full[st], 2 * S::kTile);
-        tma_load_2d_w(smem + S::kK + st * S::kTile, &tm_k, 0, krow + b * kBlk, &bar_kv_full[st]);
-        tma_load_2d_w(smem + S::kV + st * S::kTile, &tm_v, 0, krow + b * kBlk, &bar_kv_full[st]);
-        if (++b == p.nb) {
-          b = 0;
-          if (++kt == n_kt) kt = 0;  // exact / normalised modes stream the keys 2 / 3 times
-          krow = (h * p.M + __ldg(p.ids + kt0 + kt)) * p.pitch;
+        if (!p.packed || split == kBlk) {
+          mbar_arrive_expect_tx_w(&bar_kv_full[st], 2 * S::kTile);
+          tma_load_2d_w(ks, &tm_k, 0, krow, &bar_kv_full[st]);
+          tma_load_2d_w(vs, &tm_v, 0, krow, &bar_kv_full[st]);
+        } else {
+          // two segments of 16-row boxes: rows [row0, tv) of tile kt_a, rows [0, nvalid - split) of kt_a + 1
+          mbar_arrive_expect_tx_w(&bar_kv_full[st], 2 * nvalid * D);
+          for (int32_t i = 0; i < split; i += 16) {
+            tma_load_2d_w(ks + i * D, &tm_k16, 0, krow + i, &bar_kv_full[st]);
+            tma_load_2d_w(vs + i * D, &tm_v16, 0, krow + i, &bar_kv_full[st]);
+          }
+          if (nvalid > split) {
+            const int32_t krow2 = (h * p.M + __ldg(p.ids + kt0 + kt_a + 1)) * p.pitch - split;
+            for (int32_t i = split; i < nvalid; i += 16) {
+              tma_load_2d_w(ks + i * D, &tm_k16, 0, krow2 + i, &bar_kv_full[st]);
+              tma_load_2d_w(vs + i * D, &tm_v16, 0, krow2 + i, &bar_kv_full[st]);
+            }
+          }
         }
       }
     }
@@ -347,7 +421,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     int32_t h, u, qb;
     for (int32_t iter = 0; next_item(iter, h, u, qb); ++iter) {
       const int32_t n_kt = __ldg(p.offs + u + 1) - __ldg(p.offs + u);
-      const int32_t n_kv = n_kt * p.nb, steps = passes * n_kv;
+      const int32_t n_kv = blocks_per_pass(p, n_kt), steps = passes * n_kv;
       const int32_t pv0 = (passes - 1) * n_kv;  // first step with a PV
       const int qbuf = iter & 1;
       const uint64_t dq = dq0 + (uint64_t)qbuf * kTileU;
@@ -397,7 +471,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           constexpr uint64_t kVk = 32 * D / 16;
           uint64_t dv[4], dkk[4], dqq[4];
           uint32_t ta[4];
-          dv[0] = (bp == p.nb - 1 ? dvt0 : dv0) + pv_st * kVStageStep;
+          // packed blocks zero the P~ codes of absent keys, so the plain ones atom serves every block
+          dv[0] = (!p.packed && bp == p.nb - 1 ? dvt0 : dv0) + pv_st * kVStageStep;
           const uint32_t ts = tm_s(gs);  // S(j), P~(j) and S(j+2) share the buffer
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
@@ -465,7 +540,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               attn_wait(&bar_ofree, (iter - 1) & 1);  // the previous item's epilogue has read O
               tc_fence_after();
             }
-            const uint64_t dv = (bp == p.nb - 1 ? dvt0 : dv0) + pv_st * kVStageStep;
+            const uint64_t dv = (!p.packed && bp == p.nb - 1 ? dvt0 : dv0) + pv_st * kVStageStep;
             const uint32_t ts = tm_s(gs);
   #ifndef FPSA_NO_MMA
             if constexpr (kPingPong) {  // one elect for the four K32 MMAs (shorter issue path)
@@ -567,7 +642,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int slot = iter & 1;
       attn_wait(&bar_meta_full[slot], (iter >> 1) & 1);
       const int32_t kt0 = s_hdr[slot][0], n_kt = s_hdr[slot][1];
-      const int32_t n_kv = n_kt * p.nb;
+      const int32_t n_kv = blocks_per_pass(p, n_kt);
       const float* fac = s_fac[slot];
       auto factor_at = [&](int32_t kt) {
         if (kt < kFacCap) return fac[kt];
@@ -586,38 +661,41 @@ __global__ void __launch_bounds__(kThreads, 1)
         // warp's TMEM load / store and hand-off latency overlaps the other's exp work
         const uint32_t s_row = tm_s((uint32_t)part) + lane_off;
         auto owned = [&](uint32_t gg) { return (int)(gg & 1u) == part; };
-        auto ncol_blk = [&](int32_t bb) { return bb == p.nb - 1 ? p.n_tail : kBlk; };
+        // factors of a block's two key tiles: keys < split from tile kt_a, the rest from kt_a + 1
+        auto factors = [&](int32_t kt_a, int32_t split, int32_t nvalid, float& ca, float& cb) {
+          ca = factor_at(kt_a);
+          cb = nvalid > split ? factor_at(kt_a + 1) : ca;
+        };
         float l_norm = 1.0f;  // normalised-P mode: f32 of the f64 row sum
         if (NORM || p.exact) {
           // pass 0 (exact and normalised modes): running max over this warp's key blocks, then over the pair
           float m_acc = -INFINITY;
-          int32_t kt = 0, b = 0;
+          KeyWalk wk;
           for (int32_t j = 0; j < n_kv; ++j, ++g) {
+            int32_t kt_a, row0, split, nvalid;
+            next_block(p, n_kt, wk, kt_a, row0, split, nvalid);
             if (owned(g)) {
-              const float c = factor_at(kt);
+              float ca, cb;
+              factors(kt_a, split, nvalid, ca, cb);
               attn_wait(&bar_s_full[g & 1], (g >> 1) & 1);
               tc_fence_after();
-              m_acc = fmaxf(m_acc, block_max<kBlk>(s_row, ncol_blk(b), false) * c);
+              m_acc = fmaxf(m_acc, block_max_split(s_row, split, nvalid, ca, cb));
               tc_fence_before();
               __syncwarp();
               if (lane == 0) mbar_arrive(&bar_p_ready[g & 1]);  // S consumed
-            }
-            if (b == p.nb - 1) {
-              b = 0;
-              ++kt;
-            } else {
-              ++b;
             }
           }
           m_ref = row_max(m_acc);
           if constexpr (NORM) {
             // pass 1: l = sum exp(s - m) in f64 over this warp's blocks, then over the pair
             double l_acc = 0.0;
-            int32_t kt = 0, b = 0;
+            KeyWalk wk1;
             for (int32_t j = 0; j < n_kv; ++j, ++g) {
+              int32_t kt_a, row0, split, nvalid;
+              next_block(p, n_kt, wk1, kt_a, row0, split, nvalid);
               if (owned(g)) {
-                const float c = factor_at(kt);
-                const int n = ncol_blk(b);
+                float ca, cb;
+                factors(kt_a, split, nvalid, ca, cb);
                 attn_wait(&bar_s_full[g & 1], (g >> 1) & 1);
                 tc_fence_after();
 #pragma unroll
@@ -625,17 +703,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                   uint32_t sreg[64];
                   load_s_all<64>(s_row + 64 * hb, sreg);
                   tmem_wait_ld();
-                  l_acc += expsum_norm<64>(sreg, n - 64 * hb, c, m_ref);
+                  l_acc += expsum_norm<64>(sreg, split - 64 * hb, nvalid - 64 * hb, ca, cb, m_ref);
                 }
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&bar_p_ready[g & 1]);  // S consumed
-              }
-              if (b == p.nb - 1) {
-                b = 0;
-                ++kt;
-              } else {
-                ++b;
               }
             }
             s_xchg_d[part][row] = l_acc;
@@ -650,16 +722,24 @@ __global__ void __launch_bounds__(kThreads, 1)
           // reference max = row max of the item's first key block, taken by the warp that owns it
           float m0 = -INFINITY;
           if (owned(g)) {
+            KeyWalk wk0;
+            int32_t kt_a, row0, split, nvalid;
+            next_block(p, n_kt, wk0, kt_a, row0, split, nvalid);
+            float ca, cb;
+            factors(kt_a, split, nvalid, ca, cb);
             attn_wait(&bar_s_full[g & 1], (g >> 1) & 1);
             tc_fence_after();
-            m0 = block_max<kBlk>(s_row, ncol_blk(0), false) * factor_at(0);
+            m0 = block_max_split(s_row, split, nvalid, ca, cb);
           }
           m_ref = row_max(m0);
         }
-        int32_t kt = 0, b = 0;
-        float c = factor_at(0);
+        KeyWalk wk;
         for (int32_t j = 0; j < n_kv; ++j, ++g) {
+          int32_t kt_a, row0, split, nvalid;
+          next_block(p, n_kt, wk, kt_a, row0, split, nvalid);
           if (owned(g)) {
+            float ca, cb;
+            factors(kt_a, split, nvalid, ca, cb);
 #ifdef FPSA_TRACE
             const long long ts0 = clock64();
 #endif
@@ -672,7 +752,6 @@ __global__ void __launch_bounds__(kThreads, 1)
             ++n_steps;
 #endif
             tc_fence_after();
-            const int n = ncol_blk(b);
             const float bias = kLog2_448 - m_ref - tau;
             uint32_t w[kBlk / 4];
             if constexpr (NORM) {
@@ -681,20 +760,20 @@ __global__ void __launch_bounds__(kThreads, 1)
                 uint32_t sreg[64];
                 load_s_all<64>(s_row + 64 * hb, sreg);
                 tmem_wait_ld();
-                compute_p_norm<64>(sreg, n - 64 * hb, c, m_ref, l_norm, w + 16 * hb);
+                compute_p_norm<64>(sreg, split - 64 * hb, nvalid - 64 * hb, ca, cb, m_ref, l_norm, w + 16 * hb);
               }
             } else {
               {
                 uint32_t sreg[64];
                 load_s_all<64>(s_row, sreg);
                 tmem_wait_ld();
-                sat |= compute_p_regs<64>(sreg, min(n, 64), c, bias, w);
+                sat |= compute_p_regs2<64>(sreg, split, nvalid, ca, cb, bias, w);
               }
               {
                 uint32_t sreg[64];
                 load_s_all<64>(s_row + 64, sreg);
                 tmem_wait_ld();
-                sat |= compute_p_regs<64>(sreg, max(n - 64, 0), c, bias, w + 16);
+                sat |= compute_p_regs2<64>(sreg, split - 64, nvalid - 64, ca, cb, bias, w + 16);
               }
             }
 #ifdef FPSA_TRACE
@@ -707,12 +786,6 @@ __global__ void __launch_bounds__(kThreads, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive(&bar_p_ready[g & 1]);
             FPSA_TL(warp, 3, g);
-          }
-          if (b == p.nb - 1) {
-            b = 0;
-            if (++kt < n_kt) c = factor_at(kt);
-          } else {
-            ++b;
           }
         }
       } else {
@@ -924,7 +997,8 @@ int make_code_map(CUtensorMap* m, const uint8_t* base, int64_t rows, int32_t d, 
 // is empty).  Normalised-P mode: one three-pass launch, nothing to redo.  Workspace words 0..2 (redo count,
 // the two launches' claim counters) are zeroed first.
 template <int D, int FMT, int OUT, bool NORM>
-int launch(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, AttnParams p, cudaStream_t st) {
+int launch(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, const CUtensorMap& tk16,
+           const CUtensorMap& tv16, AttnParams p, cudaStream_t st) {
   auto kern = fpsa_attn_kernel<D, FMT, OUT, NORM>;
   constexpr int smem = Smem<D>::kBytes + 1024;
   if (int s = ensure_smem_attr(reinterpret_cast<const void*>(kern), smem, "fpsa_attn_fwd")) return s;
@@ -933,11 +1007,11 @@ int launch(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, 
   const int grid = std::min(p.n_items, device_sm_count());
   p.exact = 0;
   p.claim = p.redo + 1;
-  kern<<<grid, kThreads, smem, st>>>(tq, tk, tv, p);
+  kern<<<grid, kThreads, smem, st>>>(tq, tk, tv, tk16, tv16, p);
   if constexpr (!NORM) {
     p.exact = 1;
     p.claim = p.redo + 2;
-    kern<<<grid, kThreads, smem, st>>>(tq, tk, tv, p);
+    kern<<<grid, kThreads, smem, st>>>(tq, tk, tv, tk16, tv16, p);
   }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(FPSA_ECUDA, std::string("fpsa_attn_fwd launch: ") + cudaGetErrorString(e));
@@ -979,10 +1053,12 @@ extern "C" int fpsa_attn_fwd(const uint8_t* q_codes, const uint8_t* k_codes, con
     return fail(FPSA_ECAPACITY, "attention workspace must hold " + std::to_string(need) + " bytes");
   const int32_t M = td.t * td.h * td.w;
   const int64_t rows = (int64_t)heads * M * tile_pitch;
-  CUtensorMap tq, tk, tvm;
+  CUtensorMap tq, tk, tvm, tk16, tv16;
   if (int s = make_code_map(&tq, q_codes, rows, d, kBlk)) return s;
   if (int s = make_code_map(&tk, k_codes, rows, d, kBlk)) return s;
   if (int s = make_code_map(&tvm, v_codes, rows, d, kBlk)) return s;
+  if (int s = make_code_map(&tk16, k_codes, rows, d, 16)) return s;  // packed key blocks' 16-row segments
+  if (int s = make_code_map(&tv16, v_codes, rows, d, 16)) return s;
   AttnParams p{};
   p.q_scales = q_scales;
   p.k_scales = k_scales;
@@ -1011,15 +1087,18 @@ extern "C" int fpsa_attn_fwd(const uint8_t* q_codes, const uint8_t* k_codes, con
   p.sw = tile.w;
   p.dh = td.h;
   p.dw = td.w;
+  // packed key blocks: needs 16-row segment boundaries and at most two key tiles per 128-key block
+  static const bool no_pack = getenv("FPSA_ATTN_NO_PACK") != nullptr;  // measurement switch
+  p.packed = !no_pack && kPingPong && tv % 16 == 0 && tv > kBlk && tv % kBlk != 0;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-#define FPSA_LAUNCH(D_, F_, O_) return launch<D_, F_, O_, false>(tq, tk, tvm, p, st)
+#define FPSA_LAUNCH(D_, F_, O_) return launch<D_, F_, O_, false>(tq, tk, tvm, tk16, tv16, p, st)
   if (norm) {  // f32 output only
     if (d == 128) {
-      if (fmt == FPSA_E4M3) return launch<128, FPSA_E4M3, FPSA_F32, true>(tq, tk, tvm, p, st);
-      return launch<128, FPSA_E5M2, FPSA_F32, true>(tq, tk, tvm, p, st);
+      if (fmt == FPSA_E4M3) return launch<128, FPSA_E4M3, FPSA_F32, true>(tq, tk, tvm, tk16, tv16, p, st);
+      return launch<128, FPSA_E5M2, FPSA_F32, true>(tq, tk, tvm, tk16, tv16, p, st);
     }
-    if (fmt == FPSA_E4M3) return launch<64, FPSA_E4M3, FPSA_F32, true>(tq, tk, tvm, p, st);
-    return launch<64, FPSA_E5M2, FPSA_F32, true>(tq, tk, tvm, p, st);
+    if (fmt == FPSA_E4M3) return launch<64, FPSA_E4M3, FPSA_F32, true>(tq, tk, tvm, tk16, tv16, p, st);
+    return launch<64, FPSA_E5M2, FPSA_F32, true>(tq, tk, tvm, tk16, tv16, p, st);
   }
   if (d == 128) {
     if (fmt == FPSA_E4M3) {

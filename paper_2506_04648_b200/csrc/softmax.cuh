@@ -284,6 +284,82 @@ __device__ __forceinline__ uint32_t compute_p_regs(const uint32_t* s, int ncol, 
   return saturated<NC>(w);
 }
 
+// softmax_chunk32 with two key tiles in the block (packed key blocks): columns < split take factor a, the
+// others factor b.  split is a multiple of 16, so the factor is chosen once per 16-column unit.
+template <int C>
+__device__ __forceinline__ void softmax_chunk32_split(const uint32_t* s, int split, f2 cca, f2 ccb, float csa,
+                                                      float csb, f2 bb, float bs, uint32_t* w) {
+  const bool s0 = 32 * C >= split, s1 = 32 * C + 16 >= split;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const bool sb = q < 4 ? s0 : s1;
+    const f2 cc = sb ? ccb : cca;
+    const float cs = sb ? csb : csa;
+    const float* v = reinterpret_cast<const float*>(s + 4 * q);
+    constexpr int kPer8 = FPSA_POLY_PER8;
+    f2 m;
+    if (kPer8 == 8 || (kPer8 == 6 && (q & 1))) {
+      m = exp2_poly_sat(f2{fma_sat(v[0], cs, bs), fma_sat(v[1], cs, bs)});
+    } else {
+      m = fma2(f2{v[0], v[1]}, cc, bb);
+      m = f2{ex2(m.x), ex2(m.y)};
+    }
+    const bool poly = kPer8 >= 4 || (kPer8 == 2 && (q & 1));
+    f2 pp;
+    if (poly) {
+      pp = exp2_poly_sat(f2{fma_sat(v[2], cs, bs), fma_sat(v[3], cs, bs)});
+    } else {
+      pp = fma2(f2{v[2], v[3]}, cc, bb);
+      pp = f2{ex2(pp.x), ex2(pp.y)};
+    }
+    w[8 * C + q] = e4m3x4(m, pp);
+  }
+}
+
+// compute_p_regs for a block whose columns < split belong to one key tile (factor ca) and the rest to the
+// next (cb); columns >= ncol (padding keys, or past the end of a packed key stream) get P~ = 0.  split and
+// ncol are relative to this NC-column part (may be <= 0 or >= NC).
+template <int NC>
+__device__ __forceinline__ uint32_t compute_p_regs2(const uint32_t* s, int split, int ncol, float ca, float cb,
+                                                    float boff, uint32_t* w) {
+  const f2 cca = bcast(ca), ccb = bcast(cb), bb = bcast(boff);
+  const float csa = ca * (1.0f / 256.0f), csb = cb * (1.0f / 256.0f), bs = (boff + 126.0f) * (1.0f / 256.0f);
+  softmax_chunk32_split<0>(s, split, cca, ccb, csa, csb, bb, bs, w);
+  if constexpr (NC == 64) softmax_chunk32_split<1>(s + 32, split, cca, ccb, csa, csb, bb, bs, w);
+  if (ncol < NC) {
+#pragma unroll
+    for (int i = 0; i < NC / 4; ++i)
+      if (4 * i >= ncol) w[i] = 0u;
+  }
+  return saturated<NC>(w);
+}
+
+// max over the first ncol (<= 128) columns of S * c, c = ca for columns < split and cb above (-inf if none)
+template <int NC>
+__device__ __forceinline__ float block_max(uint32_t s_addr, int ncol, bool pad8);
+__device__ __forceinline__ float block_max_split(uint32_t s_addr, int split, int ncol, float ca, float cb) {
+  if (split >= ncol) return block_max<128>(s_addr, ncol, false) * ca;  // one key tile (the common case)
+  float ma = -INFINITY, mb = -INFINITY;
+#pragma unroll
+  for (int base = 0; base < 128; base += 32) {
+    if (base < ncol) {
+      uint32_t s[32];
+      tmem_ld32(s_addr + base, s);
+      tmem_wait_ld();
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const float x = __uint_as_float(s[i]);
+        if (base + i < ncol) {
+          if (base + i < split) ma = fmaxf(ma, x);
+          else mb = fmaxf(mb, x);
+        }
+      }
+    }
+  }
+  // c > 0: max(S) * c == max(S * c) under round-to-nearest (monotone)
+  return fmaxf(ma * ca, mb * cb);
+}
+
 // Max of the first ncol (0..NC) raw S values of a row part (-inf if none).
 template <int NC>
 __device__ __forceinline__ float block_max(uint32_t s_addr, int ncol, bool pad8) {
