@@ -138,6 +138,13 @@ struct AttnParams {
   int32_t packed;  // key blocks run over the concatenated valid keys of the window's tiles (no padding keys)
 };
 
+// TMA maps of the packed key blocks' segments: box heights 16, 32, ..., 128 rows (index n / 16 - 1), so a
+// block split between two key tiles costs two loads per operand.
+struct SegMaps {
+  CUtensorMap k[kBlk / 16];
+  CUtensorMap v[kBlk / 16];
+};
+
 // Position in an item's key stream during one pass.  Unpacked: every tile is cut into nb 128-key blocks (the
 // last has n_tail valid keys); packed (tile volume a multiple of 16 and >= 128): blocks of 128 consecutive
 // keys of the concatenated tiles, so a block holds the tail of tile kt and the head of tile kt + 1.
@@ -147,10 +154,11 @@ struct KeyWalk {
 };
 // The next block: keys [0, split) come from tile kt_a (from row `row0` on), keys [split, nvalid) from tile
 // kt_a + 1 (from row 0), keys >= nvalid are absent (padding or past the stream end).
+template <bool PACKED>
 __device__ __forceinline__ void next_block(const AttnParams& p, int32_t n_kt, KeyWalk& w, int32_t& kt_a,
                                            int32_t& row0, int32_t& split, int32_t& nvalid) {
   kt_a = w.kt;
-  if (p.packed) {
+  if constexpr (PACKED) {
     row0 = w.r;
     const int32_t n1 = min(kBlk, p.tv - w.r);
     split = nvalid = n1;
@@ -174,8 +182,9 @@ __device__ __forceinline__ void next_block(const AttnParams& p, int32_t n_kt, Ke
   }
 }
 // 128-key blocks of one pass over an item's n_kt key tiles
+template <bool PACKED>
 __device__ __forceinline__ int32_t blocks_per_pass(const AttnParams& p, int32_t n_kt) {
-  return p.packed ? (n_kt * p.tv + kBlk - 1) / kBlk : n_kt * p.nb;
+  return PACKED ? (n_kt * p.tv + kBlk - 1) / kBlk : n_kt * p.nb;
 }
 
 template <int D>
@@ -249,11 +258,11 @@ __device__ __forceinline__ void compute_p_norm(const uint32_t* s, int split, int
   }
 }
 
-template <int D, int FMT, int OUT, bool NORM>
+template <int D, int FMT, int OUT, bool NORM, bool PACKED>
 __global__ void __launch_bounds__(kThreads, 1)
     fpsa_attn_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
-                     const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_k16,
-                     const __grid_constant__ CUtensorMap tm_v16, const AttnParams p) {
+                     const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ SegMaps seg,
+                     const AttnParams p) {
   using S = Smem<D>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -326,7 +335,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     reinterpret_cast<uint32_t*>(smem + S::kOnes)[i] = one;
     reinterpret_cast<uint32_t*>(smem + S::kOnesTail)[i] = (4 * i) / D < p.n_tail ? one : 0u;
   }
-  if (p.packed) {
+  if constexpr (PACKED) {
     // a stream's last block leaves stage rows unloaded: their P~ codes are zeroed, and zero-initialised
     // stages guarantee that what those codes multiply is a finite e4m3 value, never a NaN pattern
     for (int i = threadIdx.x; i < 2 * kStages * S::kTile / 16; i += kThreads)
@@ -349,17 +358,18 @@ __global__ void __launch_bounds__(kThreads, 1)
       prefetch_tmap(&tm_q);
       prefetch_tmap(&tm_k);
       prefetch_tmap(&tm_v);
-      if (p.packed) {
-        prefetch_tmap(&tm_k16);
-        prefetch_tmap(&tm_v16);
-      }
+      if constexpr (PACKED)
+        for (int i = 0; i < kBlk / 16; ++i) {
+          prefetch_tmap(&seg.k[i]);
+          prefetch_tmap(&seg.v[i]);
+        }
     }
     __syncwarp();
     uint32_t g = 0;  // K/V block counter over all items of this CTA
     int32_t h, u, qb;
     for (int32_t iter = 0; next_item(iter, h, u, qb); ++iter) {
       const int32_t kt0 = __ldg(p.offs + u), n_kt = __ldg(p.offs + u + 1) - kt0;
-      const int32_t n_kv = blocks_per_pass(p, n_kt), steps = passes * n_kv;
+      const int32_t n_kv = blocks_per_pass<PACKED>(p, n_kt), steps = passes * n_kv;
       const int qbuf = iter & 1;
       if (iter >= 2) attn_wait(&bar_qfree[qbuf], ((iter >> 1) - 1) & 1);
       mbar_arrive_expect_tx_w(&bar_q[qbuf], S::kTile);
@@ -372,29 +382,26 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         ++j;
         int32_t kt_a, row0, split, nvalid;
-        next_block(p, n_kt, w, kt_a, row0, split, nvalid);
+        next_block<PACKED>(p, n_kt, w, kt_a, row0, split, nvalid);
         const int32_t krow = (h * p.M + __ldg(p.ids + kt0 + kt_a)) * p.pitch + row0;
         const uint32_t st = g % kStages;
         uint8_t* const ks = smem + S::kK + st * S::kTile;
         uint8_t* const vs = smem + S::kV + st * S::kTile;
         if (g >= (uint32_t)kStages) attn_wait(&bar_kv_empty[st], ((g / kStages) - 1) & 1);
-        if (!p.packed || split == kBlk) {
+        if (!PACKED || split == kBlk) {
           mbar_arrive_expect_tx_w(&bar_kv_full[st], 2 * S::kTile);
           tma_load_2d_w(ks, &tm_k, 0, krow, &bar_kv_full[st]);
           tma_load_2d_w(vs, &tm_v, 0, krow, &bar_kv_full[st]);
         } else {
-          // two segments of 16-row boxes: rows [row0, tv) of tile kt_a, rows [0, nvalid - split) of kt_a + 1
+          // two segments: rows [row0, tv) of tile kt_a, rows [0, nvalid - split) of tile kt_a + 1
           mbar_arrive_expect_tx_w(&bar_kv_full[st], 2 * nvalid * D);
-          for (int32_t i = 0; i < split; i += 16) {
-            tma_load_2d_w(ks + i * D, &tm_k16, 0, krow + i, &bar_kv_full[st]);
-            tma_load_2d_w(vs + i * D, &tm_v16, 0, krow + i, &bar_kv_full[st]);
-          }
+          tma_load_2d_w(ks, &seg.k[split / 16 - 1], 0, krow, &bar_kv_full[st]);
+          tma_load_2d_w(vs, &seg.v[split / 16 - 1], 0, krow, &bar_kv_full[st]);
           if (nvalid > split) {
-            const int32_t krow2 = (h * p.M + __ldg(p.ids + kt0 + kt_a + 1)) * p.pitch - split;
-            for (int32_t i = split; i < nvalid; i += 16) {
-              tma_load_2d_w(ks + i * D, &tm_k16, 0, krow2 + i, &bar_kv_full[st]);
-              tma_load_2d_w(vs + i * D, &tm_v16, 0, krow2 + i, &bar_kv_full[st]);
-            }
+            const int32_t krow2 = (h * p.M + __ldg(p.ids + kt0 + kt_a + 1)) * p.pitch;
+            const int n2 = nvalid - split;
+            tma_load_2d_w(ks + split * D, &seg.k[n2 / 16 - 1], 0, krow2, &bar_kv_full[st]);
+            tma_load_2d_w(vs + split * D, &seg.v[n2 / 16 - 1], 0, krow2, &bar_kv_full[st]);
           }
         }
       }
@@ -421,7 +428,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     int32_t h, u, qb;
     for (int32_t iter = 0; next_item(iter, h, u, qb); ++iter) {
       const int32_t n_kt = __ldg(p.offs + u + 1) - __ldg(p.offs + u);
-      const int32_t n_kv = blocks_per_pass(p, n_kt), steps = passes * n_kv;
+      const int32_t n_kv = blocks_per_pass<PACKED>(p, n_kt), steps = passes * n_kv;
       const int32_t pv0 = (passes - 1) * n_kv;  // first step with a PV
       const int qbuf = iter & 1;
       const uint64_t dq = dq0 + (uint64_t)qbuf * kTileU;
@@ -472,7 +479,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           uint64_t dv[4], dkk[4], dqq[4];
           uint32_t ta[4];
           // packed blocks zero the P~ codes of absent keys, so the plain ones atom serves every block
-          dv[0] = (!p.packed && bp == p.nb - 1 ? dvt0 : dv0) + pv_st * kVStageStep;
+          dv[0] = (!PACKED && bp == p.nb - 1 ? dvt0 : dv0) + pv_st * kVStageStep;
           const uint32_t ts = tm_s(gs);  // S(j), P~(j) and S(j+2) share the buffer
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
@@ -540,7 +547,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               attn_wait(&bar_ofree, (iter - 1) & 1);  // the previous item's epilogue has read O
               tc_fence_after();
             }
-            const uint64_t dv = (!p.packed && bp == p.nb - 1 ? dvt0 : dv0) + pv_st * kVStageStep;
+            const uint64_t dv = (!PACKED && bp == p.nb - 1 ? dvt0 : dv0) + pv_st * kVStageStep;
             const uint32_t ts = tm_s(gs);
   #ifndef FPSA_NO_MMA
             if constexpr (kPingPong) {  // one elect for the four K32 MMAs (shorter issue path)
@@ -642,7 +649,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int slot = iter & 1;
       attn_wait(&bar_meta_full[slot], (iter >> 1) & 1);
       const int32_t kt0 = s_hdr[slot][0], n_kt = s_hdr[slot][1];
-      const int32_t n_kv = blocks_per_pass(p, n_kt);
+      const int32_t n_kv = blocks_per_pass<PACKED>(p, n_kt);
       const float* fac = s_fac[slot];
       auto factor_at = [&](int32_t kt) {
         if (kt < kFacCap) return fac[kt];
@@ -673,7 +680,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           KeyWalk wk;
           for (int32_t j = 0; j < n_kv; ++j, ++g) {
             int32_t kt_a, row0, split, nvalid;
-            next_block(p, n_kt, wk, kt_a, row0, split, nvalid);
+            next_block<PACKED>(p, n_kt, wk, kt_a, row0, split, nvalid);
             if (owned(g)) {
               float ca, cb;
               factors(kt_a, split, nvalid, ca, cb);
@@ -692,7 +699,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             KeyWalk wk1;
             for (int32_t j = 0; j < n_kv; ++j, ++g) {
               int32_t kt_a, row0, split, nvalid;
-              next_block(p, n_kt, wk1, kt_a, row0, split, nvalid);
+              next_block<PACKED>(p, n_kt, wk1, kt_a, row0, split, nvalid);
               if (owned(g)) {
                 float ca, cb;
                 factors(kt_a, split, nvalid, ca, cb);
@@ -724,7 +731,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (owned(g)) {
             KeyWalk wk0;
             int32_t kt_a, row0, split, nvalid;
-            next_block(p, n_kt, wk0, kt_a, row0, split, nvalid);
+            next_block<PACKED>(p, n_kt, wk0, kt_a, row0, split, nvalid);
             float ca, cb;
             factors(kt_a, split, nvalid, ca, cb);
             attn_wait(&bar_s_full[g & 1], (g >> 1) & 1);
@@ -736,7 +743,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         KeyWalk wk;
         for (int32_t j = 0; j < n_kv; ++j, ++g) {
           int32_t kt_a, row0, split, nvalid;
-          next_block(p, n_kt, wk, kt_a, row0, split, nvalid);
+          next_block<PACKED>(p, n_kt, wk, kt_a, row0, split, nvalid);
           if (owned(g)) {
             float ca, cb;
             factors(kt_a, split, nvalid, ca, cb);
@@ -761,6 +768,20 @@ __global__ void __launch_bounds__(kThreads, 1)
                 load_s_all<64>(s_row + 64 * hb, sreg);
                 tmem_wait_ld();
                 compute_p_norm<64>(sreg, split - 64 * hb, nvalid - 64 * hb, ca, cb, m_ref, l_norm, w + 16 * hb);
+              }
+            } else if constexpr (!PACKED) {
+              // one key tile per block; padding keys need no mask (zero V rows, zero rows of the tail ones atom)
+              {
+                uint32_t sreg[64];
+                load_s_all<64>(s_row, sreg);
+                tmem_wait_ld();
+                sat |= compute_p_regs<64>(sreg, min(nvalid, 64), ca, bias, w);
+              }
+              {
+                uint32_t sreg[64];
+                load_s_all<64>(s_row + 64, sreg);
+                tmem_wait_ld();
+                sat |= compute_p_regs<64>(sreg, max(nvalid - 64, 0), ca, bias, w + 16);
               }
             } else {
               {
@@ -996,10 +1017,10 @@ int make_code_map(CUtensorMap* m, const uint8_t* base, int64_t rows, int32_t d, 
 // Main persistent launch, then the exact-mode launch over the redo list (its CTAs exit at once when the list
 // is empty).  Normalised-P mode: one three-pass launch, nothing to redo.  Workspace words 0..2 (redo count,
 // the two launches' claim counters) are zeroed first.
-template <int D, int FMT, int OUT, bool NORM>
-int launch(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, const CUtensorMap& tk16,
-           const CUtensorMap& tv16, AttnParams p, cudaStream_t st) {
-  auto kern = fpsa_attn_kernel<D, FMT, OUT, NORM>;
+template <int D, int FMT, int OUT, bool NORM, bool PACKED>
+int launch(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, const SegMaps& seg, AttnParams p,
+           cudaStream_t st) {
+  auto kern = fpsa_attn_kernel<D, FMT, OUT, NORM, PACKED>;
   constexpr int smem = Smem<D>::kBytes + 1024;
   if (int s = ensure_smem_attr(reinterpret_cast<const void*>(kern), smem, "fpsa_attn_fwd")) return s;
   if (cudaMemsetAsync(p.redo, 0, kRedoHeader * sizeof(int32_t), st) != cudaSuccess)
@@ -1007,15 +1028,23 @@ int launch(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, 
   const int grid = std::min(p.n_items, device_sm_count());
   p.exact = 0;
   p.claim = p.redo + 1;
-  kern<<<grid, kThreads, smem, st>>>(tq, tk, tv, tk16, tv16, p);
+  kern<<<grid, kThreads, smem, st>>>(tq, tk, tv, seg, p);
   if constexpr (!NORM) {
     p.exact = 1;
     p.claim = p.redo + 2;
-    kern<<<grid, kThreads, smem, st>>>(tq, tk, tv, tk16, tv16, p);
+    kern<<<grid, kThreads, smem, st>>>(tq, tk, tv, seg, p);
   }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(FPSA_ECUDA, std::string("fpsa_attn_fwd launch: ") + cudaGetErrorString(e));
   return FPSA_OK;
+}
+
+// packed or per-tile key blocks (p.packed, chosen by the host)
+template <int D, int FMT, int OUT, bool NORM>
+int launch_p(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tv, const SegMaps& seg, AttnParams p,
+             cudaStream_t st) {
+  if (p.packed) return launch<D, FMT, OUT, NORM, true>(tq, tk, tv, seg, p, st);
+  return launch<D, FMT, OUT, NORM, false>(tq, tk, tv, seg, p, st);
 }
 
 }  // namespace
@@ -1053,12 +1082,15 @@ extern "C" int fpsa_attn_fwd(const uint8_t* q_codes, const uint8_t* k_codes, con
     return fail(FPSA_ECAPACITY, "attention workspace must hold " + std::to_string(need) + " bytes");
   const int32_t M = td.t * td.h * td.w;
   const int64_t rows = (int64_t)heads * M * tile_pitch;
-  CUtensorMap tq, tk, tvm, tk16, tv16;
+  CUtensorMap tq, tk, tvm;
   if (int s = make_code_map(&tq, q_codes, rows, d, kBlk)) return s;
   if (int s = make_code_map(&tk, k_codes, rows, d, kBlk)) return s;
   if (int s = make_code_map(&tvm, v_codes, rows, d, kBlk)) return s;
-  if (int s = make_code_map(&tk16, k_codes, rows, d, 16)) return s;  // packed key blocks' 16-row segments
-  if (int s = make_code_map(&tv16, v_codes, rows, d, 16)) return s;
+  SegMaps seg;  // packed key blocks' segments, 16..128 rows
+  for (int i = 0; i < kBlk / 16; ++i) {
+    if (int s = make_code_map(&seg.k[i], k_codes, rows, d, 16 * (i + 1))) return s;
+    if (int s = make_code_map(&seg.v[i], v_codes, rows, d, 16 * (i + 1))) return s;
+  }
   AttnParams p{};
   p.q_scales = q_scales;
   p.k_scales = k_scales;
@@ -1091,14 +1123,14 @@ extern "C" int fpsa_attn_fwd(const uint8_t* q_codes, const uint8_t* k_codes, con
   static const bool no_pack = getenv("FPSA_ATTN_NO_PACK") != nullptr;  // measurement switch
   p.packed = !no_pack && kPingPong && tv % 16 == 0 && tv > kBlk && tv % kBlk != 0;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-#define FPSA_LAUNCH(D_, F_, O_) return launch<D_, F_, O_, false>(tq, tk, tvm, tk16, tv16, p, st)
+#define FPSA_LAUNCH(D_, F_, O_) return launch_p<D_, F_, O_, false>(tq, tk, tvm, seg, p, st)
   if (norm) {  // f32 output only
     if (d == 128) {
-      if (fmt == FPSA_E4M3) return launch<128, FPSA_E4M3, FPSA_F32, true>(tq, tk, tvm, tk16, tv16, p, st);
-      return launch<128, FPSA_E5M2, FPSA_F32, true>(tq, tk, tvm, tk16, tv16, p, st);
+      if (fmt == FPSA_E4M3) return launch_p<128, FPSA_E4M3, FPSA_F32, true>(tq, tk, tvm, seg, p, st);
+      return launch_p<128, FPSA_E5M2, FPSA_F32, true>(tq, tk, tvm, seg, p, st);
     }
-    if (fmt == FPSA_E4M3) return launch<64, FPSA_E4M3, FPSA_F32, true>(tq, tk, tvm, tk16, tv16, p, st);
-    return launch<64, FPSA_E5M2, FPSA_F32, true>(tq, tk, tvm, tk16, tv16, p, st);
+    if (fmt == FPSA_E4M3) return launch_p<64, FPSA_E4M3, FPSA_F32, true>(tq, tk, tvm, seg, p, st);
+    return launch_p<64, FPSA_E5M2, FPSA_F32, true>(tq, tk, tvm, seg, p, st);
   }
   if (d == 128) {
     if (fmt == FPSA_E4M3) {
