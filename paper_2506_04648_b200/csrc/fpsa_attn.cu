@@ -136,7 +136,11 @@ struct AttnParams {
   int32_t natural;
   int32_t gh, gw, st, sh, sw, dh, dw;
   int32_t packed;  // key blocks run over the concatenated valid keys of the window's tiles (no padding keys)
+  uint32_t div_tv, div_nb;  // ceil(2^32 / tv), ceil(2^32 / nb): exact quotients of the block geometry
 };
+
+// floor(x / d) for the magic m = ceil(2^32 / d), exact while x < 2^32 / d (key positions here are < 2^21)
+__device__ __forceinline__ uint32_t div_magic(uint32_t x, uint32_t m) { return __umulhi(x, m); }
 
 // TMA maps of the packed key blocks' segments: box heights 16, 32, ..., 128 rows (index n / 16 - 1), so a
 // block split between two key tiles costs two loads per operand.
@@ -181,6 +185,22 @@ __device__ __forceinline__ void next_block(const AttnParams& p, int32_t n_kt, Ke
     }
   }
 }
+// Geometry of block j of a pass in closed form (the softmax warps visit only the blocks they own).
+template <bool PACKED>
+__device__ __forceinline__ void block_at(const AttnParams& p, int32_t n_kt, int32_t j, int32_t& kt_a, int32_t& split,
+                                         int32_t& nvalid) {
+  if constexpr (PACKED) {
+    const int32_t pos = j * kBlk;
+    kt_a = p.div_tv ? (int32_t)div_magic((uint32_t)pos, p.div_tv) : pos / p.tv;
+    split = min(kBlk, p.tv - (pos - kt_a * p.tv));
+    nvalid = min(kBlk, n_kt * p.tv - pos);
+  } else {
+    kt_a = p.div_nb ? (int32_t)div_magic((uint32_t)j, p.div_nb) : j / p.nb;
+    nvalid = j - kt_a * p.nb == p.nb - 1 ? p.n_tail : kBlk;
+    split = kBlk;
+  }
+}
+
 // 128-key blocks of one pass over an item's n_kt key tiles
 template <bool PACKED>
 __device__ __forceinline__ int32_t blocks_per_pass(const AttnParams& p, int32_t n_kt) {
@@ -668,6 +688,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         // warp's TMEM load / store and hand-off latency overlaps the other's exp work
         const uint32_t s_row = tm_s((uint32_t)part) + lane_off;
         auto owned = [&](uint32_t gg) { return (int)(gg & 1u) == part; };
+        // first block of a pass starting at step counter gg that this warp owns (then every second one)
+        auto first_owned = [&](uint32_t gg) { return (int32_t)(((uint32_t)part - gg) & 1u); };
         // factors of a block's two key tiles: keys < split from tile kt_a, the rest from kt_a + 1
         auto factors = [&](int32_t kt_a, int32_t split, int32_t nvalid, float& ca, float& cb) {
           ca = factor_at(kt_a);
@@ -677,46 +699,44 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (NORM || p.exact) {
           // pass 0 (exact and normalised modes): running max over this warp's key blocks, then over the pair
           float m_acc = -INFINITY;
-          KeyWalk wk;
-          for (int32_t j = 0; j < n_kv; ++j, ++g) {
-            int32_t kt_a, row0, split, nvalid;
-            next_block<PACKED>(p, n_kt, wk, kt_a, row0, split, nvalid);
-            if (owned(g)) {
-              float ca, cb;
-              factors(kt_a, split, nvalid, ca, cb);
-              attn_wait(&bar_s_full[g & 1], (g >> 1) & 1);
-              tc_fence_after();
-              m_acc = fmaxf(m_acc, block_max_split(s_row, split, nvalid, ca, cb));
-              tc_fence_before();
-              __syncwarp();
-              if (lane == 0) mbar_arrive(&bar_p_ready[g & 1]);  // S consumed
-            }
+          for (int32_t j = first_owned(g); j < n_kv; j += 2) {
+            const uint32_t gj = g + j;
+            int32_t kt_a, split, nvalid;
+            block_at<PACKED>(p, n_kt, j, kt_a, split, nvalid);
+            float ca, cb;
+            factors(kt_a, split, nvalid, ca, cb);
+            attn_wait(&bar_s_full[gj & 1], (gj >> 1) & 1);
+            tc_fence_after();
+            m_acc = fmaxf(m_acc, block_max_split(s_row, split, nvalid, ca, cb));
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&bar_p_ready[gj & 1]);  // S consumed
           }
+          g += n_kv;
           m_ref = row_max(m_acc);
           if constexpr (NORM) {
             // pass 1: l = sum exp(s - m) in f64 over this warp's blocks, then over the pair
             double l_acc = 0.0;
-            KeyWalk wk1;
-            for (int32_t j = 0; j < n_kv; ++j, ++g) {
-              int32_t kt_a, row0, split, nvalid;
-              next_block<PACKED>(p, n_kt, wk1, kt_a, row0, split, nvalid);
-              if (owned(g)) {
-                float ca, cb;
-                factors(kt_a, split, nvalid, ca, cb);
-                attn_wait(&bar_s_full[g & 1], (g >> 1) & 1);
-                tc_fence_after();
+            for (int32_t j = first_owned(g); j < n_kv; j += 2) {
+              const uint32_t gj = g + j;
+              int32_t kt_a, split, nvalid;
+              block_at<PACKED>(p, n_kt, j, kt_a, split, nvalid);
+              float ca, cb;
+              factors(kt_a, split, nvalid, ca, cb);
+              attn_wait(&bar_s_full[gj & 1], (gj >> 1) & 1);
+              tc_fence_after();
 #pragma unroll
-                for (int hb = 0; hb < 2; ++hb) {
-                  uint32_t sreg[64];
-                  load_s_all<64>(s_row + 64 * hb, sreg);
-                  tmem_wait_ld();
-                  l_acc += expsum_norm<64>(sreg, split - 64 * hb, nvalid - 64 * hb, ca, cb, m_ref);
-                }
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&bar_p_ready[g & 1]);  // S consumed
+              for (int hb = 0; hb < 2; ++hb) {
+                uint32_t sreg[64];
+                load_s_all<64>(s_row + 64 * hb, sreg);
+                tmem_wait_ld();
+                l_acc += expsum_norm<64>(sreg, split - 64 * hb, nvalid - 64 * hb, ca, cb, m_ref);
               }
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive(&bar_p_ready[gj & 1]);  // S consumed
             }
+            g += n_kv;
             s_xchg_d[part][row] = l_acc;
             row_sync();
             double l_row = s_xchg_d[0][row];
@@ -729,9 +749,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           // reference max = row max of the item's first key block, taken by the warp that owns it
           float m0 = -INFINITY;
           if (owned(g)) {
-            KeyWalk wk0;
-            int32_t kt_a, row0, split, nvalid;
-            next_block<PACKED>(p, n_kt, wk0, kt_a, row0, split, nvalid);
+            int32_t kt_a, split, nvalid;
+            block_at<PACKED>(p, n_kt, 0, kt_a, split, nvalid);
             float ca, cb;
             factors(kt_a, split, nvalid, ca, cb);
             attn_wait(&bar_s_full[g & 1], (g >> 1) & 1);
@@ -740,19 +759,19 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           m_ref = row_max(m0);
         }
-        KeyWalk wk;
-        for (int32_t j = 0; j < n_kv; ++j, ++g) {
-          int32_t kt_a, row0, split, nvalid;
-          next_block<PACKED>(p, n_kt, wk, kt_a, row0, split, nvalid);
-          if (owned(g)) {
+        for (int32_t j = first_owned(g); j < n_kv; j += 2) {
+          const uint32_t g_own = g + j;
+          {
+            int32_t kt_a, split, nvalid;
+            block_at<PACKED>(p, n_kt, j, kt_a, split, nvalid);
             float ca, cb;
             factors(kt_a, split, nvalid, ca, cb);
 #ifdef FPSA_TRACE
             const long long ts0 = clock64();
 #endif
-            FPSA_TL(warp, 0, g);
-            attn_wait(&bar_s_full[g & 1], (g >> 1) & 1);
-            FPSA_TL(warp, 1, g);
+            FPSA_TL(warp, 0, g_own);
+            attn_wait(&bar_s_full[g_own & 1], (g_own >> 1) & 1);
+            FPSA_TL(warp, 1, g_own);
 #ifdef FPSA_TRACE
             w_s += clock64() - ts0;
             const long long tc0 = clock64();
@@ -800,15 +819,16 @@ __global__ void __launch_bounds__(kThreads, 1)
 #ifdef FPSA_TRACE
             w_c += clock64() - tc0;
 #endif
-            FPSA_TL(warp, 2, g);
+            FPSA_TL(warp, 2, g_own);
             tmem_st32(s_row, w);  // P~ of the 128 keys over the first 32 columns of this S buffer
             tmem_wait_st();
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&bar_p_ready[g & 1]);
-            FPSA_TL(warp, 3, g);
+            if (lane == 0) mbar_arrive(&bar_p_ready[g_own & 1]);
+            FPSA_TL(warp, 3, g_own);
           }
         }
+        g += n_kv;
       } else {
       if (p.exact) {
         // pass 0 (exact mode only): running max of x over all key blocks
@@ -1122,6 +1142,14 @@ extern "C" int fpsa_attn_fwd(const uint8_t* q_codes, const uint8_t* k_codes, con
   // packed key blocks: needs 16-row segment boundaries and at most two key tiles per 128-key block
   static const bool no_pack = getenv("FPSA_ATTN_NO_PACK") != nullptr;  // measurement switch
   p.packed = !no_pack && kPingPong && tv % 16 == 0 && tv > kBlk && tv % kBlk != 0;
+  // magic divisors of the softmax warps' block geometry: exact while (key position) * divisor < 2^32
+  // (positions stay below M * tv); 0 selects a plain division
+  auto magic = [](uint64_t d, uint64_t bound) -> uint32_t {
+    if (d < 2 || bound * d >= (1ull << 32)) return 0u;
+    return (uint32_t)(((1ull << 32) + d - 1) / d);
+  };
+  p.div_tv = magic((uint64_t)tv, (uint64_t)M * tv + kBlk);
+  p.div_nb = magic((uint64_t)p.nb, (uint64_t)M * p.nb + 1);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
 #define FPSA_LAUNCH(D_, F_, O_) return launch_p<D_, F_, O_, false>(tq, tk, tvm, seg, p, st)
   if (norm) {  // f32 output only
