@@ -138,49 +138,11 @@ __device__ __forceinline__ void softmax_unit(const uint32_t* s, f2 cc, f2 bb, fl
 #ifndef FPSA_POLY_PER8
 #define FPSA_POLY_PER8 4
 #endif
-// FPSA_EX2_MODE 0: the split above; 1: every column through MUFU ex2.approx.f16x2 (two weights per MUFU
-// instruction, f16 argument and result, converted straight to e4m3 with cvt.e4m3x2.f16x2); 2: columns
-// 0-1 of each group on f32 MUFU ex2, columns 2-3 on f16x2 MUFU (no polynomial).
-#ifndef FPSA_EX2_MODE
-#define FPSA_EX2_MODE 0
-#endif
-__device__ __forceinline__ uint32_t h2_of(f2 a) {  // a.x in the low half
-  uint32_t r;
-  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(a.y), "f"(a.x));
-  return r;
-}
-__device__ __forceinline__ uint32_t ex2_h2(uint32_t h) {
-  uint32_t r;
-  asm("ex2.approx.f16x2 %0, %1;" : "=r"(r) : "r"(h));
-  return r;
-}
-__device__ __forceinline__ uint32_t e4m3x2_of_h2(uint32_t h) {  // low half -> low byte
-  uint16_t r;
-  asm("cvt.rn.satfinite.e4m3x2.f16x2 %0, %1;" : "=h"(r) : "r"(h));
-  return r;
-}
-// one P~ word (4 keys) in the f16x2 modes
-__device__ __forceinline__ uint32_t group_h2(const float* v, f2 cc, f2 bb) {
-  const f2 m = fma2(f2{v[0], v[1]}, cc, bb);
-  const f2 n = fma2(f2{v[2], v[3]}, cc, bb);
-  if constexpr (FPSA_EX2_MODE == 1) {
-    return e4m3x2_of_h2(ex2_h2(h2_of(m))) | (e4m3x2_of_h2(ex2_h2(h2_of(n))) << 16);
-  } else {
-    const f2 e = f2{ex2(m.x), ex2(m.y)};
-    uint16_t lo;
-    asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(lo) : "f"(e.y), "f"(e.x));
-    return (uint32_t)lo | (e4m3x2_of_h2(ex2_h2(h2_of(n))) << 16);
-  }
-}
 template <int C>
 __device__ __forceinline__ void softmax_chunk32(const uint32_t* s, f2 cc, f2 bb, float cs, float bs, uint32_t* w) {
 #pragma unroll
   for (int q = 0; q < 8; ++q) {
     const float* v = reinterpret_cast<const float*>(s + 4 * q);
-    if constexpr (FPSA_EX2_MODE != 0) {
-      w[8 * C + q] = group_h2(v, cc, bb);
-      continue;
-    }
     constexpr int kPer8 = FPSA_POLY_PER8;
     f2 m;
     if (kPer8 == 8 || (kPer8 == 6 && (q & 1))) {  // columns 0 and 1 on the polynomial too
@@ -334,10 +296,6 @@ __device__ __forceinline__ void softmax_chunk32_split(const uint32_t* s, int spl
     const f2 cc = sb ? ccb : cca;
     const float cs = sb ? csb : csa;
     const float* v = reinterpret_cast<const float*>(s + 4 * q);
-    if constexpr (FPSA_EX2_MODE != 0) {
-      w[8 * C + q] = group_h2(v, cc, bb);
-      continue;
-    }
     constexpr int kPer8 = FPSA_POLY_PER8;
     f2 m;
     if (kPer8 == 8 || (kPer8 == 6 && (q & 1))) {
