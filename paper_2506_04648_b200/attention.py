@@ -119,20 +119,20 @@ def _padded_dim(d: int) -> int:
 def _cached_plan(kind: str, tmap: TileMap, config: ForwardConfig, dp: int, device):
     import torch
 
-    from .ops import FpsaPlan, PassthroughPlan
+    from .ops import FpsaPlan, PassthroughPlan, cache_get
 
     stream = torch.cuda.current_stream(device).cuda_stream
     key = (kind, tmap.grid.dims, tmap.scheme.dims, config.window.dims, dp, config.fmt.name, config.p_mode,
            float(config.tau), str(device), stream, threading.get_ident())
+
+    def make():
+        if kind == "passthrough":
+            return PassthroughPlan(tmap.grid.dims, tmap.scheme.dims, config.window, 1, dp, device=device)
+        return FpsaPlan(tmap.grid.dims, tmap.scheme.dims, config.window, 1, dp, config.fmt, device=device,
+                        tau=config.tau, p_mode=config.p_mode)
+
     with _PLAN_LOCK:
-        plan = _PLAN_CACHE.get(key)
-        if plan is None:
-            if kind == "passthrough":
-                plan = PassthroughPlan(tmap.grid.dims, tmap.scheme.dims, config.window, 1, dp, device=device)
-            else:
-                plan = FpsaPlan(tmap.grid.dims, tmap.scheme.dims, config.window, 1, dp, config.fmt, device=device,
-                                tau=config.tau, p_mode=config.p_mode)
-            _PLAN_CACHE[key] = plan
+        plan = cache_get(_PLAN_CACHE, key, make)
     return plan
 
 

@@ -442,6 +442,18 @@ def device_fidelity(ref, approx, layout: str = "lhd", stream=None) -> list[tuple
 
 
 _PLANS: dict = {}
+_PLANS_MAX = 8  # cached plans (each holds the code buffers of its shape); the least recently used is dropped
+
+
+def cache_get(cache: dict, key, make, limit: int = _PLANS_MAX):
+    """LRU lookup shared by the plan caches of fps_attention and fp8_sparse_forward."""
+    plan = cache.pop(key, None)
+    if plan is None:
+        plan = make()
+        while len(cache) >= limit:
+            cache.pop(next(iter(cache)))
+    cache[key] = plan  # most recent last
+    return plan
 
 
 def fps_attention(q, k, v, grid, tile, window, *, fmt: Fp8Format = E4M3, softmax_scale: float | None = None,
@@ -466,10 +478,7 @@ def fps_attention(q, k, v, grid, tile, window, *, fmt: Fp8Format = E4M3, softmax
     stream = torch.cuda.current_stream(q.device)
     key = (tuple(grid), tuple(tile), win.dims, H, d, fmt.name, str(q.device), tau, stream.cuda_stream,
            threading.get_ident())
-    plan = _PLANS.get(key)
-    if plan is None:
-        plan = FpsaPlan(grid, tile, win, H, d, fmt, device=q.device, tau=tau)
-        _PLANS[key] = plan
+    plan = cache_get(_PLANS, key, lambda: FpsaPlan(grid, tile, win, H, d, fmt, device=q.device, tau=tau))
     out = torch.empty(q.shape, dtype=out_dtype or q.dtype, device=q.device)
     for b in range(B):
         sl = (lambda x: x[b]) if batched else (lambda x: x)

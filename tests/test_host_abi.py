@@ -288,3 +288,14 @@ def test_fidelity_from_sums_matches_reference_metrics(fpsa):
         fpsa.fidelity_from_sums(0, 0, 0, 0, 0.0, 0.0, n=4)
     assert fpsa.fidelity_from_sums(0, 1, 0, 1, 1.0, 0.0, n=4)[0] == 0.0  # one zero vector: cosine 0
     assert fpsa.fidelity_from_sums(*sums[:3], 0.0, *sums[4:], n=x.size)[2] == math.inf
+
+
+def test_plan_cache_is_lru_bounded():
+    from paper_2506_04648_b200.ops import cache_get
+
+    cache, made = {}, []
+    for k in [1, 2, 3, 1, 4, 5]:
+        cache_get(cache, k, lambda k=k: made.append(k) or k, limit=3)
+    assert made == [1, 2, 3, 4, 5]          # 1 was a hit the second time
+    assert list(cache) == [1, 4, 5]         # least recently used (2, then 3) dropped
+    assert len(cache) == 3 and 5 in cache and 2 not in cache
