@@ -56,6 +56,8 @@ def parse():
     ap.add_argument("--ulysses", action="store_true", help="sequence-sharded inputs + all-to-all (C3)")
     ap.add_argument("--ulysses-chunk", type=int, default=1,
                     help="heads per pipelined all-to-all chunk (0: one all-to-all per tensor, no overlap)")
+    ap.add_argument("--p-mode", default="onepass", choices=["onepass", "normalized"],
+                    help="softmax-weight semantics (normalized: the reference's arithmetic, f32 output)")
     ap.add_argument("--dump-out", default=None,
                     help="directory: each rank writes sha256 of its heads' outputs (head-parallel runs)")
     return ap.parse_args()
@@ -317,7 +319,7 @@ def main():
             gen.manual_seed(1234 + h0 + j)
             for x in (q, k, v):
                 x[:, j].copy_(torch.randn((Lr, d), generator=gen, device=dev))
-    out = torch.empty_like(q)
+    out = torch.empty_like(q) if args.p_mode == "onepass" else torch.empty(q.shape, dtype=torch.float32, device=dev)
     if args.ulysses:
         uly = UlyssesAttention(grid, tile, win, H, d, device=dev, tau=args.tau,
                                chunk_heads=args.ulysses_chunk or None)
@@ -326,7 +328,7 @@ def main():
         def step(q_, k_, v_, out_):
             out_.copy_(uly(q_, k_, v_))
     else:
-        plan = fpsa.FpsaPlan(grid, tile, win, Hr, d, tau=args.tau, device=dev)
+        plan = fpsa.FpsaPlan(grid, tile, win, Hr, d, tau=args.tau, device=dev, p_mode=args.p_mode)
 
         def step(q_, k_, v_, out_):
             plan.quantize(q_, k_, v_, "lhd")
@@ -454,6 +456,7 @@ def main():
             "workload": args.config, "grid": grid, "heads": H, "d": d, "tile": tile, "window": win,
             "density": plan.density, "global_batch": 1, "heads_per_gpu": Hr if not args.ulysses else H // world,
             "flops_per_step": total_flops, "flops_per_step_rank0": flops, "tau_log2": args.tau,
+            "p_mode": args.p_mode,
             "parallelism": (f"ulysses: sequence-sharded inputs, NCCL all-to-all seq<->head, {world} ranks"
                             if args.ulysses else f"head-parallel, {world} rank(s), no collective"),
             "l2": "inputs larger than L2 (bf16 q,k,v = %.2f GB per rank; codes %.2f GB)" % (
