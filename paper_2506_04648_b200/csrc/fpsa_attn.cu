@@ -247,9 +247,14 @@ __device__ __forceinline__ uint64_t desc_mnmajor(uint32_t addr) {
 //   [4] softmax: S load (tcgen05.ld + wait) cycles   [7] MMA: cycles waiting for K/V
 #endif
 
-// Correctly rounded f32 exp (through f64): the normalised-P mode's exp.  Not inlined: it is called per
-// element of a fully unrolled row and would otherwise multiply the code size.
+// The normalised-P mode's exp: CUDA's accurate expf (<= 2 ulp, like numpy's own f32 exp against the
+// correctly rounded value; an f64 exp rounded to f32 measured 34x slower for the same parity).
+// Not inlined: it is called per element of a fully unrolled row and would otherwise multiply the code size.
+#ifndef FPSA_NORM_EXP_F64
+__device__ __noinline__ float exp_f32_cr(float x) { return expf(x); }
+#else
 __device__ __noinline__ float exp_f32_cr(float x) { return __double2float_rn(exp((double)x)); }
+#endif
 
 // Normalised-P pass 2: f64 sum of exp(S * c - m) over the first ncol of NC S columns; columns < split use
 // factor ca, the others cb (a packed block's two key tiles).
