@@ -155,3 +155,22 @@ def quantize_dequantize(x, scale, fmt: Fp8Format):
     if scalar or (not isinstance(x, (np.ndarray, torch.Tensor)) and np.ndim(x) == 0):
         return float(out.item())
     return out.cpu().numpy().reshape(shape) if host else out.reshape(shape)
+
+
+def code_table(fmt: Fp8Format) -> np.ndarray:
+    """All 256 decoded values in code order, float64, NaN patterns as nan (fp8.py:214-216); decoded on the
+    GPU (fpsa_decode, whose NaN flag is expected here)."""
+    from . import _lib
+
+    torch = _torch()
+    codes = torch.arange(256, dtype=torch.uint8, device="cuda")
+    out = torch.empty(256, dtype=torch.float64, device="cuda")
+    err = torch.zeros(1, dtype=torch.int32, device="cuda")
+    _lib.check(_lib.lib().fpsa_decode(codes.data_ptr(), 256, fmt.abi_id, None, out.data_ptr(), _lib.F64,
+                                      err.data_ptr(), torch.cuda.current_stream().cuda_stream))
+    return out.cpu().numpy()
+
+
+def is_nan_code(code, fmt: Fp8Format):
+    """True where a byte is one of the format's NaN patterns (fp8.py:208-211)."""
+    return np.isnan(code_table(fmt)[np.asarray(code, dtype=np.uint8)])

@@ -43,6 +43,9 @@ def test_encode_decode_vs_reference_goldens(fpsa, codec_golden, fmt):
     else:
         assert fpsa.encode(-np.inf, F) == 0xFC
     assert isinstance(fpsa.encode(1.0, F), int) and isinstance(fpsa.decode(0x38, F), float)
+    ct = fpsa.code_table(F)
+    assert np.array_equal(np.isnan(ct), np.isnan(table)) and np.array_equal(ct[ok], table[ok])
+    assert np.array_equal(fpsa.is_nan_code(np.arange(256), F), ~ok)
 
 
 def test_quantize_dequantize_and_dequantize_tensor(fpsa):
