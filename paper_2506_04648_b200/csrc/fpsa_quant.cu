@@ -539,6 +539,7 @@ constexpr int kTmaStageBytes = kTmaMaxRows * kTmaD * 2;
 constexpr uint32_t kTmaQueueCap = 2048;
 
 struct TmaQuantArgs {
+  int32_t whole_tile;  // one TMA box per tile (5D natural-order view / tv-row box) instead of one per w-run
   uint8_t* codes[3];
   double* scales[3];
   int32_t channel[3];
@@ -585,12 +586,24 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
         const void* tm = z == 0 ? (const void*)&tm0 : (z == 1 ? (const void*)&tm1 : (const void*)&tm2);
         uint8_t* dst = smem + st * kTmaStageBytes;
         mbar_arrive_expect_tx(&full[st], (uint32_t)g.tv * kTmaD * 2);
-        const int32_t base = tile_base(g, u);
-        for (int32_t r = 0; r < runs; ++r) {
-          // run r = (lt, lh) of the tile; in tile order runs are consecutive rows
-          const int32_t lt = r / g.sh, lh = r - lt * g.sh;
-          const int32_t tok = g.natural ? base + (lt * g.gh + lh) * g.gw : base + r * g.sw;
-          tma_load_3d(dst + r * g.sw * kTmaD * 2, tm, 0, tok, h, &full[st]);
+        if (a.whole_tile) {
+          // one box per tile: natural order through the 5D view (c, head, w, h, t) with box
+          // (128, 1, sw, sh, st), which lands the tile in its local (t, h, w) row order; tile order
+          // through the 3D view with a box of tv rows
+          if (g.natural) {
+            const int32_t ut = u / (g.dh * g.dw), uh = (u / g.dw) % g.dh, uw = u % g.dw;
+            tma_load_5d(dst, tm, 0, h, uw * g.sw, uh * g.sh, ut * g.st, &full[st]);
+          } else {
+            tma_load_3d(dst, tm, 0, u * g.tv, h, &full[st]);
+          }
+        } else {
+          const int32_t base = tile_base(g, u);
+          for (int32_t r = 0; r < runs; ++r) {
+            // run r = (lt, lh) of the tile; in tile order runs are consecutive rows
+            const int32_t lt = r / g.sh, lh = r - lt * g.sh;
+            const int32_t tok = g.natural ? base + (lt * g.gh + lh) * g.gw : base + r * g.sw;
+            tma_load_3d(dst + r * g.sw * kTmaD * 2, tm, 0, tok, h, &full[st]);
+          }
         }
       }
     }
@@ -717,6 +730,32 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 
 // [heads][L][d] view of a bf16 input with token / head strides (elements).
+// One box per tile.  Natural order: 5D view (c, head, w, h, t) of a [t][h][w] token grid with box
+// (128, 1, sw, sh, st); tile order: 3D view [heads][L][d] with a box of tv rows.
+bool make_tile_map(CUtensorMap* m, const void* x, const Geometry& g, int32_t heads, int64_t ts, int64_t hs) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  const int64_t hstride = (hs > 0 ? hs : ts) * 2;
+  if (g.natural) {
+    cuuint64_t dims[5] = {(cuuint64_t)kTmaD, (cuuint64_t)heads, (cuuint64_t)g.gw, (cuuint64_t)g.gh, (cuuint64_t)g.gt};
+    cuuint64_t strides[4] = {(cuuint64_t)hstride, (cuuint64_t)ts * 2, (cuuint64_t)ts * 2 * g.gw,
+                             (cuuint64_t)ts * 2 * g.gw * g.gh};
+    cuuint32_t box[5] = {(cuuint32_t)kTmaD, 1, (cuuint32_t)g.sw, (cuuint32_t)g.sh, (cuuint32_t)g.st};
+    cuuint32_t es[5] = {1, 1, 1, 1, 1};
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void*>(x), dims, strides, box, es,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  }
+  const int64_t L = (int64_t)g.gt * g.gh * g.gw;
+  cuuint64_t dims[3] = {(cuuint64_t)kTmaD, (cuuint64_t)L, (cuuint64_t)heads};
+  cuuint64_t strides[2] = {(cuuint64_t)ts * 2, (cuuint64_t)hstride};
+  cuuint32_t box[3] = {(cuuint32_t)kTmaD, (cuuint32_t)g.tv, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(x), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 bool make_input_map(CUtensorMap* m, const void* x, int64_t L, int32_t heads, int64_t ts, int64_t hs, int32_t sw) {
   auto fn = encode_fn();
   if (!fn) return false;
@@ -738,14 +777,22 @@ bool try_tma_quant(const void* const* xs, int njobs, int dtype, int64_t ts, int6
   if (heads > 1 && hs == 0) return false;
   const int64_t L = (int64_t)g.gt * g.gh * g.gw;
   CUtensorMap tm[3];
-  for (int i = 0; i < 3; ++i)
-    if (!make_input_map(&tm[i], xs[i < njobs ? i : 0], L, heads, ts, hs, g.sw)) return false;
+  static const bool runs_only = getenv("FPSA_QUANT_RUNS") != nullptr;  // measurement switch: one box per w-run
+  TmaQuantArgs aa = a;
+  aa.whole_tile = !runs_only && g.st <= 256 && g.sh <= 256 && g.sw <= 256;
+  for (int i = 0; i < 3; ++i) {
+    const void* x = xs[i < njobs ? i : 0];
+    if (aa.whole_tile && !make_tile_map(&tm[i], x, g, heads, ts, hs)) aa.whole_tile = 0;
+  }
+  if (!aa.whole_tile)
+    for (int i = 0; i < 3; ++i)
+      if (!make_input_map(&tm[i], xs[i < njobs ? i : 0], L, heads, ts, hs, g.sw)) return false;
   const int smem = kTmaStages * kTmaStageBytes;
   auto kern = fmt == FPSA_E4M3 ? quant_tma_kernel<FPSA_E4M3> : quant_tma_kernel<FPSA_E5M2>;
   if (ensure_smem_attr(reinterpret_cast<const void*>(kern), smem, "quant_tma_kernel") != FPSA_OK) return false;
   const int64_t items = (int64_t)njobs * heads * g.M;
   const int grid = (int)std::min<int64_t>(items, device_sm_count());
-  kern<<<grid, kTmaThreads, smem, st>>>(tm[0], tm[1], tm[2], g, a);
+  kern<<<grid, kTmaThreads, smem, st>>>(tm[0], tm[1], tm[2], g, aa);
   return true;
 }
 
