@@ -289,6 +289,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                      const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ SegMaps seg,
                      const AttnParams p) {
   using S = Smem<D>;
+  static_assert(kPingPong || (!NORM && !PACKED), "the normalised-P and packed-key paths are ping-pong only");
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   __shared__ uint64_t bar_q[2], bar_qfree[2];  // query-block buffer (item parity): loaded / no longer read
