@@ -72,6 +72,9 @@
 #ifndef FPSA_MMA_ONE_ELECT
 #define FPSA_MMA_ONE_ELECT 1
 #endif
+#ifndef FPSA_PACK_FASTPATH
+#define FPSA_PACK_FASTPATH 1  // packed blocks inside one key tile take the per-tile softmax code
+#endif
 
 
 namespace fpsa {
@@ -807,6 +810,20 @@ __global__ void __launch_bounds__(kThreads, 1)
                 load_s_all<64>(s_row + 64, sreg);
                 tmem_wait_ld();
                 sat |= compute_p_regs<64>(sreg, max(nvalid - 64, 0), ca, bias, w + 16);
+              }
+            } else if (FPSA_PACK_FASTPATH && split == kBlk && nvalid == kBlk) {
+              // a packed block inside one key tile: the per-tile code (no factor selects, nothing to mask)
+              {
+                uint32_t sreg[64];
+                load_s_all<64>(s_row, sreg);
+                tmem_wait_ld();
+                sat |= compute_p_regs<64>(sreg, 64, ca, bias, w);
+              }
+              {
+                uint32_t sreg[64];
+                load_s_all<64>(s_row + 64, sreg);
+                tmem_wait_ld();
+                sat |= compute_p_regs<64>(sreg, 64, ca, bias, w + 16);
               }
             } else {
               {
