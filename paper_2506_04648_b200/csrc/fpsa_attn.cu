@@ -72,6 +72,9 @@
 #ifndef FPSA_MMA_ONE_ELECT
 #define FPSA_MMA_ONE_ELECT 1
 #endif
+#ifndef FPSA_EARLY_QK
+#define FPSA_EARLY_QK 0  // P~ in its own TMEM columns, QK(j+2) issued once S(j) is in registers (D = 128)
+#endif
 #ifndef FPSA_PACK_FASTPATH
 #define FPSA_PACK_FASTPATH 1  // packed blocks inside one key tile take the per-tile softmax code
 #endif
@@ -299,6 +302,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __shared__ uint64_t bar_o, bar_ofree;        // O complete for the item / epilogue has read O
   __shared__ uint64_t bar_kv_full[kStages], bar_kv_empty[kStages];
   __shared__ uint64_t bar_s_full[2], bar_p_ready[2];  // by S buffer / step parity
+  __shared__ uint64_t bar_s_free[2], bar_p_free[2];   // early QK: S(j) loaded by its owners / PV(j) done
   __shared__ uint32_t s_tmem;
   __shared__ float s_xchg[kParts][kBlk];  // [part][row] exchange between the warps of a row
   // per-item metadata, prefetched by the helper warp one item ahead (slot = item parity)
@@ -341,6 +345,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&bar_qfree[i], 1);
       mbar_init(&bar_s_full[i], 1);
       mbar_init(&bar_p_ready[i], kPingPong ? kSoftmaxWarps / 2 : kSoftmaxWarps);  // one arrival per writing warp
+      mbar_init(&bar_s_free[i], kSoftmaxWarps / 2);
+      mbar_init(&bar_p_free[i], 1);
     }
     mbar_init(&bar_o, 1);
     mbar_init(&bar_ofree, kSoftmaxWarps);
@@ -378,6 +384,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tm_o = tmem;  // O: columns 0..D-1, row sums of P~: D..D+15
   // S buffers at columns 256 and 384 (computed, not indexed: a local array would live in memory)
   auto tm_s = [tmem](uint32_t g) { return tmem + 256u + 128u * (g & 1u); };
+  // early-QK mode: P~(j) in its own 32 columns (160 / 192), so S(j)'s buffer is free once loaded
+  constexpr bool kEarly = FPSA_EARLY_QK && kPingPong && D == 128;
+  auto tm_p = [tmem](uint32_t g) { return tmem + 160u + 32u * (g & 1u); };
   const float tau = p.exact ? 0.0f : p.tau;
 
   if (warp >= kSoftmaxWarps) regs_dec<kRegsProducer>();  // producer warpgroup: TMA, MMA, 2 idle warps
@@ -468,6 +477,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       // S(step gg) = Q K^T into TMEM buffer gg % 2
       auto issue_qk = [&](uint32_t gg) {
         attn_wait(&bar_kv_full[qk_st], qk_ph);
+        if (kEarly && gg >= 2) attn_wait(&bar_s_free[gg & 1], ((gg - 2) >> 1) & 1);  // S(gg - 2) loaded
         tc_fence_after();
         const uint64_t dk = dk0 + qk_st * kTileU;
         // N = 128 for every block: a tile's last block reads zero K rows past tv (S = 0 there,
@@ -496,6 +506,47 @@ __global__ void __launch_bounds__(kThreads, 1)
         // Everything that does not depend on P~(j) is done before waiting for it: the K/V-full wait and
         // descriptors of QK(j+2), the V descriptor of PV(j), the O-free wait. After p_ready(j) the warp
         // only issues PV(j), QK(j+2) and the commits (the issue path is the step's critical path).
+        if constexpr (kEarly) {
+          // QK(j+2) as soon as the owners of S(j) have it in registers, then PV(j) from its P~ buffer
+          for (int32_t s = 0; s < steps; ++s) {
+            const uint32_t gs = g + s;
+            const bool do_qk = s + 2 < steps;
+            if (do_qk) {
+              attn_wait(&bar_kv_full[qk_st], qk_ph);
+              const uint64_t dk = dk0 + qk_st * kTileU;
+              attn_wait(&bar_s_free[gs & 1], (gs >> 1) & 1);
+              tc_fence_after();
+#ifndef FPSA_NO_MMA
+              mma_f8_ss_x4_w(tm_s(gs), dq, dq + 2, dq + 4, dq + 6, dk, dk + 2, dk + 4, dk + 6, idesc_qk, 0u);
+#endif
+              mma_commit_w(&bar_s_full[gs & 1]);
+              if (++qk_st == kStages) {
+                qk_st = 0;
+                qk_ph ^= 1;
+              }
+              if (s + 3 == steps) mma_commit_w(&bar_qfree[qbuf]);
+            }
+            constexpr uint64_t kVk = 32 * D / 16;
+            const uint64_t dv = (!PACKED && bp == p.nb - 1 ? dvt0 : dv0) + pv_st * kVStageStep;
+            if (s == pv0 && iter > 0) attn_wait(&bar_ofree, (iter - 1) & 1);  // the previous item's epilogue read O
+            FPSA_TL(9, 0, gs);
+            attn_wait(&bar_p_ready[gs & 1], (gs >> 1) & 1);
+            FPSA_TL(9, 1, gs);
+            tc_fence_after();
+            const uint32_t tp = tm_p(gs);
+#ifndef FPSA_NO_MMA
+            if (s >= pv0)
+              mma_f8_ts_x4_w(tm_o, tp, tp + 8, tp + 16, tp + 24, dv, dv + kVk, dv + 2 * kVk, dv + 3 * kVk, idesc_pv,
+                             s > pv0 ? 1u : 0u);
+#endif
+            FPSA_TL(9, 2, gs);
+            mma_commit_w(&bar_kv_empty[pv_st]);
+            mma_commit_w(&bar_p_free[gs & 1]);  // every step, so its phases count steps
+            FPSA_TL(9, 3, gs);
+            if (++pv_st == kStages) pv_st = 0;
+            if (++bp == p.nb) bp = 0;
+          }
+        } else
         for (int32_t s = 0; s < steps; ++s) {
           const uint32_t gs = g + s;
           const bool do_qk = s + 2 < steps;
@@ -719,7 +770,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             m_acc = fmaxf(m_acc, block_max_split(s_row, split, nvalid, ca, cb));
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&bar_p_ready[gj & 1]);  // S consumed
+            if (lane == 0) {
+              if (kEarly) mbar_arrive(&bar_s_free[gj & 1]);
+              mbar_arrive(&bar_p_ready[gj & 1]);  // S consumed
+            }
           }
           g += n_kv;
           m_ref = row_max(m_acc);
@@ -743,7 +797,10 @@ __global__ void __launch_bounds__(kThreads, 1)
               }
               tc_fence_before();
               __syncwarp();
-              if (lane == 0) mbar_arrive(&bar_p_ready[gj & 1]);  // S consumed
+              if (lane == 0) {
+                if (kEarly) mbar_arrive(&bar_s_free[gj & 1]);
+                mbar_arrive(&bar_p_ready[gj & 1]);  // S consumed
+              }
             }
             g += n_kv;
             s_xchg_d[part][row] = l_acc;
@@ -789,61 +846,46 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc_fence_after();
             const float bias = kLog2_448 - m_ref - tau;
             uint32_t w[kBlk / 4];
-            if constexpr (NORM) {
-#pragma unroll
-              for (int hb = 0; hb < 2; ++hb) {
-                uint32_t sreg[64];
-                load_s_all<64>(s_row + 64 * hb, sreg);
-                tmem_wait_ld();
+            const bool fast = FPSA_PACK_FASTPATH && PACKED && split == kBlk && nvalid == kBlk;
+            // P~ words of one 64-column half (hb) from its S registers
+            auto half = [&](int hb, const uint32_t* sreg) {
+              if constexpr (NORM) {
                 compute_p_norm<64>(sreg, split - 64 * hb, nvalid - 64 * hb, ca, cb, m_ref, l_norm, w + 16 * hb);
+              } else if constexpr (!PACKED) {
+                // one key tile per block; padding keys need no mask (zero V rows, zero rows of the tail ones atom)
+                sat |= compute_p_regs<64>(sreg, hb ? max(nvalid - 64, 0) : min(nvalid, 64), ca, bias, w + 16 * hb);
+              } else {
+                if (fast)  // a packed block inside one key tile: the per-tile code (no selects, no mask)
+                  sat |= compute_p_regs<64>(sreg, 64, ca, bias, w + 16 * hb);
+                else
+                  sat |= compute_p_regs2<64>(sreg, split - 64 * hb, nvalid - 64 * hb, ca, cb, bias, w + 16 * hb);
               }
-            } else if constexpr (!PACKED) {
-              // one key tile per block; padding keys need no mask (zero V rows, zero rows of the tail ones atom)
-              {
-                uint32_t sreg[64];
-                load_s_all<64>(s_row, sreg);
-                tmem_wait_ld();
-                sat |= compute_p_regs<64>(sreg, min(nvalid, 64), ca, bias, w);
-              }
-              {
-                uint32_t sreg[64];
-                load_s_all<64>(s_row + 64, sreg);
-                tmem_wait_ld();
-                sat |= compute_p_regs<64>(sreg, max(nvalid - 64, 0), ca, bias, w + 16);
-              }
-            } else if (FPSA_PACK_FASTPATH && split == kBlk && nvalid == kBlk) {
-              // a packed block inside one key tile: the per-tile code (no factor selects, nothing to mask)
-              {
-                uint32_t sreg[64];
-                load_s_all<64>(s_row, sreg);
-                tmem_wait_ld();
-                sat |= compute_p_regs<64>(sreg, 64, ca, bias, w);
-              }
-              {
-                uint32_t sreg[64];
-                load_s_all<64>(s_row + 64, sreg);
-                tmem_wait_ld();
-                sat |= compute_p_regs<64>(sreg, 64, ca, bias, w + 16);
-              }
-            } else {
-              {
-                uint32_t sreg[64];
-                load_s_all<64>(s_row, sreg);
-                tmem_wait_ld();
-                sat |= compute_p_regs2<64>(sreg, split, nvalid, ca, cb, bias, w);
-              }
-              {
-                uint32_t sreg[64];
-                load_s_all<64>(s_row + 64, sreg);
-                tmem_wait_ld();
-                sat |= compute_p_regs2<64>(sreg, split - 64, nvalid - 64, ca, cb, bias, w + 16);
-              }
+            };
+            {
+              uint32_t sreg[64];
+              load_s_all<64>(s_row, sreg);
+              tmem_wait_ld();
+              half(0, sreg);
             }
-#ifdef FPSA_TRACE
-            w_c += clock64() - tc0;
-#endif
-            FPSA_TL(warp, 2, g_own);
-            tmem_st32(s_row, w);  // P~ of the 128 keys over the first 32 columns of this S buffer
+            {
+              uint32_t sreg[64];
+              load_s_all<64>(s_row + 64, sreg);
+              tmem_wait_ld();
+              if constexpr (kEarly) {  // S(j) is in registers: its buffer may take S(j+2)
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&bar_s_free[g_own & 1]);
+              }
+              half(1, sreg);
+            }
+            if constexpr (kEarly) {
+              // P~(j) into its own columns once PV(j - 2) has read them
+              if (g_own >= 2) attn_wait(&bar_p_free[g_own & 1], ((g_own - 2) >> 1) & 1);
+              tc_fence_after();
+              tmem_st32(tm_p(g_own) + lane_off, w);
+            } else {
+              tmem_st32(s_row, w);  // P~ of the 128 keys over the first 32 columns of this S buffer
+            }
             tmem_wait_st();
             tc_fence_before();
             __syncwarp();
