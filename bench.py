@@ -37,6 +37,9 @@ CONFIGS = {
     "wan14b_720p_w333": ((21, 45, 80), 40, 128, (3, 5, 16), (3, 3, 3)),
     "wan13b_480p": ((21, 30, 52), 12, 128, (3, 10, 4), (3, 3, 5)),
     "hunyuan_720p": ((33, 45, 80), 24, 128, (3, 5, 16), (5, 5, 3)),
+    # the C4 schedule's early and late regimes (schedule_runner.c4_schedule) at the 14B 720p grid
+    "c4_early": ((21, 45, 80), 40, 128, (7, 15, 16), (3, 3, 1)),
+    "c4_late": ((21, 45, 80), 40, 128, (7, 9, 8), (3, 3, 3)),
 }
 
 

@@ -384,6 +384,118 @@ __global__ void __launch_bounds__(kQuantThreads, 1)
   for (int32_t row = g.tv + warp; row < g.pitch; row += kQuantWarps) store_codes<VEC>(out + (int64_t)row * D, 0u);
 }
 
+// ---------------------------------------------------------------------------
+// Chunked two-pass quantiser for tiles the TMA kernel cannot stage (more than
+// 256 tokens, e.g. the C4 early / late regimes' 1680- and 504-token tiles):
+// every CTA takes 128 rows of one tile, pass 1 reduces the chunk's |x| max
+// into the tile's slot (atomicMax on the f32 bits), pass 2 -- a second
+// launch -- encodes the chunk with the tile's scale, pass 3 turns the slots
+// into the f64 scales.  The slot of tile (h, u) is the low word of its own
+// (zeroed) f64 scale, so no workspace is needed.  Streaming grids of many
+// small CTAs instead of one CTA walking a whole tile twice.
+constexpr int kChunkRows = 128;
+constexpr int kChunkThreads = 256;
+constexpr int kChunkWarps = kChunkThreads / 32;
+
+// element offset of local row r of tile u (natural or tile order)
+__device__ __forceinline__ int64_t chunk_row_offset(const Geometry& g, int32_t r, int64_t ts) {
+  return (g.natural ? (int64_t)local_offset(g, r) : (int64_t)r) * ts;
+}
+
+__device__ __forceinline__ uint32_t* amax_slot(const QuantJob& job, int32_t h, int32_t u, int32_t M) {
+  return reinterpret_cast<uint32_t*>(job.scales + (int64_t)h * M + u);
+}
+
+// pass 3: f64 scales from the tile max slots, in place
+template <int FMT>
+__global__ void scales_from_amax_kernel(double* scales, int64_t n, int32_t* err) {
+  constexpr double kMax = FMT == FPSA_E4M3 ? 448.0 : 57344.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    float peak = __uint_as_float(*reinterpret_cast<const uint32_t*>(scales + i));
+    if (!(peak <= FLT_MAX)) {
+      if (err) atomicOr(err, 1);
+      peak = 0.0f;
+    }
+    scales[i] = scale_of(peak, kMax);
+  }
+}
+
+template <typename T, int D>
+__global__ void __launch_bounds__(kChunkThreads) tile_amax_chunk_kernel(Geometry g, QuantArgs a, int32_t chunks) {
+  constexpr int VEC = D / 32;
+  using V = Vec<T, VEC>;
+  __shared__ int64_t s_off[kChunkRows];
+  __shared__ uint32_t s_m;
+  const int32_t u = blockIdx.x / chunks, c = blockIdx.x % chunks, h = blockIdx.y, z = blockIdx.z;
+  const QuantJob job = a.job[z];
+  if (job.channel) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int32_t r0 = c * kChunkRows, nr = min(kChunkRows, g.tv - r0);
+  if (threadIdx.x < nr) s_off[threadIdx.x] = chunk_row_offset(g, r0 + threadIdx.x, job.ts);
+  if (threadIdx.x == 0) s_m = 0u;
+  __syncthreads();
+  const T* xt = static_cast<const T*>(job.x) + (int64_t)h * job.hs + (int64_t)tile_base(g, u) * job.ts + lane * VEC;
+  uint32_t m = 0;
+#pragma unroll 4
+  for (int32_t r = warp; r < nr; r += kChunkWarps) m = absmax_bits<T, VEC>(V::load(xt + s_off[r]), m);
+  m = __float_as_uint(bits_to_peak<T>(m));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if (lane == 0) atomicMax(&s_m, m);
+  __syncthreads();
+  if (threadIdx.x == 0) atomicMax(amax_slot(job, h, u, g.M), s_m);
+}
+
+template <typename T, int D, int FMT>
+__global__ void __launch_bounds__(kChunkThreads) encode_chunk_kernel(Geometry g, QuantArgs a, int32_t chunks) {
+  constexpr int VEC = D / 32;
+  constexpr double kMax = FMT == FPSA_E4M3 ? 448.0 : 57344.0;
+  using V = Vec<T, VEC>;
+  __shared__ int64_t s_off[kChunkRows];
+  const int32_t u = blockIdx.x / chunks, c = blockIdx.x % chunks, h = blockIdx.y, z = blockIdx.z;
+  const QuantJob job = a.job[z];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int32_t r0 = c * kChunkRows, nr = min(kChunkRows, g.tv - r0);
+  if (threadIdx.x < nr) s_off[threadIdx.x] = chunk_row_offset(g, r0 + threadIdx.x, job.ts);
+  __syncthreads();
+  float pk[VEC];
+  Bracket b[VEC];
+  if (!job.channel) {
+    float peak = __uint_as_float(*amax_slot(job, h, u, g.M));
+    if (!(peak <= FLT_MAX)) peak = 0.0f;  // reported by scales_from_amax_kernel
+    const Bracket bb = bracket_f32<FMT>(peak);
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) {
+      pk[e] = peak;
+      b[e] = bb;
+    }
+  } else {
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) {
+      const float peak = __uint_as_float(a.amax[(int64_t)h * D + lane * VEC + e]);
+      pk[e] = peak <= FLT_MAX ? peak : 0.0f;
+      b[e] = bracket_f32<FMT>(pk[e]);
+      if (u == 0 && c == 0 && warp == 0) job.scales[(int64_t)h * D + lane * VEC + e] = scale_of(pk[e], kMax);
+    }
+  }
+  bool fast_ok = true;
+#pragma unroll
+  for (int e = 0; e < VEC; ++e) fast_ok &= b[e].ok;
+  const T* xt = static_cast<const T*>(job.x) + (int64_t)h * job.hs + (int64_t)tile_base(g, u) * job.ts + lane * VEC;
+  uint8_t* out = job.codes + ((int64_t)h * g.M + u) * g.pitch * D + lane * VEC;
+#pragma unroll 4
+  for (int32_t r = warp; r < nr; r += kChunkWarps) {
+    float v[VEC];
+    V::unpack(V::load(xt + s_off[r]), v);
+    bool slow = !fast_ok;
+    uint32_t code = encode_fast<FMT, VEC>(v, b, slow);
+    if (slow) code = encode_slow<FMT, VEC>(v, pk);  // rare: exact f64 path (ties of bf16 data)
+    store_codes<VEC>(out + (int64_t)(r0 + r) * D, code);
+  }
+  if (c == chunks - 1)  // the tile slot's padding rows
+    for (int32_t r = g.tv + warp; r < g.pitch; r += kChunkWarps) store_codes<VEC>(out + (int64_t)r * D, 0u);
+}
+
 // V pass A: per-(head, channel) |x| max over all tokens (bit domain, atomicMax).
 template <typename T, int D>
 __global__ void __launch_bounds__(kQuantThreads)
@@ -856,6 +968,21 @@ void dispatch(int dtype, int32_t d, int fmt, Args&&... args) {
   }
 }
 template <typename T, int D, int FMT>
+struct RunChunked {
+  // jobs with channel == 0 must have zeroed scale arrays (their words hold the tile maxima until pass 3)
+  static void run(const Geometry& g, int32_t heads, const QuantArgs& a, int njobs, cudaStream_t st) {
+    const int32_t chunks = (g.tv + kChunkRows - 1) / kChunkRows;
+    dim3 grid(g.M * chunks, heads, njobs);
+    tile_amax_chunk_kernel<T, D><<<grid, kChunkThreads, 0, st>>>(g, a, chunks);
+    encode_chunk_kernel<T, D, FMT><<<grid, kChunkThreads, 0, st>>>(g, a, chunks);
+    const int64_t n = (int64_t)heads * g.M;
+    for (int z = 0; z < njobs; ++z)
+      if (!a.job[z].channel)
+        scales_from_amax_kernel<FMT><<<(int)std::min<int64_t>((n + 255) / 256, 1024), 256, 0, st>>>(a.job[z].scales,
+                                                                                                  n, a.err);
+  }
+};
+template <typename T, int D, int FMT>
 struct RunJobs {
   static void run(const Geometry& g, int32_t heads, const QuantArgs& a, int njobs, cudaStream_t st) {
     launch_jobs<T, D, FMT>(g, heads, a, njobs, st);
@@ -1021,7 +1148,16 @@ int quantize_qkv(const void* q, const void* k, const void* v, int dtype, int64_t
   a.job[2] = QuantJob{v, token_stride, head_stride, v_codes, v_scales, 1};
   a.amax = vmax;
   a.err = err_flag;
-  dispatch<RunJobs>(dtype, d, fmt, g, heads, a, 3, st);
+  static const bool per_tile_cta = getenv("FPSA_QUANT_TILE_CTA") != nullptr;  // measurement switch
+  if (per_tile_cta) {
+    dispatch<RunJobs>(dtype, d, fmt, g, heads, a, 3, st);
+    return cuda_status(name);
+  }
+  // chunked passes: the q / k scale arrays hold the tile maxima until the last pass
+  if (cudaMemsetAsync(q_scales, 0, (size_t)heads * g.M * 8, st) != cudaSuccess ||
+      cudaMemsetAsync(k_scales, 0, (size_t)heads * g.M * 8, st) != cudaSuccess)
+    return cuda_status(name);
+  dispatch<RunChunked>(dtype, d, fmt, g, heads, a, 3, st);
   return cuda_status(name);
 }
 }  // namespace
