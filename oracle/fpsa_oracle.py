@@ -24,7 +24,7 @@ __all__ = [
     "axis_interval", "window_lists", "density_of", "flops_sparse_of",
     "regime_of", "schedule_valid",
     "fp8_sparse_forward", "sparse_forward_f32", "onepass_forward", "bf16_round", "passthrough_emulation",
-    "normalized_rows", "p_flip_budget", "packed_keys",
+    "normalized_rows", "fp8_sparse_rows", "p_flip_budget", "packed_keys",
     "cosine", "max_abs", "gen_inputs",
 ]
 
@@ -347,6 +347,15 @@ def normalized_rows(q, k, v, tv, offs, ids, rows, fmt: Fmt = E4M3, softmax_scale
         s /= s.sum(axis=1, dtype=np.float64, keepdims=True).astype(np.float32)
         s *= np.float32(448.0)
         yield int(r), s[0], vv[kr], v_fac
+
+
+def fp8_sparse_rows(q, k, v, tv, offs, ids, rows, fmt: Fmt = E4M3, softmax_scale=None) -> np.ndarray:
+    """fp8_sparse_forward's output for selected query rows only ([len(rows), d] f32): the same arithmetic
+    (attention.py:133-149) one row at a time, for tiles too large for the full-matrix pass (24576 tokens)."""
+    out = np.empty((len(rows), np.asarray(q).shape[1]), dtype=np.float32)
+    for i, (_, x, vrows, v_fac) in enumerate(normalized_rows(q, k, v, tv, offs, ids, rows, fmt, softmax_scale)):
+        out[i] = (grid_round(x, E4M3)[None, :] @ vrows)[0] * v_fac
+    return out
 
 
 def p_flip_budget(q, k, v, tv, offs, ids, rows, fmt: Fmt = E4M3, softmax_scale=None, rel: float = 2.0 ** -19):

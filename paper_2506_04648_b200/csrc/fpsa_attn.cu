@@ -75,6 +75,9 @@
 #ifndef FPSA_EARLY_QK
 #define FPSA_EARLY_QK 0  // P~ in its own TMEM columns, QK(j+2) issued once S(j) is in registers (D = 128)
 #endif
+#ifndef FPSA_PREADY_SPIN
+#define FPSA_PREADY_SPIN 0  // P~(j) hand-off to the MMA warp through a shared-memory counter instead of an mbarrier
+#endif
 #ifndef FPSA_PACK_FASTPATH
 #define FPSA_PACK_FASTPATH 1  // packed blocks inside one key tile take the per-tile softmax code
 #endif
@@ -304,6 +307,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __shared__ uint64_t bar_s_full[2], bar_p_ready[2];  // by S buffer / step parity
   __shared__ uint64_t bar_s_free[2], bar_p_free[2];   // early QK: S(j) loaded by its owners / PV(j) done
   __shared__ uint32_t s_tmem;
+  __shared__ uint32_t s_pcnt[2];  // FPSA_PREADY_SPIN: P~-ready arrivals by step parity
   __shared__ float s_xchg[kParts][kBlk];  // [part][row] exchange between the warps of a row
   // per-item metadata, prefetched by the helper warp one item ahead (slot = item parity)
   __shared__ float s_fac[2][kFacCap];  // key-tile factors c(kt) = (sq * sk) * scale log2 e
@@ -335,6 +339,26 @@ __global__ void __launch_bounds__(kThreads, 1)
     return h >= 0;
   };
 
+  // P~(gg) ready (or S(gg) consumed): one arrival per owning warp; the MMA warp waits for all of them
+  [[maybe_unused]] constexpr uint32_t kPArrivals = kPingPong ? kSoftmaxWarps / 2 : kSoftmaxWarps;
+  auto p_arrive = [&](uint32_t gg) {  // lane 0 of an owning warp, after its tcgen05 fence
+    if constexpr (FPSA_PREADY_SPIN)
+      asm volatile("red.release.cta.shared::cta.add.u32 [%0], 1;" ::"r"(smem_u32(&s_pcnt[gg & 1])) : "memory");
+    else
+      mbar_arrive(&bar_p_ready[gg & 1]);
+  };
+  auto p_wait = [&](uint32_t gg) {
+    if constexpr (FPSA_PREADY_SPIN) {
+      const uint32_t want = kPArrivals * ((gg >> 1) + 1u), addr = smem_u32(&s_pcnt[gg & 1]);
+      uint32_t v;
+      do {
+        asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+      } while ((int32_t)(v - want) < 0);
+    } else {
+      attn_wait(&bar_p_ready[gg & 1], (gg >> 1) & 1);
+    }
+  };
+
   if (threadIdx.x == 0) {
     for (int i = 0; i < kItemRing; ++i) {
       mbar_init(&bar_item_full[i], 1);
@@ -359,6 +383,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&bar_kv_empty[i], 1);
     }
     s_ovf[0] = s_ovf[1] = 0;
+    s_pcnt[0] = s_pcnt[1] = 0;
     fence_barrier_init();
   }
   if (warp == kTmaWarp) {
@@ -530,7 +555,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint64_t dv = (!PACKED && bp == p.nb - 1 ? dvt0 : dv0) + pv_st * kVStageStep;
             if (s == pv0 && iter > 0) attn_wait(&bar_ofree, (iter - 1) & 1);  // the previous item's epilogue read O
             FPSA_TL(9, 0, gs);
-            attn_wait(&bar_p_ready[gs & 1], (gs >> 1) & 1);
+            p_wait(gs);
             FPSA_TL(9, 1, gs);
             tc_fence_after();
             const uint32_t tp = tm_p(gs);
@@ -570,7 +595,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           if (s == pv0 && iter > 0) attn_wait(&bar_ofree, (iter - 1) & 1);  // the previous item's epilogue read O
           FPSA_TL(9, 0, gs);
-          attn_wait(&bar_p_ready[gs & 1], (gs >> 1) & 1);
+          p_wait(gs);
           FPSA_TL(9, 1, gs);
           tc_fence_after();
 #if FPSA_MMA_ONE_ELECT
@@ -614,7 +639,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const long long tp0 = clock64();
   #endif
           FPSA_TL(9, 0, gs);
-          attn_wait(&bar_p_ready[gs & 1], (gs >> 1) & 1);
+          p_wait(gs);
           FPSA_TL(9, 1, gs);
   #ifdef FPSA_TRACE
           if (lane == 0) atomicAdd(&g_trace[3], (unsigned long long)(clock64() - tp0));
@@ -772,7 +797,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             __syncwarp();
             if (lane == 0) {
               if (kEarly) mbar_arrive(&bar_s_free[gj & 1]);
-              mbar_arrive(&bar_p_ready[gj & 1]);  // S consumed
+              p_arrive(gj);  // S consumed
             }
           }
           g += n_kv;
@@ -799,7 +824,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               __syncwarp();
               if (lane == 0) {
                 if (kEarly) mbar_arrive(&bar_s_free[gj & 1]);
-                mbar_arrive(&bar_p_ready[gj & 1]);  // S consumed
+                p_arrive(gj);  // S consumed
               }
             }
             g += n_kv;
@@ -889,7 +914,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             tmem_wait_st();
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&bar_p_ready[g_own & 1]);
+            if (lane == 0) p_arrive(g_own);
             FPSA_TL(warp, 3, g_own);
           }
         }
@@ -909,7 +934,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           m_acc = fmaxf(m_acc, block_max<kPartCols>(tm_s(g) + lane_off + part * kPartCols, ncol_h, false) * c);
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(&bar_p_ready[g & 1]);  // S consumed
+          if (lane == 0) p_arrive(g);  // S consumed
           if (tail) {
             b = 0;
             ++kt;
@@ -974,7 +999,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           tmem_wait_st();
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(&bar_p_ready[g & 1]);
+          if (lane == 0) p_arrive(g);
           FPSA_TL(warp, 3, g);
           if (more) tmem_wait_ld();
         }

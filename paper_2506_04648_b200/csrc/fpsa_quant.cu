@@ -660,6 +660,25 @@ struct TmaQuantArgs {
   int32_t* err;
 };
 
+#ifndef FPSA_QUANT_ORDER
+#define FPSA_QUANT_ORDER 0  // 0: (tensor, head, tile) with tiles fastest; 1: (tensor, tile, head), heads fastest
+#endif
+#ifndef FPSA_QUANT_LOADONLY
+#define FPSA_QUANT_LOADONLY 0
+#endif
+__device__ __forceinline__ void item_of(int32_t it, int32_t per_job, int32_t heads, int32_t M, int32_t& z,
+                                        int32_t& h, int32_t& u) {
+  z = it / per_job;
+  const int32_t rem = it - z * per_job;
+  if (FPSA_QUANT_ORDER) {
+    u = rem / heads;
+    h = rem - u * heads;
+  } else {
+    h = rem / M;
+    u = rem - h * M;
+  }
+}
+
 template <int FMT>
 __global__ void __launch_bounds__(kTmaThreads, 1)
     quant_tma_kernel(const __grid_constant__ CUtensorMap tm0, const __grid_constant__ CUtensorMap tm1,
@@ -694,7 +713,8 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
       for (int32_t it = blockIdx.x; it < n_items; it += gridDim.x, ++k) {
         const int st = k % kTmaStages;
         if (k >= kTmaStages) mbar_wait(&empty[st], ((k / kTmaStages) - 1) & 1);
-        const int32_t z = it / per_job, rem = it - z * per_job, h = rem / g.M, u = rem - h * g.M;
+        int32_t z, h, u;
+        item_of(it, per_job, a.heads, g.M, z, h, u);
         const void* tm = z == 0 ? (const void*)&tm0 : (z == 1 ? (const void*)&tm1 : (const void*)&tm2);
         uint8_t* dst = smem + st * kTmaStageBytes;
         mbar_arrive_expect_tx(&full[st], (uint32_t)g.tv * kTmaD * 2);
@@ -732,7 +752,14 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
   int k = 0;
   for (int32_t it = blockIdx.x; it < n_items; it += gridDim.x, ++k) {
     const int st = k % kTmaStages;
-    const int32_t z = it / per_job, rem = it - z * per_job, h = rem / g.M, u = rem - h * g.M;
+    int32_t z, h, u;
+    item_of(it, per_job, a.heads, g.M, z, h, u);
+#if FPSA_QUANT_LOADONLY
+    mbar_wait(&full[st], (k / kTmaStages) & 1);  // measurement build: the loads alone (codes not written)
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[st]);
+    continue;
+#endif
     // select, do not index: a dynamically indexed parameter array is copied to local memory
     const bool channel = (z == 0 ? a.channel[0] : z == 1 ? a.channel[1] : a.channel[2]) != 0;
     uint8_t* const codes = z == 0 ? a.codes[0] : z == 1 ? a.codes[1] : a.codes[2];

@@ -137,11 +137,11 @@ def test_natural_order_large_tiles(fpsa):
         assert np.array_equal(plan.q_scales.cpu().numpy(), s)
         assert np.array_equal(plan.q_codes.view(M, plan.pitch, d)[:, :tv].reshape(L, d).cpu().numpy(), c)
         offs, ids = O.window_lists(O.tile_grid_dims(grid, tile), win)
-        ref, _ = O.fp8_sparse_forward(q, k, v, tv, offs, ids)
         got = out[:, 0].cpu().numpy()[perm]
         rows = np.unique(np.linspace(0, L - 1, 256).astype(np.int64))
+        ref = O.fp8_sparse_rows(q, k, v, tv, offs, ids, rows).astype(np.float64)  # the oracle on the sampled rows
         budget, n_amb = O.p_flip_budget(q, k, v, tv, offs, ids, rows)
-        err = np.abs(got[rows].astype(np.float64) - ref[rows])
+        err = np.abs(got[rows].astype(np.float64) - ref)
         peak = float(np.abs(ref).max())
         print(f"tile {tile}: max rel err {err.max() / peak:.3e}, ambiguous {n_amb}")
         assert (err <= 1e-5 * peak + budget).all()

@@ -242,3 +242,20 @@ def test_onepass_emulation_close_to_reference(attn_golden):
     emu = O.onepass_forward(codes, tv, offs, ids, tau=8.0, poly=True)
     assert O.cosine(emu, ref) >= 0.999
     assert O.max_abs(emu, ref) <= 0.1 * float(np.abs(ref).max())
+
+
+
+@pytest.mark.parametrize("name", CASE_NAMES)
+def test_sampled_rows_vs_reference(attn_golden, name):
+    """oracle.fp8_sparse_rows (the large-tile parity checker: one query row at a time) against the
+    reference's own outputs on the golden rows (attention.py:179-208)."""
+    c = golden_cases(attn_golden)[name]
+    L = c["grid"][0] * c["grid"][1] * c["grid"][2]
+    tv = c["tile"][0] * c["tile"][1] * c["tile"][2]
+    q, k, v = O.gen_inputs(c["seed"], 1, 0, L, c["d"], c["dist"])
+    offs, ids = O.window_lists(O.tile_grid_dims(c["grid"], c["tile"]), c["window"])
+    rows = attn_golden[name + "__rows"]
+    ref = attn_golden[name + "__out"]
+    got = O.fp8_sparse_rows(q, k, v, tv, offs, ids, rows, O.FORMATS[c["fmt"]])
+    budget, _ = O.p_flip_budget(q, k, v, tv, offs, ids, rows, O.FORMATS[c["fmt"]])
+    assert (np.abs(got.astype(np.float64) - ref) <= 1e-5 * float(np.abs(ref).max()) + budget).all()
