@@ -73,8 +73,8 @@
 #define FPSA_MMA_ONE_ELECT 1
 #endif
 #ifndef FPSA_EARLY_QK
-#define FPSA_EARLY_QK 0  // P~ in its own TMEM columns, QK(j+2) issued once S(j) is in registers (D = 128)
-#endif
+#define FPSA_EARLY_QK 2  // P~ in its own TMEM columns, QK(j+2) issued once S(j) is in registers (D = 128);
+#endif                    // 2: QK and PV issued by two different warps (warp 9 / warp 11)
 #ifndef FPSA_PREADY_SPIN
 #define FPSA_PREADY_SPIN 0  // P~(j) hand-off to the MMA warp through a shared-memory counter instead of an mbarrier
 #endif
@@ -96,7 +96,11 @@ __device__ __forceinline__ void attn_wait(uint64_t* bar, uint32_t parity) {
   mbar_wait<FPSA_MBAR_SUSPEND_NS>(bar, parity);
 }
 
-constexpr int kParts = 2;                       // softmax warps sharing one TMEM lane quarter (row)
+#ifndef FPSA_PARTS
+#define FPSA_PARTS 2  // softmax warps per SMSP (per TMEM lane quarter); 3 needs the split-issue ping-pong path
+#endif
+constexpr int kParts = FPSA_PARTS;              // softmax warps sharing one TMEM lane quarter (row)
+constexpr int kEpiParts = 2;                    // parts that read O in the epilogue (D / 2 channels each)
 [[maybe_unused]] constexpr int kPartCols = 128 / kParts;  // S columns per softmax thread in the FPSA_PINGPONG=0 variant
 constexpr int kSoftmaxWarps = 4 * kParts;
 constexpr int kTmaWarp = kSoftmaxWarps;
@@ -104,7 +108,7 @@ constexpr int kMmaWarp = kSoftmaxWarps + 1;
 constexpr int kThreads = (kSoftmaxWarps + 4) * 32;  // softmax warpgroups + 1 producer (TMA, MMA, helper, idle)
 // setmaxnreg split of the 64K-register file: per SMSP one warp of each warpgroup
 // (4 warps per quarter at 104 registers was measured slower: 13.4 vs 12.8 ms at C2; 112/64 deadlocks)
-constexpr uint32_t kRegsSoftmax = 216, kRegsProducer = 64;
+constexpr uint32_t kRegsSoftmax = kParts == 2 ? 216 : 144, kRegsProducer = 64;
 
 constexpr int kStages = 4;     // K/V ring depth (128-key blocks)
 constexpr int kBlk = 128;      // rows per query block = keys per key block
@@ -121,7 +125,7 @@ constexpr int kItemReaders = 2 + kSoftmaxWarps;  // TMA warp, MMA warp, softmax 
 #define FPSA_PINGPONG 1
 #endif
 constexpr bool kPingPong = FPSA_PINGPONG != 0;
-static_assert(!kPingPong || kParts == 2, "ping-pong pairs the two warps of a TMEM lane quarter");
+static_assert(kParts == 2 || (kParts == 3 && kPingPong), "three parts take the key blocks round-robin (ping-pong)");
 
 struct AttnParams {
   const double* q_scales;
@@ -216,6 +220,17 @@ __device__ __forceinline__ int32_t blocks_per_pass(const AttnParams& p, int32_t 
   return PACKED ? (n_kt * p.tv + kBlk - 1) / kBlk : n_kt * p.nb;
 }
 
+// S = Q K^T: K = D in K32 steps (one elect for the four MMAs of D = 128)
+template <int D>
+__device__ __forceinline__ void qk_mma(uint32_t ts, uint64_t dq, uint64_t dk, uint32_t idesc) {
+  if constexpr (D == 128) {
+    mma_f8_ss_x4_w(ts, dq, dq + 2, dq + 4, dq + 6, dk, dk + 2, dk + 4, dk + 6, idesc, 0u);
+  } else {
+#pragma unroll
+    for (int k = 0; k < D / 32; ++k) mma_f8_ss_w(ts, dq + 2 * k, dk + 2 * k, idesc, k > 0 ? 1u : 0u);
+  }
+}
+
 template <int D>
 struct Smem {
   static constexpr int kTile = kBlk * D;  // bytes of one 128-row fp8 tile
@@ -304,10 +319,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   __shared__ uint64_t bar_q[2], bar_qfree[2];  // query-block buffer (item parity): loaded / no longer read
   __shared__ uint64_t bar_o, bar_ofree;        // O complete for the item / epilogue has read O
   __shared__ uint64_t bar_kv_full[kStages], bar_kv_empty[kStages];
-  __shared__ uint64_t bar_s_full[2], bar_p_ready[2];  // by S buffer / step parity
-  __shared__ uint64_t bar_s_free[2], bar_p_free[2];   // early QK: S(j) loaded by its owners / PV(j) done
+  // S(j) full: by j mod kSF (a waiter is never two phases ahead); P~(j) ready / its buffer free: by j mod
+  // kParts (the owning part); S buffer j mod 2 loaded by its owners (early QK)
+  constexpr int kSF = kParts == 2 ? 2 : 6;
+  __shared__ uint64_t bar_s_full[kSF], bar_p_ready[kParts];
+  __shared__ uint64_t bar_s_free[2], bar_p_free[kParts];
   __shared__ uint32_t s_tmem;
-  __shared__ uint32_t s_pcnt[2];  // FPSA_PREADY_SPIN: P~-ready arrivals by step parity
+  __shared__ uint32_t s_pcnt[kParts];  // FPSA_PREADY_SPIN: P~-ready arrivals by owning part
   __shared__ float s_xchg[kParts][kBlk];  // [part][row] exchange between the warps of a row
   // per-item metadata, prefetched by the helper warp one item ahead (slot = item parity)
   __shared__ float s_fac[2][kFacCap];  // key-tile factors c(kt) = (sq * sk) * scale log2 e
@@ -340,36 +358,49 @@ __global__ void __launch_bounds__(kThreads, 1)
   };
 
   // P~(gg) ready (or S(gg) consumed): one arrival per owning warp; the MMA warp waits for all of them
-  [[maybe_unused]] constexpr uint32_t kPArrivals = kPingPong ? kSoftmaxWarps / 2 : kSoftmaxWarps;
+  [[maybe_unused]] constexpr uint32_t kPArrivals = kPingPong ? kSoftmaxWarps / kParts : kSoftmaxWarps;
+  // barrier slot and phase of step gg: S full (kSF slots), P~ ready / P~ buffer free (kParts slots)
+  auto sf_wait = [&](uint32_t gg) { attn_wait(&bar_s_full[gg % kSF], (gg / kSF) & 1); };
+  // Split issue: before P~(gg) ready (or S(gg) consumed) is signalled, PV(gg - kParts) must have been
+  // handled, so that p_ready[gg % kParts] never runs two phases ahead of the PV warp.  The main pass gets this
+  // from waiting for its P~ buffer; the max / sum passes of the exact and normalised modes, which store no
+  // P~, wait here (without it the softmax could signal two phases of one barrier before the PV warp
+  // observed the first, and the PV warp would then wait for a phase that needs its own K/V release).
+  auto p_free_wait = [&](uint32_t gg) {
+    if constexpr (FPSA_EARLY_QK == 2 && kPingPong)
+      if (gg >= (uint32_t)kParts) attn_wait(&bar_p_free[gg % kParts], ((gg / kParts) - 1) & 1);
+  };
   auto p_arrive = [&](uint32_t gg) {  // lane 0 of an owning warp, after its tcgen05 fence
     if constexpr (FPSA_PREADY_SPIN)
-      asm volatile("red.release.cta.shared::cta.add.u32 [%0], 1;" ::"r"(smem_u32(&s_pcnt[gg & 1])) : "memory");
+      asm volatile("red.release.cta.shared::cta.add.u32 [%0], 1;" ::"r"(smem_u32(&s_pcnt[gg % kParts])) : "memory");
     else
-      mbar_arrive(&bar_p_ready[gg & 1]);
+      mbar_arrive(&bar_p_ready[gg % kParts]);
   };
   auto p_wait = [&](uint32_t gg) {
     if constexpr (FPSA_PREADY_SPIN) {
-      const uint32_t want = kPArrivals * ((gg >> 1) + 1u), addr = smem_u32(&s_pcnt[gg & 1]);
+      const uint32_t want = kPArrivals * ((gg / kParts) + 1u), addr = smem_u32(&s_pcnt[gg % kParts]);
       uint32_t v;
       do {
         asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
       } while ((int32_t)(v - want) < 0);
     } else {
-      attn_wait(&bar_p_ready[gg & 1], (gg >> 1) & 1);
+      attn_wait(&bar_p_ready[gg % kParts], (gg / kParts) & 1);
     }
   };
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < kItemRing; ++i) {
       mbar_init(&bar_item_full[i], 1);
-      mbar_init(&bar_item_empty[i], kItemReaders);
+      mbar_init(&bar_item_empty[i], kItemReaders + (FPSA_EARLY_QK == 2 && kPingPong ? 1 : 0));
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&bar_q[i], 1);
       mbar_init(&bar_qfree[i], 1);
-      mbar_init(&bar_s_full[i], 1);
-      mbar_init(&bar_p_ready[i], kPingPong ? kSoftmaxWarps / 2 : kSoftmaxWarps);  // one arrival per writing warp
-      mbar_init(&bar_s_free[i], kSoftmaxWarps / 2);
+      mbar_init(&bar_s_free[i], kSoftmaxWarps / kParts);
+    }
+    for (int i = 0; i < kSF; ++i) mbar_init(&bar_s_full[i], 1);
+    for (int i = 0; i < kParts; ++i) {
+      mbar_init(&bar_p_ready[i], kPArrivals);  // one arrival per writing warp
       mbar_init(&bar_p_free[i], 1);
     }
     mbar_init(&bar_o, 1);
@@ -383,7 +414,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&bar_kv_empty[i], 1);
     }
     s_ovf[0] = s_ovf[1] = 0;
-    s_pcnt[0] = s_pcnt[1] = 0;
+    for (int i = 0; i < kParts; ++i) s_pcnt[i] = 0;
     fence_barrier_init();
   }
   if (warp == kTmaWarp) {
@@ -410,8 +441,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   // S buffers at columns 256 and 384 (computed, not indexed: a local array would live in memory)
   auto tm_s = [tmem](uint32_t g) { return tmem + 256u + 128u * (g & 1u); };
   // early-QK mode: P~(j) in its own 32 columns (160 / 192), so S(j)'s buffer is free once loaded
-  constexpr bool kEarly = FPSA_EARLY_QK && kPingPong && D == 128;
-  auto tm_p = [tmem](uint32_t g) { return tmem + 160u + 32u * (g & 1u); };
+  constexpr bool kEarly = FPSA_EARLY_QK && kPingPong;
+  static_assert(kParts == 2 || (kEarly && FPSA_EARLY_QK == 2), "three parts need the split QK / PV issue");
+  // split issue: warp 9 issues the QKs (on S(j) loaded), warp 11 the PVs (on P~(j) stored); QK and PV touch
+  // disjoint TMEM (S buffers / P~ buffers and O), and every PV comes from the one PV warp, in order
+  constexpr bool kSplit = kEarly && FPSA_EARLY_QK == 2;
+  constexpr int kPvWarp = kSoftmaxWarps + 3;
+  auto tm_p = [tmem](uint32_t g) { return tmem + 160u + 32u * (g % (uint32_t)kParts); };
+  static_assert(D + 16 <= 160 && 160 + 32 * kParts <= 256, "TMEM: O | P~ buffers | S buffers at 256 and 384");
   const float tau = p.exact ? 0.0f : p.tau;
 
   if (warp >= kSoftmaxWarps) regs_dec<kRegsProducer>();  // producer warpgroup: TMA, MMA, 2 idle warps
@@ -517,7 +554,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int k = 0; k < D / 32; ++k) mma_f8_ss_w(ts, dq + 2 * k, dk + 2 * k, idq, k > 0 ? 1u : 0u);
         }
 #endif
-        mma_commit_w(&bar_s_full[gg & 1]);
+        mma_commit_w(&bar_s_full[gg % kSF]);
         if (++b2 == p.nb) b2 = 0;
         if (++qk_st == kStages) {
           qk_st = 0;
@@ -527,7 +564,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int32_t s = 0; s < min(steps, 2); ++s) issue_qk(g + s);
       if (steps <= 2) mma_commit_w(&bar_qfree[qbuf]);
 #if FPSA_MMA_HOIST
-      if constexpr (kPingPong && D == 128) {
+      if constexpr (kPingPong && (kEarly || D == 128)) {
         // Everything that does not depend on P~(j) is done before waiting for it: the K/V-full wait and
         // descriptors of QK(j+2), the V descriptor of PV(j), the O-free wait. After p_ready(j) the warp
         // only issues PV(j), QK(j+2) and the commits (the issue path is the step's critical path).
@@ -542,15 +579,16 @@ __global__ void __launch_bounds__(kThreads, 1)
               attn_wait(&bar_s_free[gs & 1], (gs >> 1) & 1);
               tc_fence_after();
 #ifndef FPSA_NO_MMA
-              mma_f8_ss_x4_w(tm_s(gs), dq, dq + 2, dq + 4, dq + 6, dk, dk + 2, dk + 4, dk + 6, idesc_qk, 0u);
+              qk_mma<D>(tm_s(gs), dq, dk, idesc_qk);
 #endif
-              mma_commit_w(&bar_s_full[gs & 1]);
+              mma_commit_w(&bar_s_full[gs % kSF]);
               if (++qk_st == kStages) {
                 qk_st = 0;
                 qk_ph ^= 1;
               }
               if (s + 3 == steps) mma_commit_w(&bar_qfree[qbuf]);
             }
+            if constexpr (kSplit) continue;  // the PV warp issues PV(j)
             constexpr uint64_t kVk = 32 * D / 16;
             const uint64_t dv = (!PACKED && bp == p.nb - 1 ? dvt0 : dv0) + pv_st * kVStageStep;
             if (s == pv0 && iter > 0) attn_wait(&bar_ofree, (iter - 1) & 1);  // the previous item's epilogue read O
@@ -566,12 +604,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 #endif
             FPSA_TL(9, 2, gs);
             mma_commit_w(&bar_kv_empty[pv_st]);
-            mma_commit_w(&bar_p_free[gs & 1]);  // every step, so its phases count steps
+            mma_commit_w(&bar_p_free[gs % kParts]);  // every step, so its phases count steps
             FPSA_TL(9, 3, gs);
             if (++pv_st == kStages) pv_st = 0;
             if (++bp == p.nb) bp = 0;
           }
-        } else
+        } else {
         for (int32_t s = 0; s < steps; ++s) {
           const uint32_t gs = g + s;
           const bool do_qk = s + 2 < steps;
@@ -630,6 +668,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (++pv_st == kStages) pv_st = 0;
           if (++bp == p.nb) bp = 0;
         }
+        }
       } else
 #endif
       {
@@ -678,6 +717,46 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (s + 3 == steps) mma_commit_w(&bar_qfree[qbuf]);
           }
         }
+      }
+      if constexpr (!kSplit) mma_commit_w(&bar_o);
+      g += steps;
+    }
+  } else if (kSplit && warp == kPvWarp) {
+    // ------------------------------------------------------------ PV issuer (split issue)
+    constexpr uint32_t idesc_pv = idesc_f8(128, D + 16, FPSA_E4M3, FMT, 1);
+    constexpr uint64_t kTileU = S::kTile >> 4;
+    constexpr uint64_t kVStageStep = kTileU - (kTileU << 16);
+    constexpr uint64_t kVk = 32 * D / 16;
+    const uint32_t sv0 = smem_u32(smem + S::kV);
+    const uint64_t dv0 = desc_mnmajor_ones<D>(sv0, smem_u32(smem + S::kOnes) - sv0);
+    const uint64_t dvt0 = desc_mnmajor_ones<D>(sv0, smem_u32(smem + S::kOnesTail) - sv0);
+    uint32_t g = 0, pv_st = 0;
+    int32_t h, u, qb;
+    for (int32_t iter = 0; next_item(iter, h, u, qb); ++iter) {
+      const int32_t n_kt = __ldg(p.offs + u + 1) - __ldg(p.offs + u);
+      const int32_t n_kv = blocks_per_pass<PACKED>(p, n_kt), steps = passes * n_kv;
+      const int32_t pv0 = (passes - 1) * n_kv;
+      int32_t bp = 0;
+      for (int32_t s = 0; s < steps; ++s) {
+        const uint32_t gs = g + s;
+        const uint64_t dv = (!PACKED && bp == p.nb - 1 ? dvt0 : dv0) + pv_st * kVStageStep;
+        if (s == pv0 && iter > 0) attn_wait(&bar_ofree, (iter - 1) & 1);  // the previous item's epilogue read O
+        FPSA_TL(9, 0, gs);
+        p_wait(gs);
+        FPSA_TL(9, 1, gs);
+        tc_fence_after();
+        const uint32_t tp = tm_p(gs);
+#ifndef FPSA_NO_MMA
+        if (s >= pv0)
+          mma_f8_ts_x4_w(tm_o, tp, tp + 8, tp + 16, tp + 24, dv, dv + kVk, dv + 2 * kVk, dv + 3 * kVk, idesc_pv,
+                         s > pv0 ? 1u : 0u);
+#endif
+        FPSA_TL(9, 2, gs);
+        mma_commit_w(&bar_kv_empty[pv_st]);  // K(j) was read by QK(j), complete before S(j) was seen full
+        mma_commit_w(&bar_p_free[gs % kParts]);
+        FPSA_TL(9, 3, gs);
+        if (++pv_st == kStages) pv_st = 0;
+        if (++bp == p.nb) bp = 0;
       }
       mma_commit_w(&bar_o);
       g += steps;
@@ -732,7 +811,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int part = warp >> 2;              // S columns [kPartCols part, kPartCols (part + 1))
     const int row = quarter * 32 + lane;     // TMEM lane = row of the query block
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
-    const uint32_t o_addr = tm_o + lane_off + part * (D / kParts);
+    const uint32_t o_addr = tm_o + lane_off + part * (D / kEpiParts);
     const float sl = p.softmax_log2;
     auto row_sync = [&]() { named_bar_sync(1 + quarter, 32 * kParts); };
     auto row_max = [&](float m) {  // max over all parts of the row
@@ -772,9 +851,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         // g % 2 == part (S buffer g % 2 == part), the other warp of the SMSP the other steps, so one
         // warp's TMEM load / store and hand-off latency overlaps the other's exp work
         const uint32_t s_row = tm_s((uint32_t)part) + lane_off;
-        auto owned = [&](uint32_t gg) { return (int)(gg & 1u) == part; };
+        auto owned = [&](uint32_t gg) { return (int)(gg % (uint32_t)kParts) == part; };
         // first block of a pass starting at step counter gg that this warp owns (then every second one)
-        auto first_owned = [&](uint32_t gg) { return (int32_t)(((uint32_t)part - gg) & 1u); };
+        auto first_owned = [&](uint32_t gg) {
+          return (int32_t)(((uint32_t)part + (uint32_t)kParts - gg % (uint32_t)kParts) % (uint32_t)kParts);
+        };
         // factors of a block's two key tiles: keys < split from tile kt_a, the rest from kt_a + 1
         auto factors = [&](int32_t kt_a, int32_t split, int32_t nvalid, float& ca, float& cb) {
           ca = factor_at(kt_a);
@@ -784,19 +865,20 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (NORM || p.exact) {
           // pass 0 (exact and normalised modes): running max over this warp's key blocks, then over the pair
           float m_acc = -INFINITY;
-          for (int32_t j = first_owned(g); j < n_kv; j += 2) {
+          for (int32_t j = first_owned(g); j < n_kv; j += kParts) {
             const uint32_t gj = g + j;
             int32_t kt_a, split, nvalid;
             block_at<PACKED>(p, n_kt, j, kt_a, split, nvalid);
             float ca, cb;
             factors(kt_a, split, nvalid, ca, cb);
-            attn_wait(&bar_s_full[gj & 1], (gj >> 1) & 1);
+            sf_wait(gj);
             tc_fence_after();
             m_acc = fmaxf(m_acc, block_max_split(s_row, split, nvalid, ca, cb));
             tc_fence_before();
             __syncwarp();
             if (lane == 0) {
               if (kEarly) mbar_arrive(&bar_s_free[gj & 1]);
+              p_free_wait(gj);
               p_arrive(gj);  // S consumed
             }
           }
@@ -805,13 +887,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           if constexpr (NORM) {
             // pass 1: l = sum exp(s - m) in f64 over this warp's blocks, then over the pair
             double l_acc = 0.0;
-            for (int32_t j = first_owned(g); j < n_kv; j += 2) {
+            for (int32_t j = first_owned(g); j < n_kv; j += kParts) {
               const uint32_t gj = g + j;
               int32_t kt_a, split, nvalid;
               block_at<PACKED>(p, n_kt, j, kt_a, split, nvalid);
               float ca, cb;
               factors(kt_a, split, nvalid, ca, cb);
-              attn_wait(&bar_s_full[gj & 1], (gj >> 1) & 1);
+              sf_wait(gj);
               tc_fence_after();
 #pragma unroll
               for (int hb = 0; hb < 2; ++hb) {
@@ -824,6 +906,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               __syncwarp();
               if (lane == 0) {
                 if (kEarly) mbar_arrive(&bar_s_free[gj & 1]);
+                p_free_wait(gj);
                 p_arrive(gj);  // S consumed
               }
             }
@@ -844,13 +927,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             block_at<PACKED>(p, n_kt, 0, kt_a, split, nvalid);
             float ca, cb;
             factors(kt_a, split, nvalid, ca, cb);
-            attn_wait(&bar_s_full[g & 1], (g >> 1) & 1);
+            sf_wait(g);
             tc_fence_after();
             m0 = block_max_split(s_row, split, nvalid, ca, cb);
           }
           m_ref = row_max(m0);
         }
-        for (int32_t j = first_owned(g); j < n_kv; j += 2) {
+        for (int32_t j = first_owned(g); j < n_kv; j += kParts) {
           const uint32_t g_own = g + j;
           {
             int32_t kt_a, split, nvalid;
@@ -861,7 +944,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const long long ts0 = clock64();
 #endif
             FPSA_TL(warp, 0, g_own);
-            attn_wait(&bar_s_full[g_own & 1], (g_own >> 1) & 1);
+            sf_wait(g_own);
             FPSA_TL(warp, 1, g_own);
 #ifdef FPSA_TRACE
             w_s += clock64() - ts0;
@@ -905,7 +988,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             if constexpr (kEarly) {
               // P~(j) into its own columns once PV(j - 2) has read them
-              if (g_own >= 2) attn_wait(&bar_p_free[g_own & 1], ((g_own - 2) >> 1) & 1);
+              if (g_own >= (uint32_t)kParts) attn_wait(&bar_p_free[g_own % kParts], ((g_own / kParts) - 1) & 1);
               tc_fence_after();
               tmem_st32(tm_p(g_own) + lane_off, w);
             } else {
@@ -1009,6 +1092,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       t_loop += clock64() - tl0;
 #endif
       // ---------------------------------------------------------- epilogue
+      // parts 0 and 1 read O (D / 2 channels each); a third part has nothing to read
+      if (part < kEpiParts) {
       attn_wait(&bar_o, iter & 1);
       tc_fence_after();
       float inv_l = 1.0f;  // normalised-P mode: P~ is already normalised (out = O * v_fac)
@@ -1028,15 +1113,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         token = (int64_t)u * p.tv + r;
       }
       const float* vs = s_vsc[slot];
-      static_assert(D / kParts >= 16, "each softmax thread stores at least 16 output channels");
+      static_assert(D / kEpiParts >= 16, "each softmax thread stores at least 16 output channels");
 #pragma unroll
-      for (int cc = 0; cc < D / kParts; cc += 32) {
-        const int col = part * (D / kParts) + cc;
+      for (int cc = 0; cc < D / kEpiParts; cc += 32) {
+        const int col = part * (D / kEpiParts) + cc;
         uint32_t o[32];
-        if constexpr (D / kParts >= 32) tmem_ld32(o_addr + cc, o);
+        if constexpr (D / kEpiParts >= 32) tmem_ld32(o_addr + cc, o);
         else tmem_ld16(o_addr + cc, *reinterpret_cast<uint32_t(*)[16]>(o));
         tmem_wait_ld();
-        constexpr int kN = D / kParts >= 32 ? 32 : 16;
+        constexpr int kN = D / kEpiParts >= 32 ? 32 : 16;
         if (r < p.tv) {
           float f[32];
 #pragma unroll
@@ -1061,6 +1146,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
         }
+      }
       }
       tc_fence_before();
       __syncwarp();

@@ -209,12 +209,21 @@ __device__ __forceinline__ uint32_t encode_slow(const float (&v)[VEC], const flo
     return encode_slow4<FMT, 2>(v[0], v[1], 0.0f, 0.0f, peak[0], peak[1], 0.0f, 0.0f);
 }
 
+#ifndef FPSA_QUANT_STORE
+#define FPSA_QUANT_STORE 0  // measurement switch: 0 st.global, 1 st.global.cs (streaming), 2 no code stores
+#endif
 template <int VEC>
 __device__ __forceinline__ void store_codes(uint8_t* p, uint32_t c) {
-  if constexpr (VEC == 4)
-    *reinterpret_cast<uint32_t*>(p) = c;
-  else
+  if constexpr (VEC == 4) {
+    if constexpr (FPSA_QUANT_STORE == 1)
+      asm volatile("st.global.cs.b32 [%0], %1;" ::"l"(p), "r"(c) : "memory");
+    else if constexpr (FPSA_QUANT_STORE == 2)
+      asm volatile("" ::"l"(p), "r"(c));
+    else
+      *reinterpret_cast<uint32_t*>(p) = c;
+  } else {
     *reinterpret_cast<uint16_t*>(p) = (uint16_t)c;
+  }
 }
 
 // |x| max in the bit domain (exact for floats; NaN/inf bit patterns sort above
@@ -648,7 +657,6 @@ constexpr int kTmaStages = 3;
 constexpr int kTmaMaxRows = 256;
 constexpr int kTmaD = 128;
 constexpr int kTmaStageBytes = kTmaMaxRows * kTmaD * 2;
-constexpr uint32_t kTmaQueueCap = 2048;
 
 struct TmaQuantArgs {
   int32_t whole_tile;  // one TMA box per tile (5D natural-order view / tv-row box) instead of one per w-run
@@ -679,6 +687,20 @@ __device__ __forceinline__ void item_of(int32_t it, int32_t per_job, int32_t hea
   }
 }
 
+#ifdef FPSA_QTRACE
+// measurement builds only: per-tile timeline of CTA 0 (clock64): [0] load issued, [1] warp 0 saw it full,
+// [2] warp 0 past the tile-max barrier, [3] warp 0 released the stage, [4] warp 23 released the stage
+__device__ long long g_qtl[128][5];
+#define FPSA_QTL(k, ev)                                                            \
+  do {                                                                            \
+    if (blockIdx.x == 0 && (threadIdx.x & 31) == 0 && (k) < 128) g_qtl[(k)][(ev)] = clock64(); \
+  } while (0)
+#else
+#define FPSA_QTL(k, ev) \
+  do {                  \
+  } while (0)
+#endif
+
 template <int FMT>
 __global__ void __launch_bounds__(kTmaThreads, 1)
     quant_tma_kernel(const __grid_constant__ CUtensorMap tm0, const __grid_constant__ CUtensorMap tm1,
@@ -689,7 +711,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
   using V = Vec<__nv_bfloat16, VEC>;
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ uint64_t full[kTmaStages], empty[kTmaStages];
-  __shared__ uint32_t s_peak[2];  // tile |x| max bits by tile parity (shared-memory atomicMax of the warps)
+  __shared__ uint32_t s_peak[3];  // tile |x| max bits by tile index mod 3 (shared-memory atomicMax of the warps)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int32_t per_job = a.heads * g.M;
   const int32_t n_items = a.njobs * per_job;
@@ -717,6 +739,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
         item_of(it, per_job, a.heads, g.M, z, h, u);
         const void* tm = z == 0 ? (const void*)&tm0 : (z == 1 ? (const void*)&tm1 : (const void*)&tm2);
         uint8_t* dst = smem + st * kTmaStageBytes;
+        FPSA_QTL(k, 0);
         mbar_arrive_expect_tx(&full[st], (uint32_t)g.tv * kTmaD * 2);
         if (a.whole_tile) {
           // one box per tile: natural order through the 5D view (c, head, w, h, t) with box
@@ -742,12 +765,14 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
     return;
   }
   // -------------------------------------------------------------- consumers
-  // Ambiguous elements (the bracket straddles a rounding boundary: mostly
-  // exact ties of bf16 data, ~0.4% of elements) are queued in shared memory
-  // and re-encoded exactly by all consumer threads after the tile.
-  __shared__ uint16_t s_queue[2][kTmaQueueCap];
-  __shared__ uint32_t s_count[2];
-  if (threadIdx.x == 0) s_count[0] = s_peak[0] = 0;
+  // One CTA-wide barrier per tile (the tile max); each warp then encodes its rows and releases the stage
+  // itself.  Ambiguous elements (the bracket straddles a rounding boundary: exact ties of bf16 data, ~0.4%
+  // of elements) are flagged per row in a register mask and re-encoded exactly by their own lane after
+  // the row loop, while the tile is still in shared memory (no queue, no atomics).  Holding the stage
+  // until then is deliberate: copying the rows to registers and releasing the stage first keeps three
+  // loads in flight per SM and measured 1.78 ms against 1.16 (profiles/r02_quant_early_release_rejected.txt).
+  static_assert(kTmaMaxRows <= 32 * kTmaConsumerWarps, "row mask holds one bit per row of a warp");
+  if (threadIdx.x == 0) s_peak[0] = s_peak[1] = s_peak[2] = 0;
   named_bar_sync(1, kTmaConsumerWarps * 32);
   int k = 0;
   for (int32_t it = blockIdx.x; it < n_items; it += gridDim.x, ++k) {
@@ -764,25 +789,28 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
     const bool channel = (z == 0 ? a.channel[0] : z == 1 ? a.channel[1] : a.channel[2]) != 0;
     uint8_t* const codes = z == 0 ? a.codes[0] : z == 1 ? a.codes[1] : a.codes[2];
     double* const scales = z == 0 ? a.scales[0] : z == 1 ? a.scales[1] : a.scales[2];
-    uint8_t* out_tile = codes + ((int64_t)h * g.M + u) * g.pitch * kTmaD;
-    uint8_t* out = out_tile + lane * VEC;
+    uint8_t* out = codes + ((int64_t)h * g.M + u) * g.pitch * kTmaD + lane * VEC;
     const uint2* tile = reinterpret_cast<const uint2*>(smem + st * kTmaStageBytes) + lane;
+    uint32_t* const peak_slot = &s_peak[k % 3];
     mbar_wait(&full[st], (k / kTmaStages) & 1);
-    uint32_t m = 0;
+    if (warp == 0) FPSA_QTL(k, 1);
     if (!channel) {
+      uint32_t m = 0;
 #pragma unroll 8
       for (int32_t r = warp; r < g.tv; r += kTmaConsumerWarps) m = absmax_bits<__nv_bfloat16, VEC>(tile[r * 32], m);
       m = __float_as_uint(bits_to_peak<__nv_bfloat16>(m));
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
-      if (lane == 0) atomicMax(&s_peak[k & 1], m);
+      if (lane == 0) atomicMax(peak_slot, m);
     }
     named_bar_sync(1, kTmaConsumerWarps * 32);
-    if (threadIdx.x == 0) s_count[(k + 1) & 1] = s_peak[(k + 1) & 1] = 0;
+    // slot (k + 2) % 3 was last read after the previous barrier and is next written after the following one
+    if (threadIdx.x == 0) s_peak[(k + 2) % 3] = 0;
+    if (warp == 0) FPSA_QTL(k, 2);
     float pk[VEC];
     Bracket b[VEC];
     if (!channel) {
-      float peak = __uint_as_float(s_peak[k & 1]);
+      float peak = __uint_as_float(*peak_slot);
       if (!(peak <= FLT_MAX)) {
         if (warp == 0 && lane == 0 && a.err) atomicOr(a.err, 1);
         peak = 0.0f;
@@ -806,10 +834,11 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
     bool fast_ok = true;
 #pragma unroll
     for (int e = 0; e < VEC; ++e) fast_ok &= b[e].ok;
-    uint32_t* count = &s_count[k & 1];
-    uint16_t* queue = s_queue[k & 1];
+    const uint32_t force = fast_ok ? 0u : 0xFFFFFFFFu;  // a bracket out of range: every element exact
+    uint32_t amb = 0;  // bit i: row warp + i * kTmaConsumerWarps has an ambiguous element in this lane
+    int32_t i = 0;
 #pragma unroll 4
-    for (int32_t r = warp; r < g.tv; r += kTmaConsumerWarps) {
+    for (int32_t r = warp; r < g.tv; r += kTmaConsumerWarps, ++i) {
       float v[VEC];
       V::unpack(tile[r * 32], v);
       uint32_t clo = 0, chi = 0;
@@ -822,34 +851,33 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
         chi |= cvt_pair<FMT>(h1, h0) << (8 * e);
       }
       store_codes<VEC>(out + (int64_t)r * kTmaD, clo);
-      uint32_t diff = fast_ok ? (clo ^ chi) : 0xFFFFFFFFu;
-      while (diff) {  // rare: enqueue each ambiguous byte as (row, column)
-        const int e = (__ffs(diff) - 1) >> 3;
-        diff &= ~(0xFFu << (8 * e));
-        const uint32_t slot = atomicAdd(count, 1u);
-        if (slot < kTmaQueueCap) queue[slot] = (uint16_t)((r << 7) | (lane * VEC + e));
-      }
+      amb |= ((clo ^ chi) | force) != 0u ? 1u << i : 0u;
     }
-    named_bar_sync(1, kTmaConsumerWarps * 32);
-    const uint32_t n = *count;
-    if (n <= kTmaQueueCap) {
-      for (uint32_t i = threadIdx.x; i < n; i += kTmaConsumerWarps * 32) {
-        const uint32_t rc = queue[i];
-        const int32_t r = rc >> 7, c = rc & 127;
-        const uint16_t bits = reinterpret_cast<const uint16_t*>(smem + st * kTmaStageBytes)[r * kTmaD + c];
-        const float xv = __uint_as_float((uint32_t)bits << 16);
-        const float peak = channel ? __uint_as_float(a.amax[(int64_t)h * kTmaD + c]) : pk[0];
-        out_tile[(int64_t)r * kTmaD + c] = (uint8_t)encode_exact<FMT>(xv, scale_of(peak <= FLT_MAX ? peak : 0.0f, kMax));
+    while (amb) {  // rare: this lane's rows with ambiguous bytes, re-encoded from the f64 quotient
+      const int32_t ri = __ffs(amb) - 1;
+      amb &= amb - 1;
+      const int32_t r = warp + ri * kTmaConsumerWarps;
+      float v[VEC];
+      V::unpack(tile[r * 32], v);
+      uint32_t clo = 0, chi = 0;
+#pragma unroll
+      for (int e = 0; e < VEC; e += 2) {
+        float l0, l1, h0, h1;
+        mul2(v[e], v[e + 1], b[e].lo, b[e + 1].lo, l0, l1);
+        mul2(v[e], v[e + 1], b[e].hi, b[e + 1].hi, h0, h1);
+        clo |= cvt_pair<FMT>(l1, l0) << (8 * e);
+        chi |= cvt_pair<FMT>(h1, h0) << (8 * e);
       }
-    } else {
-      // queue overflow (adversarial data): exact pass over the whole tile
-      for (int32_t r = warp; r < g.tv; r += kTmaConsumerWarps) {
-        float v[VEC];
-        V::unpack(tile[r * 32], v);
-        store_codes<VEC>(out + (int64_t)r * kTmaD, encode_slow<FMT, VEC>(v, pk));
-      }
+      const uint32_t diff = (clo ^ chi) | force;
+#pragma unroll
+      for (int e = 0; e < VEC; ++e)
+        if ((diff >> (8 * e)) & 0xFFu)
+          clo = (clo & ~(0xFFu << (8 * e))) | (encode_exact<FMT>(v[e], scale_of(pk[e], kMax)) << (8 * e));
+      store_codes<VEC>(out + (int64_t)r * kTmaD, clo);
     }
     __syncwarp();
+    if (warp == 0) FPSA_QTL(k, 3);
+    if (warp == kTmaConsumerWarps - 1) FPSA_QTL(k, 4);
     if (lane == 0) mbar_arrive(&empty[st]);
     for (int32_t r = g.tv + warp; r < g.pitch; r += kTmaConsumerWarps) store_codes<VEC>(out + (int64_t)r * kTmaD, 0u);
   }
@@ -1329,3 +1357,10 @@ extern "C" int fpsa_decode(const uint8_t* codes, int64_t n, int fmt, const doubl
 #undef FPSA_DEC
   return cuda_status("fpsa_decode");
 }
+
+#ifdef FPSA_QTRACE
+extern "C" int fpsa_qtrace_timeline(long long* out) {
+  cudaMemcpyFromSymbol(out, fpsa::g_qtl, sizeof(fpsa::g_qtl));
+  return (int)(sizeof(fpsa::g_qtl) / sizeof(long long));
+}
+#endif

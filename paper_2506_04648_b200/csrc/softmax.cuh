@@ -22,7 +22,7 @@ constexpr int kTlSteps = 256;
 __device__ long long g_tl[kTlSteps][10][4];
 #define FPSA_TL(slot, ev, step)                                                        \
   do {                                                                                 \
-    if (blockIdx.x == 0 && (threadIdx.x & 31) == 0 && (step) < kTlSteps)               \
+    if (blockIdx.x == 0 && (threadIdx.x & 31) == 0 && (step) < kTlSteps && (slot) < 10) \
       g_tl[(step)][(slot)][(ev)] = clock64();                                          \
   } while (0)
 #else

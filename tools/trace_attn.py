@@ -40,6 +40,17 @@ for j in range(2, 40):
     w0 = T[j, 0] - t0; w4 = T[j, 4] - t0; w1 = T[j, 1] - t0; m = T[j, 9] - t0
     print(f"{j:3d} | {w0[0]:7d} {w0[1]:7d} {w0[2]:7d} {w0[3]:7d} | {w4[1]:7d} {w4[2]:7d} {w4[3]:7d} | w1 {w1[1]:7d} {w1[3]:7d} | {m[1]:7d} {m[2]:7d} {m[3]:7d}")
 
+print("hand-off per step (clk): last owner arrival -> MMA at p_ready wait (TL0) / p_ready ok (TL1) / PV+QK issued (TL2) / S(j+2) ready at its owner")
+rows = []
+for j in range(4, 120):
+    own = range(0, 4) if j % 2 == 0 else range(4, 8)
+    arr = max(T[j, w, 3] for w in own)
+    if arr <= 0 or T[j, 9, 1] <= 0 or T[j + 2, own[0], 1] <= 0:
+        continue
+    rows.append((T[j, 9, 0] - arr, T[j, 9, 1] - arr, T[j, 9, 2] - T[j, 9, 1], T[j + 2, own[0], 1] - T[j, 9, 2]))
+if rows:
+    r = np.array(rows)
+    print("  mean: MMA at wait %+.0f, p_ready ok %+.0f, issue %.0f, QK->S ready %.0f" % tuple(r.mean(0)))
 print("per-warp compute+store time (S-ready -> arrived), steps 2..60 mean, by warp (SMSP = warp % 4):")
 for w in range(8):
     d = [T[j, w, 3] - T[j, w, 1] for j in range(2, 60) if T[j, w, 3] > 0]
