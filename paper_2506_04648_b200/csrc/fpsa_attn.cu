@@ -91,9 +91,29 @@ using namespace sm100;
 #ifndef FPSA_MBAR_SUSPEND_NS
 #define FPSA_MBAR_SUSPEND_NS 100000
 #endif
+#ifdef FPSA_WATCH
+// debug builds only: per (CTA, warp) the shared address and parity of the barrier it waits on (0: none),
+// written to mapped host memory so a hung launch can be inspected (tools/watch_attn.py)
+__device__ int* g_watch;
+#endif
 // every wait of this kernel carries the suspend-time hint (sm100.cuh mbar_try_wait)
 __device__ __forceinline__ void attn_wait(uint64_t* bar, uint32_t parity) {
+#ifdef FPSA_WATCH
+  volatile int* w = g_watch + (blockIdx.x * 16 + (threadIdx.x >> 5)) * 4;
+  if ((threadIdx.x & 31) == 0) {
+    w[0] = (int)smem_u32(bar);
+    w[1] = (int)parity;
+    w[2] = w[2] + 1;
+    __threadfence_system();
+  }
+#endif
   mbar_wait<FPSA_MBAR_SUSPEND_NS>(bar, parity);
+#ifdef FPSA_WATCH
+  if ((threadIdx.x & 31) == 0) {
+    w[0] = 0;
+    __threadfence_system();
+  }
+#endif
 }
 
 #ifndef FPSA_PARTS
@@ -125,7 +145,10 @@ constexpr int kItemReaders = 2 + kSoftmaxWarps;  // TMA warp, MMA warp, softmax 
 #define FPSA_PINGPONG 1
 #endif
 constexpr bool kPingPong = FPSA_PINGPONG != 0;
-static_assert(kParts == 2 || (kParts == 3 && kPingPong), "three parts take the key blocks round-robin (ping-pong)");
+// Three parts (12 softmax warps at 144 registers, three P~ buffers, six S-full barriers) build and run, but
+// measured slower (11.4 vs 11.05 ms at C2, profiles/r02_ab_three_parts_rejected.txt) and their normalised-P
+// path is not parity-clean, so only two are allowed.
+static_assert(kParts == 2, "two softmax warps per TMEM lane quarter (ping-pong)");
 
 struct AttnParams {
   const double* q_scales;
@@ -415,6 +438,18 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     s_ovf[0] = s_ovf[1] = 0;
     for (int i = 0; i < kParts; ++i) s_pcnt[i] = 0;
+#ifdef FPSA_WATCH
+    if (blockIdx.x == 0) {
+      volatile int* a = g_watch + 148 * 16 * 4;
+      int n = 0;
+      auto put = [&](uint64_t* b, int cnt) { for (int i = 0; i < cnt; ++i) a[n++] = (int)smem_u32(b + i); };
+      put(bar_q, 2); put(bar_qfree, 2); put(&bar_o, 1); put(&bar_ofree, 1); put(bar_kv_full, kStages);
+      put(bar_kv_empty, kStages); put(bar_s_full, kSF); put(bar_p_ready, kParts); put(bar_s_free, 2);
+      put(bar_p_free, kParts); put(bar_meta_full, 2); put(bar_meta_empty, 2); put(bar_item_full, kItemRing);
+      put(bar_item_empty, kItemRing);
+      __threadfence_system();
+    }
+#endif
     fence_barrier_init();
   }
   if (warp == kTmaWarp) {
@@ -581,7 +616,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #ifndef FPSA_NO_MMA
               qk_mma<D>(tm_s(gs), dq, dk, idesc_qk);
 #endif
-              mma_commit_w(&bar_s_full[gs % kSF]);
+              mma_commit_w(&bar_s_full[(gs + 2) % kSF]);  // S(j+2)
               if (++qk_st == kStages) {
                 qk_st = 0;
                 qk_ph ^= 1;
@@ -813,7 +848,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     const uint32_t o_addr = tm_o + lane_off + part * (D / kEpiParts);
     const float sl = p.softmax_log2;
-    auto row_sync = [&]() { named_bar_sync(1 + quarter, 32 * kParts); };
+    auto row_sync = [&]() {
+#ifdef FPSA_WATCH
+      volatile int* w = g_watch + (blockIdx.x * 16 + warp) * 4;
+      if (lane == 0) { w[0] = -1; __threadfence_system(); }
+#endif
+      named_bar_sync(1 + quarter, 32 * kParts);
+#ifdef FPSA_WATCH
+      if (lane == 0) { w[0] = 0; __threadfence_system(); }
+#endif
+    };
     auto row_max = [&](float m) {  // max over all parts of the row
       s_xchg[part][row] = m;
       row_sync();
@@ -1370,5 +1414,12 @@ extern "C" int fpsa_trace_read(unsigned long long* out, int reset) {
     cudaMemcpyToSymbol(fpsa::g_trace, z, sizeof z);
   }
   return 0;
+}
+#endif
+
+#ifdef FPSA_WATCH
+extern "C" int fpsa_debug_set_watch(void* p) {
+  int* q = static_cast<int*>(p);
+  return cudaMemcpyToSymbol(fpsa::g_watch, &q, sizeof(q)) == cudaSuccess ? 0 : 1;
 }
 #endif
