@@ -353,3 +353,31 @@ def test_full_size_head_passthrough(fpsa):
     print(f"passthrough {grid}: cos={cos:.7f} max-abs={mabs:.3e}")
     assert cos >= 0.9999
     assert mabs <= 1e-2 * float(np.abs(ref).max())
+
+
+@pytest.mark.parametrize("grid,tile,win,d", [
+    ((4, 6, 9), (1, 3, 3), (3, 3, 3), 64),     # tv = 9: cheap max / sum passes, many steps per item
+    ((6, 8, 8), (3, 4, 4), (3, 3, 3), 128),    # tv = 48
+])
+@pytest.mark.parametrize("p_mode", ["normalized", "onepass"])
+def test_split_issue_repeated_launches(fpsa, grid, tile, win, d, p_mode):
+    """The split QK / PV issue under repetition: 300 launches of the multi-pass modes (normalised P: three
+    passes; one-pass with tau = 0: saturating items go to the exact-max redo launch, two passes) on small
+    tiles.  Their max / sum passes store no P~, so without the p_free wait before each p_ready signal one
+    softmax part could signal two phases of its p_ready barrier while the PV warp waits for the other
+    part, a deadlock the first split build hit twice in full GPU-suite runs (K4).
+    The race is timing-dependent and this test did not reproduce it on demand (2 x 1200 launches of the
+    unfixed build passed), so it guards the schedule's determinism: every repetition must reproduce the
+    first output bit for bit."""
+    L = grid[0] * grid[1] * grid[2]
+    q, k, v = O.gen_inputs(5, 1, 0, L, d)
+    plan = fpsa.FpsaPlan(grid, tile, win, 1, d, p_mode=p_mode, tau=0.0 if p_mode == "onepass" else 8.0)
+    out = torch.empty((L, d), dtype=torch.float32, device="cuda")
+    args = [torch.from_numpy(x).cuda() for x in (q, k, v)]
+    plan.quantize(*args, layout="ld", tile_order=True)
+    plan.attention(out, layout="ld", tile_order=True)
+    first = out.clone()
+    for _ in range(300):
+        plan.attention(out, layout="ld", tile_order=True)
+    torch.cuda.synchronize()
+    assert torch.equal(out, first)
