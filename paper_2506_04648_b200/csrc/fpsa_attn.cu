@@ -78,6 +78,9 @@
 #ifndef FPSA_PREADY_SPIN
 #define FPSA_PREADY_SPIN 0  // P~(j) hand-off to the MMA warp through a shared-memory counter instead of an mbarrier
 #endif
+#ifndef FPSA_GEOM_PREFETCH
+#define FPSA_GEOM_PREFETCH 1  // next block's geometry / factors computed during the current S load
+#endif
 #ifndef FPSA_PACK_FASTPATH
 #define FPSA_PACK_FASTPATH 1  // packed blocks inside one key tile take the per-tile softmax code
 #endif
@@ -977,13 +980,22 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           m_ref = row_max(m0);
         }
+        // block geometry and key-tile factors of this warp's next block, computed while the current
+        // block's S is loaded (FPSA_GEOM_PREFETCH) instead of between its P~ signal and the next S wait
+        int32_t nx_kt = 0, nx_split = 0, nx_nvalid = 0;
+        float nx_ca = 0.0f, nx_cb = 0.0f;
+        auto geom = [&](int32_t jj) {
+          block_at<PACKED>(p, n_kt, jj, nx_kt, nx_split, nx_nvalid);
+          factors(nx_kt, nx_split, nx_nvalid, nx_ca, nx_cb);
+        };
+        if (FPSA_GEOM_PREFETCH && first_owned(g) < n_kv) geom(first_owned(g));
         for (int32_t j = first_owned(g); j < n_kv; j += kParts) {
           const uint32_t g_own = g + j;
           {
-            int32_t kt_a, split, nvalid;
-            block_at<PACKED>(p, n_kt, j, kt_a, split, nvalid);
-            float ca, cb;
-            factors(kt_a, split, nvalid, ca, cb);
+            if (!FPSA_GEOM_PREFETCH) geom(j);
+            const int32_t kt_a = nx_kt, split = nx_split, nvalid = nx_nvalid;
+            const float ca = nx_ca, cb = nx_cb;
+            (void)kt_a;
 #ifdef FPSA_TRACE
             const long long ts0 = clock64();
 #endif
@@ -1016,6 +1028,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             {
               uint32_t sreg[64];
               load_s_all<64>(s_row, sreg);
+              if (FPSA_GEOM_PREFETCH && j + kParts < n_kv) geom(j + kParts);
               tmem_wait_ld();
               half(0, sreg);
             }
