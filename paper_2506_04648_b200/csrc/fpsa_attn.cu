@@ -81,6 +81,9 @@
 #ifndef FPSA_GEOM_PREFETCH
 #define FPSA_GEOM_PREFETCH 1  // next block's geometry / factors computed during the current S load
 #endif
+#ifndef FPSA_P_STORE_SPLIT
+#define FPSA_P_STORE_SPLIT 1  // store the two 64-key halves of P~ separately (the first during the second's exp)
+#endif
 #ifndef FPSA_PACK_FASTPATH
 #define FPSA_PACK_FASTPATH 1  // packed blocks inside one key tile take the per-tile softmax code
 #endif
@@ -1032,6 +1035,12 @@ __global__ void __launch_bounds__(kThreads, 1)
               tmem_wait_ld();
               half(0, sreg);
             }
+            if constexpr (kEarly && FPSA_P_STORE_SPLIT) {
+              // the first 64 keys' P~ go out while the second half is computed
+              if (g_own >= (uint32_t)kParts) attn_wait(&bar_p_free[g_own % kParts], ((g_own / kParts) - 1) & 1);
+              tc_fence_after();
+              tmem_st16(tm_p(g_own) + lane_off, w);
+            }
             {
               uint32_t sreg[64];
               load_s_all<64>(s_row + 64, sreg);
@@ -1043,7 +1052,9 @@ __global__ void __launch_bounds__(kThreads, 1)
               }
               half(1, sreg);
             }
-            if constexpr (kEarly) {
+            if constexpr (kEarly && FPSA_P_STORE_SPLIT) {
+              tmem_st16(tm_p(g_own) + 16 + lane_off, w + 16);
+            } else if constexpr (kEarly) {
               // P~(j) into its own columns once PV(j - 2) has read them
               if (g_own >= (uint32_t)kParts) attn_wait(&bar_p_free[g_own % kParts], ((g_own / kParts) - 1) & 1);
               tc_fence_after();
