@@ -671,9 +671,6 @@ struct TmaQuantArgs {
 #ifndef FPSA_QUANT_ORDER
 #define FPSA_QUANT_ORDER 0  // 0: (tensor, head, tile) with tiles fastest; 1: (tensor, tile, head), heads fastest
 #endif
-#ifndef FPSA_QUANT_PREFETCH
-#define FPSA_QUANT_PREFETCH 0  // tiles prefetched into L2 ahead of the stage-bound loads (0: none)
-#endif
 #ifndef FPSA_QUANT_LOADONLY
 #define FPSA_QUANT_LOADONLY 0
 #endif
@@ -734,25 +731,9 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
       prefetch_tmap(&tm0);
       prefetch_tmap(&tm1);
       prefetch_tmap(&tm2);
-      // L2 prefetch of the whole tile FPSA_QUANT_PREFETCH items ahead: the tile's rows (256 B each at the
-      // token stride) are in L2 when its stage frees, so the stage-bound load does not pay DRAM latency
-      auto prefetch = [&](int32_t pit) {
-        if (pit >= n_items || !a.whole_tile) return;
-        int32_t z, h, u;
-        item_of(pit, per_job, a.heads, g.M, z, h, u);
-        const void* tm = z == 0 ? (const void*)&tm0 : (z == 1 ? (const void*)&tm1 : (const void*)&tm2);
-        if (g.natural) {
-          const int32_t ut = u / (g.dh * g.dw), uh = (u / g.dw) % g.dh, uw = u % g.dw;
-          tma_prefetch_5d(tm, 0, h, uw * g.sw, uh * g.sh, ut * g.st);
-        } else {
-          tma_prefetch_3d(tm, 0, u * g.tv, h);
-        }
-      };
-      for (int i = 1; i <= FPSA_QUANT_PREFETCH; ++i) prefetch(blockIdx.x + (i - 1 + kTmaStages) * gridDim.x);
       int k = 0;
       for (int32_t it = blockIdx.x; it < n_items; it += gridDim.x, ++k) {
         const int st = k % kTmaStages;
-        if (FPSA_QUANT_PREFETCH > 0) prefetch(it + (FPSA_QUANT_PREFETCH + kTmaStages - 1) * gridDim.x);
         if (k >= kTmaStages) mbar_wait(&empty[st], ((k / kTmaStages) - 1) & 1);
         int32_t z, h, u;
         item_of(it, per_job, a.heads, g.M, z, h, u);
