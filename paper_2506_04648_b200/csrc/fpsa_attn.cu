@@ -66,23 +66,8 @@
 #include "sm100.cuh"
 #include "softmax.cuh"
 
-#ifndef FPSA_MMA_HOIST
-#define FPSA_MMA_HOIST 1
-#endif
-#ifndef FPSA_MMA_ONE_ELECT
-#define FPSA_MMA_ONE_ELECT 1
-#endif
-#ifndef FPSA_EARLY_QK
-#define FPSA_EARLY_QK 2  // P~ in its own TMEM columns, QK(j+2) issued once S(j) is in registers (D = 128);
-#endif                    // 2: QK and PV issued by two different warps (warp 9 / warp 11)
-#ifndef FPSA_PREADY_SPIN
-#define FPSA_PREADY_SPIN 0  // P~(j) hand-off to the MMA warp through a shared-memory counter instead of an mbarrier
-#endif
 #ifndef FPSA_GEOM_PREFETCH
 #define FPSA_GEOM_PREFETCH 1  // next block's geometry / factors computed during the current S load
-#endif
-#ifndef FPSA_P_STORE_SPLIT
-#define FPSA_P_STORE_SPLIT 1  // store the two 64-key halves of P~ separately (the first during the second's exp)
 #endif
 #ifndef FPSA_PACK_FASTPATH
 #define FPSA_PACK_FASTPATH 1  // packed blocks inside one key tile take the per-tile softmax code
@@ -122,40 +107,28 @@ __device__ __forceinline__ void attn_wait(uint64_t* bar, uint32_t parity) {
 #endif
 }
 
-#ifndef FPSA_PARTS
-#define FPSA_PARTS 2  // softmax warps per SMSP (per TMEM lane quarter); 3 needs the split-issue ping-pong path
-#endif
-constexpr int kParts = FPSA_PARTS;              // softmax warps sharing one TMEM lane quarter (row)
+// Ping-pong softmax: the two warps of an SMSP (one TMEM lane quarter) take alternate key blocks, each
+// computing whole 128-key rows (both warps on the two halves of every block measured 12.65 vs 12.1 ms;
+// three warps per SMSP at 144 registers 11.4 vs 11.05 ms, profiles/r02_ab_three_parts_rejected.txt).
+constexpr int kParts = 2;                       // softmax warps sharing one TMEM lane quarter (row)
 constexpr int kEpiParts = 2;                    // parts that read O in the epilogue (D / 2 channels each)
-[[maybe_unused]] constexpr int kPartCols = 128 / kParts;  // S columns per softmax thread in the FPSA_PINGPONG=0 variant
 constexpr int kSoftmaxWarps = 4 * kParts;
 constexpr int kTmaWarp = kSoftmaxWarps;
-constexpr int kMmaWarp = kSoftmaxWarps + 1;
-constexpr int kThreads = (kSoftmaxWarps + 4) * 32;  // softmax warpgroups + 1 producer (TMA, MMA, helper, idle)
+constexpr int kMmaWarp = kSoftmaxWarps + 1;     // issues the QKs
+constexpr int kHelperWarp = kSoftmaxWarps + 2;  // claims items, prefetches their metadata
+constexpr int kPvWarp = kSoftmaxWarps + 3;      // issues the PVs
+constexpr int kThreads = (kSoftmaxWarps + 4) * 32;  // two softmax warpgroups + the producer warpgroup
 // setmaxnreg split of the 64K-register file: per SMSP one warp of each warpgroup
 // (4 warps per quarter at 104 registers was measured slower: 13.4 vs 12.8 ms at C2; 112/64 deadlocks)
-constexpr uint32_t kRegsSoftmax = kParts == 2 ? 216 : 144, kRegsProducer = 64;
+constexpr uint32_t kRegsSoftmax = 216, kRegsProducer = 64;
 
 constexpr int kStages = 4;     // K/V ring depth (128-key blocks)
 constexpr int kBlk = 128;      // rows per query block = keys per key block
 constexpr float kLog2_448 = 8.807354922057604f;
 constexpr int kRedoHeader = 4;  // int32 words before the redo items in the workspace
 constexpr int kFacCap = 512;    // key-tile factors per item kept in shared memory (more: read from L2)
-constexpr int kHelperWarp = kSoftmaxWarps + 2;  // producer-warpgroup warp that claims items, prefetches metadata
 constexpr int kItemRing = 4;                    // claimed items in flight between the helper and the other roles
-constexpr int kItemReaders = 2 + kSoftmaxWarps;  // TMA warp, MMA warp, softmax warps
-// Ping-pong softmax: the warps w and w+4 of an SMSP (same TMEM lane quarter) take alternate key blocks,
-// each computing whole 128-key rows.  FPSA_PINGPONG=0 builds the earlier variant in which the two warps
-// take the two 64-column halves of every block (slower: 12.65 vs 12.1 ms at C2).
-#ifndef FPSA_PINGPONG
-#define FPSA_PINGPONG 1
-#endif
-constexpr bool kPingPong = FPSA_PINGPONG != 0;
-// Three parts (12 softmax warps at 144 registers, three P~ buffers, six S-full barriers) build and run, but
-// measured slower (11.4 vs 11.05 ms at C2, profiles/r02_ab_three_parts_rejected.txt) and their normalised-P
-// path is not parity-clean, so only two are allowed.
-static_assert(kParts == 2, "two softmax warps per TMEM lane quarter (ping-pong)");
-
+constexpr int kItemReaders = 3 + kSoftmaxWarps;  // TMA, QK and PV warps, softmax warps
 struct AttnParams {
   const double* q_scales;
   const double* k_scales;
@@ -342,7 +315,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                      const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ SegMaps seg,
                      const AttnParams p) {
   using S = Smem<D>;
-  static_assert(kPingPong || (!NORM && !PACKED), "the normalised-P and packed-key paths are ping-pong only");
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   __shared__ uint64_t bar_q[2], bar_qfree[2];  // query-block buffer (item parity): loaded / no longer read
@@ -350,11 +322,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   __shared__ uint64_t bar_kv_full[kStages], bar_kv_empty[kStages];
   // S(j) full: by j mod kSF (a waiter is never two phases ahead); P~(j) ready / its buffer free: by j mod
   // kParts (the owning part); S buffer j mod 2 loaded by its owners (early QK)
-  constexpr int kSF = kParts == 2 ? 2 : 6;
+  constexpr int kSF = 2;
   __shared__ uint64_t bar_s_full[kSF], bar_p_ready[kParts];
   __shared__ uint64_t bar_s_free[2], bar_p_free[kParts];
   __shared__ uint32_t s_tmem;
-  __shared__ uint32_t s_pcnt[kParts];  // FPSA_PREADY_SPIN: P~-ready arrivals by owning part
   __shared__ float s_xchg[kParts][kBlk];  // [part][row] exchange between the warps of a row
   // per-item metadata, prefetched by the helper warp one item ahead (slot = item parity)
   __shared__ float s_fac[2][kFacCap];  // key-tile factors c(kt) = (sq * sk) * scale log2 e
@@ -386,8 +357,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     return h >= 0;
   };
 
-  // P~(gg) ready (or S(gg) consumed): one arrival per owning warp; the MMA warp waits for all of them
-  [[maybe_unused]] constexpr uint32_t kPArrivals = kPingPong ? kSoftmaxWarps / kParts : kSoftmaxWarps;
+  // P~(gg) ready (or S(gg) consumed): one arrival per owning warp; the PV warp waits for all of them
+  constexpr uint32_t kPArrivals = kSoftmaxWarps / kParts;
   // barrier slot and phase of step gg: S full (kSF slots), P~ ready / P~ buffer free (kParts slots)
   auto sf_wait = [&](uint32_t gg) { attn_wait(&bar_s_full[gg % kSF], (gg / kSF) & 1); };
   // Split issue: before P~(gg) ready (or S(gg) consumed) is signalled, PV(gg - kParts) must have been
@@ -396,31 +367,16 @@ __global__ void __launch_bounds__(kThreads, 1)
   // P~, wait here (without it the softmax could signal two phases of one barrier before the PV warp
   // observed the first, and the PV warp would then wait for a phase that needs its own K/V release).
   auto p_free_wait = [&](uint32_t gg) {
-    if constexpr (FPSA_EARLY_QK == 2 && kPingPong)
-      if (gg >= (uint32_t)kParts) attn_wait(&bar_p_free[gg % kParts], ((gg / kParts) - 1) & 1);
+    if (gg >= (uint32_t)kParts) attn_wait(&bar_p_free[gg % kParts], ((gg / kParts) - 1) & 1);
   };
-  auto p_arrive = [&](uint32_t gg) {  // lane 0 of an owning warp, after its tcgen05 fence
-    if constexpr (FPSA_PREADY_SPIN)
-      asm volatile("red.release.cta.shared::cta.add.u32 [%0], 1;" ::"r"(smem_u32(&s_pcnt[gg % kParts])) : "memory");
-    else
-      mbar_arrive(&bar_p_ready[gg % kParts]);
-  };
-  auto p_wait = [&](uint32_t gg) {
-    if constexpr (FPSA_PREADY_SPIN) {
-      const uint32_t want = kPArrivals * ((gg / kParts) + 1u), addr = smem_u32(&s_pcnt[gg % kParts]);
-      uint32_t v;
-      do {
-        asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
-      } while ((int32_t)(v - want) < 0);
-    } else {
-      attn_wait(&bar_p_ready[gg % kParts], (gg / kParts) & 1);
-    }
-  };
+  // (a shared-memory counter instead of the p_ready mbarrier measured slower: 11.5-11.65 vs 11.26-11.33 ms)
+  auto p_arrive = [&](uint32_t gg) { mbar_arrive(&bar_p_ready[gg % kParts]); };  // lane 0, after its fence
+  auto p_wait = [&](uint32_t gg) { attn_wait(&bar_p_ready[gg % kParts], (gg / kParts) & 1); };
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < kItemRing; ++i) {
       mbar_init(&bar_item_full[i], 1);
-      mbar_init(&bar_item_empty[i], kItemReaders + (FPSA_EARLY_QK == 2 && kPingPong ? 1 : 0));
+      mbar_init(&bar_item_empty[i], kItemReaders);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&bar_q[i], 1);
@@ -443,7 +399,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&bar_kv_empty[i], 1);
     }
     s_ovf[0] = s_ovf[1] = 0;
-    for (int i = 0; i < kParts; ++i) s_pcnt[i] = 0;
 #ifdef FPSA_WATCH
     if (blockIdx.x == 0) {
       volatile int* a = g_watch + 148 * 16 * 4;
@@ -481,13 +436,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tm_o = tmem;  // O: columns 0..D-1, row sums of P~: D..D+15
   // S buffers at columns 256 and 384 (computed, not indexed: a local array would live in memory)
   auto tm_s = [tmem](uint32_t g) { return tmem + 256u + 128u * (g & 1u); };
-  // early-QK mode: P~(j) in its own 32 columns (160 / 192), so S(j)'s buffer is free once loaded
-  constexpr bool kEarly = FPSA_EARLY_QK && kPingPong;
-  static_assert(kParts == 2 || (kEarly && FPSA_EARLY_QK == 2), "three parts need the split QK / PV issue");
-  // split issue: warp 9 issues the QKs (on S(j) loaded), warp 11 the PVs (on P~(j) stored); QK and PV touch
-  // disjoint TMEM (S buffers / P~ buffers and O), and every PV comes from the one PV warp, in order
-  constexpr bool kSplit = kEarly && FPSA_EARLY_QK == 2;
-  constexpr int kPvWarp = kSoftmaxWarps + 3;
+  // P~(j) in its own 32 columns (160 / 192), so S(j)'s buffer is free once loaded.  Split issue: warp 9
+  // issues the QKs (on S(j - 2) loaded), warp 11 the PVs (on P~(j) stored); QK and PV touch disjoint TMEM
+  // (S buffers / P~ buffers and O), and every PV comes from the one PV warp, in order
   auto tm_p = [tmem](uint32_t g) { return tmem + 160u + 32u * (g % (uint32_t)kParts); };
   static_assert(D + 16 <= 160 && 160 + 32 * kParts <= 256, "TMEM: O | P~ buffers | S buffers at 256 and 384");
   const float tau = p.exact ? 0.0f : p.tau;
@@ -548,221 +499,44 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == kMmaWarp) {
-    // ------------------------------------------------------------ MMA issuer (warp-uniform, one elected lane issues)
+    // ------------------------------------------------------------ QK issuer (warp-uniform, one elected lane issues)
+    // S(j) = Q K^T into TMEM buffer j % 2, issued as soon as the owners of S(j - 2) have it in registers
+    // (s_free); the PVs come from the PV warp.  Descriptors are built once; a K-chunk / stage step only
+    // moves the 14-bit start-address field (16-byte units), which never carries out.
     constexpr uint32_t idesc_qk = idesc_f8(128, 128, FMT, FMT, 0);
-    constexpr uint32_t idesc_pv = idesc_f8(128, D + 16, FPSA_E4M3, FMT, 1);
-    // Descriptors are built once; a K-chunk / stage step only moves the 14-bit
-    // start-address field (16-byte units), which never carries out.
     constexpr uint64_t kTileU = S::kTile >> 4;
-    const uint32_t sv0 = smem_u32(smem + S::kV);
     const uint64_t dq0 = desc_kmajor<D>(smem_u32(smem + S::kQ));
     const uint64_t dk0 = desc_kmajor<D>(smem_u32(smem + S::kK));
-    // V stage st: start sv0 + st*tile, leading byte offset to the ones atom shrinks by the same amount
-    const uint64_t dv0 = desc_mnmajor_ones<D>(sv0, smem_u32(smem + S::kOnes) - sv0);
-    // a tile's last block: padding keys (zero K and V rows) get zero rows in the ones atom, so their
-    // P~ codes, whatever they are, add nothing to the row sum either
-    const uint64_t dvt0 = desc_mnmajor_ones<D>(sv0, smem_u32(smem + S::kOnesTail) - sv0);
-    constexpr uint64_t kVStageStep = kTileU - (kTileU << 16);
     uint32_t g = 0;
     uint32_t qk_st = 0, qk_ph = 0;  // K/V stage + full-barrier phase of the next QK
-    uint32_t pv_st = 0;             // K/V stage of the next PV
     int32_t h, u, qb;
     for (int32_t iter = 0; next_item(iter, h, u, qb); ++iter) {
       const int32_t n_kt = __ldg(p.offs + u + 1) - __ldg(p.offs + u);
-      const int32_t n_kv = blocks_per_pass<PACKED>(p, n_kt), steps = passes * n_kv;
-      const int32_t pv0 = (passes - 1) * n_kv;  // first step with a PV
+      const int32_t steps = passes * blocks_per_pass<PACKED>(p, n_kt);
       const int qbuf = iter & 1;
       const uint64_t dq = dq0 + (uint64_t)qbuf * kTileU;
       attn_wait(&bar_q[qbuf], (iter >> 1) & 1);
       tc_fence_after();
-      int32_t b2 = 0;  // in-tile block of the next QK
-      int32_t bp = 0;  // in-tile block of the current step (both passes cycle through whole tiles)
-      // S(step gg) = Q K^T into TMEM buffer gg % 2
-      auto issue_qk = [&](uint32_t gg) {
+      for (int32_t s = 0; s < steps; ++s) {
+        const uint32_t gs = g + s;
         attn_wait(&bar_kv_full[qk_st], qk_ph);
-        if (kEarly && gg >= 2) attn_wait(&bar_s_free[gg & 1], ((gg - 2) >> 1) & 1);  // S(gg - 2) loaded
+        if (gs >= 2) attn_wait(&bar_s_free[gs & 1], ((gs - 2) >> 1) & 1);  // S(gs - 2) is in registers
         tc_fence_after();
-        const uint64_t dk = dk0 + qk_st * kTileU;
-        // N = 128 for every block: a tile's last block reads zero K rows past tv (S = 0 there,
-        // finite), which the softmax drops; below N = 256 an MMA costs the same at any N.
-        const uint32_t idq = idesc_qk;
-        const uint32_t ts = tm_s(gg);
+        // N = 128 for every block: a tile's last block reads zero K rows past tv (S = 0 there, finite),
+        // which the softmax drops; below N = 256 an MMA costs the same at any N
 #ifndef FPSA_NO_MMA
-        if constexpr (D == 128) {  // one elect for the four K32 MMAs (shorter issue path)
-          mma_f8_ss_x4_w(ts, dq, dq + 2, dq + 4, dq + 6, dk, dk + 2, dk + 4, dk + 6, idq, 0u);
-        } else {
-#pragma unroll
-          for (int k = 0; k < D / 32; ++k) mma_f8_ss_w(ts, dq + 2 * k, dk + 2 * k, idq, k > 0 ? 1u : 0u);
-        }
+        qk_mma<D>(tm_s(gs), dq, dk0 + qk_st * kTileU, idesc_qk);
 #endif
-        mma_commit_w(&bar_s_full[gg % kSF]);
-        if (++b2 == p.nb) b2 = 0;
+        mma_commit_w(&bar_s_full[gs % kSF]);
+        if (s + 1 == steps) mma_commit_w(&bar_qfree[qbuf]);  // the item's last QK has read Q
         if (++qk_st == kStages) {
           qk_st = 0;
           qk_ph ^= 1;
         }
-      };
-      for (int32_t s = 0; s < min(steps, 2); ++s) issue_qk(g + s);
-      if (steps <= 2) mma_commit_w(&bar_qfree[qbuf]);
-#if FPSA_MMA_HOIST
-      if constexpr (kPingPong && (kEarly || D == 128)) {
-        // Everything that does not depend on P~(j) is done before waiting for it: the K/V-full wait and
-        // descriptors of QK(j+2), the V descriptor of PV(j), the O-free wait. After p_ready(j) the warp
-        // only issues PV(j), QK(j+2) and the commits (the issue path is the step's critical path).
-        if constexpr (kEarly) {
-          // QK(j+2) as soon as the owners of S(j) have it in registers, then PV(j) from its P~ buffer
-          for (int32_t s = 0; s < steps; ++s) {
-            const uint32_t gs = g + s;
-            const bool do_qk = s + 2 < steps;
-            if (do_qk) {
-              attn_wait(&bar_kv_full[qk_st], qk_ph);
-              const uint64_t dk = dk0 + qk_st * kTileU;
-              attn_wait(&bar_s_free[gs & 1], (gs >> 1) & 1);
-              tc_fence_after();
-#ifndef FPSA_NO_MMA
-              qk_mma<D>(tm_s(gs), dq, dk, idesc_qk);
-#endif
-              mma_commit_w(&bar_s_full[(gs + 2) % kSF]);  // S(j+2)
-              if (++qk_st == kStages) {
-                qk_st = 0;
-                qk_ph ^= 1;
-              }
-              if (s + 3 == steps) mma_commit_w(&bar_qfree[qbuf]);
-            }
-            if constexpr (kSplit) continue;  // the PV warp issues PV(j)
-            constexpr uint64_t kVk = 32 * D / 16;
-            const uint64_t dv = (!PACKED && bp == p.nb - 1 ? dvt0 : dv0) + pv_st * kVStageStep;
-            if (s == pv0 && iter > 0) attn_wait(&bar_ofree, (iter - 1) & 1);  // the previous item's epilogue read O
-            FPSA_TL(9, 0, gs);
-            p_wait(gs);
-            FPSA_TL(9, 1, gs);
-            tc_fence_after();
-            const uint32_t tp = tm_p(gs);
-#ifndef FPSA_NO_MMA
-            if (s >= pv0)
-              mma_f8_ts_x4_w(tm_o, tp, tp + 8, tp + 16, tp + 24, dv, dv + kVk, dv + 2 * kVk, dv + 3 * kVk, idesc_pv,
-                             s > pv0 ? 1u : 0u);
-#endif
-            FPSA_TL(9, 2, gs);
-            mma_commit_w(&bar_kv_empty[pv_st]);
-            mma_commit_w(&bar_p_free[gs % kParts]);  // every step, so its phases count steps
-            FPSA_TL(9, 3, gs);
-            if (++pv_st == kStages) pv_st = 0;
-            if (++bp == p.nb) bp = 0;
-          }
-        } else {
-        for (int32_t s = 0; s < steps; ++s) {
-          const uint32_t gs = g + s;
-          const bool do_qk = s + 2 < steps;
-          uint64_t dk = 0;
-          if (do_qk) {
-            attn_wait(&bar_kv_full[qk_st], qk_ph);
-            dk = dk0 + qk_st * kTileU;
-          }
-          constexpr uint64_t kVk = 32 * D / 16;
-          uint64_t dv[4], dkk[4], dqq[4];
-          uint32_t ta[4];
-          // packed blocks zero the P~ codes of absent keys, so the plain ones atom serves every block
-          dv[0] = (!PACKED && bp == p.nb - 1 ? dvt0 : dv0) + pv_st * kVStageStep;
-          const uint32_t ts = tm_s(gs);  // S(j), P~(j) and S(j+2) share the buffer
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            dv[k] = dv[0] + k * kVk;
-            dkk[k] = dk + 2 * k;
-            dqq[k] = dq + 2 * k;
-            ta[k] = ts + 8 * k;
-          }
-          if (s == pv0 && iter > 0) attn_wait(&bar_ofree, (iter - 1) & 1);  // the previous item's epilogue read O
-          FPSA_TL(9, 0, gs);
-          p_wait(gs);
-          FPSA_TL(9, 1, gs);
-          tc_fence_after();
-#if FPSA_MMA_ONE_ELECT
-          mma_attn_step_w(tm_o, ts, dv[0], dv[1], dv[2], dv[3], idesc_pv, s > pv0 ? 1u : 0u, s >= pv0 ? 1u : 0u, ts,
-                          dqq[0], dqq[1], dqq[2], dqq[3], dkk[0], dkk[1], dkk[2], dkk[3], idesc_qk, do_qk ? 1u : 0u,
-                          smem_u32(&bar_s_full[gs & 1]), smem_u32(&bar_kv_empty[pv_st]));
-          FPSA_TL(9, 2, gs);
-          if (do_qk) {
-            FPSA_TL(9, 3, gs);
-            if (++qk_st == kStages) {
-              qk_st = 0;
-              qk_ph ^= 1;
-            }
-            if (s + 3 == steps) mma_commit_w(&bar_qfree[qbuf]);
-          }
-#else
-          if (s >= pv0)
-            mma_f8_ts_x4_w(tm_o, ta[0], ta[1], ta[2], ta[3], dv[0], dv[1], dv[2], dv[3], idesc_pv, s > pv0 ? 1u : 0u);
-          FPSA_TL(9, 2, gs);
-          if (do_qk) {
-            mma_f8_ss_x4_w(ts, dqq[0], dqq[1], dqq[2], dqq[3], dkk[0], dkk[1], dkk[2], dkk[3], idesc_qk, 0u);
-            mma_commit_w(&bar_s_full[gs & 1]);
-            FPSA_TL(9, 3, gs);
-            if (++qk_st == kStages) {
-              qk_st = 0;
-              qk_ph ^= 1;
-            }
-            if (s + 3 == steps) mma_commit_w(&bar_qfree[qbuf]);
-          }
-          mma_commit_w(&bar_kv_empty[pv_st]);  // after QK(j+2): the stage is released when both are done
-#endif
-          if (++pv_st == kStages) pv_st = 0;
-          if (++bp == p.nb) bp = 0;
-        }
-        }
-      } else
-#endif
-      {
-      for (int32_t s = 0; s < steps; ++s) {
-          const uint32_t gs = g + s;
-  #ifdef FPSA_TRACE
-          const long long tp0 = clock64();
-  #endif
-          FPSA_TL(9, 0, gs);
-          p_wait(gs);
-          FPSA_TL(9, 1, gs);
-  #ifdef FPSA_TRACE
-          if (lane == 0) atomicAdd(&g_trace[3], (unsigned long long)(clock64() - tp0));
-  #endif
-          tc_fence_after();
-          if (s >= pv0) {
-            // [O|l] += P~ [V|1]: P~ of the keys of row part c sits in the first columns of that part's
-            // S columns; the B descriptor's leading byte offset points from V at the ones atom
-            if (s == pv0 && iter > 0) {
-              attn_wait(&bar_ofree, (iter - 1) & 1);  // the previous item's epilogue has read O
-              tc_fence_after();
-            }
-            const uint64_t dv = (!PACKED && bp == p.nb - 1 ? dvt0 : dv0) + pv_st * kVStageStep;
-            const uint32_t ts = tm_s(gs);
-  #ifndef FPSA_NO_MMA
-            if constexpr (kPingPong) {  // one elect for the four K32 MMAs (shorter issue path)
-              constexpr uint64_t kVk = 32 * D / 16;
-              mma_f8_ts_x4_w(tm_o, ts, ts + 8, ts + 16, ts + 24, dv, dv + kVk, dv + 2 * kVk, dv + 3 * kVk, idesc_pv,
-                             s > pv0 ? 1u : 0u);
-            } else {
-  #pragma unroll
-              for (int k = 0; k < kBlk / 32; ++k)
-                mma_f8_ts_w(tm_o, kPingPong ? ts + 8 * k : ts + kPartCols * (32 * k / kPartCols) + 8 * (k % (kPartCols / 32)),
-                            dv + (uint64_t)k * (32 * D / 16), idesc_pv,
-                            (s > pv0 || k > 0) ? 1u : 0u);
-            }
-  #endif
-          }
-          mma_commit_w(&bar_kv_empty[pv_st]);
-          if (++pv_st == kStages) pv_st = 0;
-          if (++bp == p.nb) bp = 0;
-          FPSA_TL(9, 2, gs);
-          if (s + 2 < steps) {
-            issue_qk(gs + 2);
-            FPSA_TL(9, 3, gs);
-            if (s + 3 == steps) mma_commit_w(&bar_qfree[qbuf]);
-          }
-        }
       }
-      if constexpr (!kSplit) mma_commit_w(&bar_o);
       g += steps;
     }
-  } else if (kSplit && warp == kPvWarp) {
+  } else if (warp == kPvWarp) {
     // ------------------------------------------------------------ PV issuer (split issue)
     constexpr uint32_t idesc_pv = idesc_f8(128, D + 16, FPSA_E4M3, FMT, 1);
     constexpr uint64_t kTileU = S::kTile >> 4;
@@ -849,7 +623,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     regs_inc<kRegsSoftmax>();
     // ------------------------------------------------------------ softmax: (row, column part)
     const int quarter = warp & 3;
-    const int part = warp >> 2;              // S columns [kPartCols part, kPartCols (part + 1))
+    const int part = warp >> 2;              // owns the steps j with j % 2 == part
     const int row = quarter * 32 + lane;     // TMEM lane = row of the query block
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     const uint32_t o_addr = tm_o + lane_off + part * (D / kEpiParts);
@@ -896,7 +670,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #ifdef FPSA_TRACE
       const long long tl0 = clock64();
 #endif
-      if constexpr (kPingPong) {
+      {
         // ping-pong: this warp computes the whole 128-key rows of its lane quarter for the steps with
         // g % 2 == part (S buffer g % 2 == part), the other warp of the SMSP the other steps, so one
         // warp's TMEM load / store and hand-off latency overlaps the other's exp work
@@ -927,7 +701,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc_fence_before();
             __syncwarp();
             if (lane == 0) {
-              if (kEarly) mbar_arrive(&bar_s_free[gj & 1]);
+              mbar_arrive(&bar_s_free[gj & 1]);
               p_free_wait(gj);
               p_arrive(gj);  // S consumed
             }
@@ -955,7 +729,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               tc_fence_before();
               __syncwarp();
               if (lane == 0) {
-                if (kEarly) mbar_arrive(&bar_s_free[gj & 1]);
+                mbar_arrive(&bar_s_free[gj & 1]);
                 p_free_wait(gj);
                 p_arrive(gj);  // S consumed
               }
@@ -1035,8 +809,9 @@ __global__ void __launch_bounds__(kThreads, 1)
               tmem_wait_ld();
               half(0, sreg);
             }
-            if constexpr (kEarly && FPSA_P_STORE_SPLIT) {
-              // the first 64 keys' P~ go out while the second half is computed
+            {
+              // P~(j) goes into P~ buffer j % 2 once PV(j - 2) has read it; the first 64 keys' codes go out
+              // while the second half is computed (11.07 -> 11.00 ms)
               if (g_own >= (uint32_t)kParts) attn_wait(&bar_p_free[g_own % kParts], ((g_own / kParts) - 1) & 1);
               tc_fence_after();
               tmem_st16(tm_p(g_own) + lane_off, w);
@@ -1045,23 +820,13 @@ __global__ void __launch_bounds__(kThreads, 1)
               uint32_t sreg[64];
               load_s_all<64>(s_row + 64, sreg);
               tmem_wait_ld();
-              if constexpr (kEarly) {  // S(j) is in registers: its buffer may take S(j+2)
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&bar_s_free[g_own & 1]);
-              }
+              // S(j) is in registers: its buffer may take S(j+2)
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive(&bar_s_free[g_own & 1]);
               half(1, sreg);
             }
-            if constexpr (kEarly && FPSA_P_STORE_SPLIT) {
-              tmem_st16(tm_p(g_own) + 16 + lane_off, w + 16);
-            } else if constexpr (kEarly) {
-              // P~(j) into its own columns once PV(j - 2) has read them
-              if (g_own >= (uint32_t)kParts) attn_wait(&bar_p_free[g_own % kParts], ((g_own / kParts) - 1) & 1);
-              tc_fence_after();
-              tmem_st32(tm_p(g_own) + lane_off, w);
-            } else {
-              tmem_st32(s_row, w);  // P~ of the 128 keys over the first 32 columns of this S buffer
-            }
+            tmem_st16(tm_p(g_own) + 16 + lane_off, w + 16);
             tmem_wait_st();
             tc_fence_before();
             __syncwarp();
@@ -1070,91 +835,6 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
         g += n_kv;
-      } else {
-      if (p.exact) {
-        // pass 0 (exact mode only): running max of x over all key blocks
-        float m_acc = -INFINITY;
-        int32_t kt = 0, b = 0;
-        for (int32_t j = 0; j < n_kv; ++j, ++g) {
-          const bool tail = b == p.nb - 1;
-          const int ncol = (tail ? p.n_tail : kBlk) - kPartCols * part;
-          const int ncol_h = min(max(ncol, 0), kPartCols);
-          const float c = factor_at(kt);
-          attn_wait(&bar_s_full[g & 1], (g >> 1) & 1);
-          tc_fence_after();
-          m_acc = fmaxf(m_acc, block_max<kPartCols>(tm_s(g) + lane_off + part * kPartCols, ncol_h, false) * c);
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) p_arrive(g);  // S consumed
-          if (tail) {
-            b = 0;
-            ++kt;
-          } else {
-            ++b;
-          }
-        }
-        m_ref = row_max(m_acc);
-      }
-      {
-        // main pass, software-pipelined: block j's P~ store is in flight while
-        // block j+1's S is waited for and loaded
-        int32_t kt = 0, b = 0;
-        float c = factor_at(0);
-        uint32_t sreg[kPartCols];
-        auto ncol_of = [&](int32_t bb) {
-          return min(max((bb == p.nb - 1 ? p.n_tail : kBlk) - kPartCols * part, 0), kPartCols);
-        };
-        attn_wait(&bar_s_full[g & 1], (g >> 1) & 1);
-        tc_fence_after();
-        if (!p.exact) {
-          // reference max = row max of the first key block (a tail block only when nb == 1)
-          m_ref = row_max(block_max<kPartCols>(tm_s(g) + lane_off + part * kPartCols, ncol_of(0), false)) * c;
-        }
-        load_s_all<kPartCols>(tm_s(g) + lane_off + part * kPartCols, sreg);
-        tmem_wait_ld();
-        for (int32_t j = 0; j < n_kv; ++j, ++g) {
-#ifdef FPSA_TRACE
-          const long long tc0 = clock64();
-          ++n_steps;
-#endif
-          const bool tail = b == p.nb - 1;
-          uint32_t w[kPartCols / 4];
-          sat |= compute_p_regs<kPartCols>(sreg, ncol_of(b), c, kLog2_448 - m_ref - tau, w);
-#ifdef FPSA_TRACE
-          w_c += clock64() - tc0;
-#endif
-          FPSA_TL(warp, 2, g);
-          const uint32_t s_addr = tm_s(g) + lane_off + part * kPartCols;
-          if constexpr (kPartCols == 64) tmem_st16(s_addr, w);
-          else tmem_st8(s_addr, w);
-          if (tail) {
-            b = 0;
-            if (++kt < n_kt) c = factor_at(kt);
-          } else {
-            ++b;
-          }
-          const bool more = j + 1 < n_kv;
-          if (more) {
-#ifdef FPSA_TRACE
-            const long long ts0 = clock64();
-#endif
-            FPSA_TL(warp, 0, g + 1);
-            attn_wait(&bar_s_full[(g + 1) & 1], ((g + 1) >> 1) & 1);
-            FPSA_TL(warp, 1, g + 1);
-#ifdef FPSA_TRACE
-            w_s += clock64() - ts0;
-#endif
-            tc_fence_after();
-            load_s_all<kPartCols>(tm_s(g + 1) + lane_off + part * kPartCols, sreg);
-          }
-          tmem_wait_st();
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) p_arrive(g);
-          FPSA_TL(warp, 3, g);
-          if (more) tmem_wait_ld();
-        }
-      }
       }
 #ifdef FPSA_TRACE
       t_loop += clock64() - tl0;
@@ -1385,7 +1065,7 @@ extern "C" int fpsa_attn_fwd(const uint8_t* q_codes, const uint8_t* k_codes, con
   p.dw = td.w;
   // packed key blocks: needs 16-row segment boundaries and at most two key tiles per 128-key block
   static const bool no_pack = getenv("FPSA_ATTN_NO_PACK") != nullptr;  // measurement switch
-  p.packed = !no_pack && kPingPong && tv % 16 == 0 && tv > kBlk && tv % kBlk != 0;
+  p.packed = !no_pack && tv % 16 == 0 && tv > kBlk && tv % kBlk != 0;
   // magic divisors of the softmax warps' block geometry: exact while (key position) * divisor < 2^32
   // (positions stay below M * tv); 0 selects a plain division
   auto magic = [](uint64_t d, uint64_t bound) -> uint32_t {

@@ -174,16 +174,6 @@ __device__ __forceinline__ void mma_f8_ss_w(uint32_t d_tmem, uint64_t adesc, uin
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
-__device__ __forceinline__ void mma_f8_ts_w(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc,
-                                            uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p, e;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "elect.sync _|e, 0xffffffff;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
-      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
-      : "memory");
-}
 // Four MMAs of one K = 128 reduction under a single elect (fewer issue-path instructions
 // than four warp-uniform calls): D (+)= A_k B_k for k = 0..3, the first accumulating iff acc.
 __device__ __forceinline__ void mma_f8_ss_x4_w(uint32_t d_tmem, uint64_t a0, uint64_t a1, uint64_t a2, uint64_t a3,
@@ -212,34 +202,6 @@ __device__ __forceinline__ void mma_f8_ts_x4_w(uint32_t d_tmem, uint32_t a0, uin
       "@e tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], [%3], %7, %9, t;\n\t"
       "@e tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], [%4], %8, %9, t;\n\t}" ::"r"(d_tmem),
       "r"(a0), "r"(a1), "r"(a2), "r"(a3), "l"(b0), "l"(b1), "l"(b2), "l"(b3), "r"(idesc), "r"(acc)
-      : "memory");
-}
-// One attention step under a single elect: PV(j) (four TS MMAs into d_o, A = P~ at TMEM columns a,
-// a+8, a+16, a+24, B descriptors b0..b3) when do_pv, then QK(j+2) (four SS MMAs into d_s) and the commit
-// of its S-full barrier when do_qk, then the commit releasing the K/V stage.
-__device__ __forceinline__ void mma_attn_step_w(uint32_t d_o, uint32_t a, uint64_t b0, uint64_t b1, uint64_t b2,
-                                                uint64_t b3, uint32_t idesc_pv, uint32_t acc, uint32_t do_pv,
-                                                uint32_t d_s, uint64_t q0, uint64_t q1, uint64_t q2, uint64_t q3,
-                                                uint64_t k0, uint64_t k1, uint64_t k2, uint64_t k3,
-                                                uint32_t idesc_qk, uint32_t do_qk, uint32_t bar_s, uint32_t bar_kv) {
-  asm volatile(
-      "{\n\t.reg .pred e, pv, pa, qk, t, f;\n\t.reg .b32 a1, a2, a3;\n\t"
-      "setp.eq.u32 t, 0, 0;\n\tsetp.ne.u32 f, 0, 0;\n\t"
-      "add.u32 a1, %1, 8;\n\tadd.u32 a2, %1, 16;\n\tadd.u32 a3, %1, 24;\n\t"
-      "elect.sync _|e, 0xffffffff;\n\t"
-      "setp.ne.and.b32 pv, %8, 0, e;\n\tsetp.ne.b32 pa, %7, 0;\n\tsetp.ne.and.b32 qk, %19, 0, e;\n\t"
-      "@pv tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], [%1], %2, %6, pa;\n\t"
-      "@pv tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], [a1], %3, %6, t;\n\t"
-      "@pv tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], [a2], %4, %6, t;\n\t"
-      "@pv tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], [a3], %5, %6, t;\n\t"
-      "@qk tcgen05.mma.cta_group::1.kind::f8f6f4 [%9], %10, %14, %18, f;\n\t"
-      "@qk tcgen05.mma.cta_group::1.kind::f8f6f4 [%9], %11, %15, %18, t;\n\t"
-      "@qk tcgen05.mma.cta_group::1.kind::f8f6f4 [%9], %12, %16, %18, t;\n\t"
-      "@qk tcgen05.mma.cta_group::1.kind::f8f6f4 [%9], %13, %17, %18, t;\n\t"
-      "@qk tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%20];\n\t"
-      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%21];\n\t}" ::"r"(d_o),
-      "r"(a), "l"(b0), "l"(b1), "l"(b2), "l"(b3), "r"(idesc_pv), "r"(acc), "r"(do_pv), "r"(d_s), "l"(q0), "l"(q1),
-      "l"(q2), "l"(q3), "l"(k0), "l"(k1), "l"(k2), "l"(k3), "r"(idesc_qk), "r"(do_qk), "r"(bar_s), "r"(bar_kv)
       : "memory");
 }
 __device__ __forceinline__ void mma_commit_w(uint64_t* bar) {

@@ -237,31 +237,6 @@ __device__ __forceinline__ uint32_t softmax_block(uint32_t s_addr, int ncol, boo
   return saturated<NC>(w);
 }
 
-// Branch-free form for blocks whose S columns are all finite (the QK MMA always
-// runs N = 128; a tile's last block has zero K rows beyond tv, so S = 0 there):
-// every column is computed and the P~ words of columns >= ncol are zeroed.
-// ncol is a multiple of 8, so whole 4-column words are dropped.
-template <int NC>
-__device__ __forceinline__ uint32_t softmax_block_full(uint32_t s_addr, int ncol, float c, float boff, uint32_t* w) {
-  const f2 cc = bcast(c), bb = bcast(boff);
-  const float cs = c * (1.0f / 256.0f), bs = (boff + 126.0f) * (1.0f / 256.0f);
-  uint32_t sa[32], sb[32];
-  tmem_ld32(s_addr, sa);
-  tmem_wait_ld();
-  softmax_chunk32<0>(sa, cc, bb, cs, bs, w);
-  if constexpr (NC == 64) {
-    tmem_ld32(s_addr + 32, sb);
-    tmem_wait_ld();
-    softmax_chunk32<1>(sb, cc, bb, cs, bs, w);
-  }
-  if (ncol < NC) {
-#pragma unroll
-    for (int i = 0; i < NC / 4; ++i)
-      if (4 * i >= ncol) w[i] = 0u;
-  }
-  return saturated<NC>(w);
-}
-
 // Software-pipelined form: the row part's S is already in registers (s[0..NC)),
 // loaded while the previous block's P~ store was in flight.  Same math as
 // softmax_block_full.
