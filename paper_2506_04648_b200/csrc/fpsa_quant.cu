@@ -127,11 +127,15 @@ __device__ __forceinline__ uint32_t cvt_pair(float hi, float lo) {
 
 // Exact code of the f64 quotient x / s (slow path).
 template <int FMT>
-__device__ __noinline__ uint32_t encode_exact(float x, double s) {
+__device__ __forceinline__ uint32_t encode_exact_inl(float x, double s) {
   const double q = __ddiv_rn((double)x, s);
   float f = __double2float_rz(q);
   if ((double)f != q) f = __uint_as_float(__float_as_uint(f) | 1u);  // round to odd
   return cvt_pair<FMT>(0.0f, f) & 0xFFu;
+}
+template <int FMT>
+__device__ __noinline__ uint32_t encode_exact(float x, double s) {
+  return encode_exact_inl<FMT>(x, s);
 }
 
 __device__ __forceinline__ double scale_of(float peak, double maxv) {
@@ -687,10 +691,71 @@ __device__ __forceinline__ void item_of(int32_t it, int32_t per_job, int32_t hea
   }
 }
 
+// Exact ties of bf16 data without f64 arithmetic per element.  With x and the block peak P both bf16, the
+// quotient Q = x * maxv / P (maxv = 448 = 7 * 2^6, or 57344 = 7 * 2^13) lies either exactly on a rounding
+// midpoint B = o * 2^f of the fp8 grid (o odd, o <= 31) or at least 2^-13 (relative) away from it, far
+// outside the fast path's 2^-19 bracket; so an ambiguous element is an exact tie.  Its code then depends
+// only on how the reference's f64 quotient q64 = RN64(x / RN64(P / maxv)) compares with B: q64 == B rounds
+// to the even code, q64 < B down, q64 > B up.  That comparison depends only on P's 8-bit significand and on
+// B's odd significand o (powers of two scale out), so one table per format, indexed by the peak's mantissa
+// bits and the tie class (the lower code's mantissa, normal or subnormal), decides every tie: bit k of .x
+// "up", of .y "even", of .z "the class can occur at all" (o * P_m divisible by 7); otherwise the element
+// takes the exact f64 path.  Built per CTA at kernel start from the same IEEE f64 operations.
+constexpr int kTieEntries = 128;  // bf16 mantissa bits of the peak
+template <int FMT>
+__device__ __forceinline__ int32_t tie_odd(int k) {  // odd significand o of tie class k
+  constexpr int kM = FMT == FPSA_E4M3 ? 8 : 4;     // mantissa codes per binade
+  return k < kM ? 2 * kM + 1 + 2 * k : 2 * (k - kM) + 1;  // normal: (2 kM + 2m + 1); subnormal: 2m + 1
+}
+template <int FMT>
+__device__ __forceinline__ int tie_class(uint32_t code) {  // class of the midpoint above code (magnitude)
+  constexpr int kMB = FMT == FPSA_E4M3 ? 3 : 2, kM = 1 << kMB;
+  const uint32_t mag = code & 0x7Fu, m = mag & (kM - 1u);
+  return (mag >> kMB) ? (int)m : kM + (int)m;
+}
+template <int FMT>
+__device__ void build_tie_table(uint3* table, int tid, int nthreads) {
+  constexpr double kMax = FMT == FPSA_E4M3 ? 448.0 : 57344.0;
+  constexpr int kClasses = FMT == FPSA_E4M3 ? 16 : 8;
+  for (int i = tid; i < kTieEntries * kClasses; i += nthreads) {
+    const int e = i / kClasses, k = i % kClasses;
+    const double pm = (double)(128 + e);                  // the peak's significand, scaled to an integer
+    const double s = __ddiv_rn(pm, kMax);                 // scale_of: RN64(P / maxv), up to a power of two
+    const double xo = (double)(tie_odd<FMT>(k) * (128 + e));  // o * P_m, exact
+    const double x = __ddiv_rn(xo, kMax);                 // the tying input, if representable
+    const bool ok = __fma_rn(x, kMax, -xo) == 0.0;
+    const double q = __ddiv_rn(x, s);                     // the reference's f64 quotient
+    const double o = (double)tie_odd<FMT>(k);
+    if (ok) {
+      atomicOr(&table[e].z, 1u << k);
+      if (q > o) atomicOr(&table[e].x, 1u << k);
+      if (q == o) atomicOr(&table[e].y, 1u << k);
+    }
+  }
+}
+// The code of an ambiguous element (clo / chi: the codes of the bracket ends, chi one step above in
+// magnitude) from the tie table; the exact f64 path when the peak is not a normal bf16 value or the class
+// cannot tie.
+template <int FMT>
+__device__ __forceinline__ uint32_t resolve_tie(const uint3* table, uint32_t clo, uint32_t chi, float x,
+                                                float peak, bool use_table) {
+  constexpr double kMax = FMT == FPSA_E4M3 ? 448.0 : 57344.0;
+  const uint32_t pb = __float_as_uint(peak);
+  const uint32_t exp = (pb >> 23) & 0xFFu;
+  if (use_table && (pb & 0xFFFFu) == 0u && exp != 0u && exp != 0xFFu) {
+    const uint3 t = table[(pb >> 16) & 0x7Fu];
+    const uint32_t bit = 1u << tie_class<FMT>(clo);
+    if (t.z & bit) return (t.x & bit) ? chi : ((t.y & bit) ? ((clo & 1u) ? chi : clo) : clo);
+  }
+  // inlined: a call here would constrain the register allocation of the whole kernel (1.30 vs 1.08 ms)
+  return encode_exact_inl<FMT>(x, scale_of(peak, kMax));
+}
+
 #ifdef FPSA_QTRACE
 // measurement builds only: per-tile timeline of CTA 0 (clock64): [0] load issued, [1] warp 0 saw it full,
 // [2] warp 0 past the tile-max barrier, [3] warp 0 released the stage, [4] warp 23 released the stage
 __device__ long long g_qtl[128][5];
+__device__ unsigned long long g_qcount[4];  // fix-up loop trips (warp), ambiguous bytes (lane), tiles
 #define FPSA_QTL(k, ev)                                                            \
   do {                                                                            \
     if (blockIdx.x == 0 && (threadIdx.x & 31) == 0 && (k) < 128) g_qtl[(k)][(ev)] = clock64(); \
@@ -712,6 +777,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ uint64_t full[kTmaStages], empty[kTmaStages];
   __shared__ uint32_t s_peak[3];  // tile |x| max bits by tile index mod 3 (shared-memory atomicMax of the warps)
+  __shared__ uint3 s_tie[kTieEntries];  // exact-tie decisions by the peak's mantissa bits (build_tie_table)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int32_t per_job = a.heads * g.M;
   const int32_t n_items = a.njobs * per_job;
@@ -773,6 +839,9 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
   // loads in flight per SM and measured 1.78 ms against 1.16 (profiles/r02_quant_early_release_rejected.txt).
   static_assert(kTmaMaxRows <= 32 * kTmaConsumerWarps, "row mask holds one bit per row of a warp");
   if (threadIdx.x == 0) s_peak[0] = s_peak[1] = s_peak[2] = 0;
+  for (int i = threadIdx.x; i < kTieEntries; i += kTmaConsumerWarps * 32) s_tie[i] = make_uint3(0u, 0u, 0u);
+  named_bar_sync(1, kTmaConsumerWarps * 32);
+  build_tie_table<FMT>(s_tie, threadIdx.x, kTmaConsumerWarps * 32);  // overlaps the first tile loads
   named_bar_sync(1, kTmaConsumerWarps * 32);
   int k = 0;
   for (int32_t it = blockIdx.x; it < n_items; it += gridDim.x, ++k) {
@@ -853,6 +922,13 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
       store_codes<VEC>(out + (int64_t)r * kTmaD, clo);
       amb |= ((clo ^ chi) | force) != 0u ? 1u << i : 0u;
     }
+#ifdef FPSA_QTRACE
+    {
+      const unsigned trips = __reduce_max_sync(0xffffffffu, (unsigned)__popc(amb));
+      if (lane == 0) atomicAdd(&g_qcount[0], (unsigned long long)trips);
+      if (lane == 0 && warp == 0) atomicAdd(&g_qcount[2], 1ull);
+    }
+#endif
     while (amb) {  // rare: this lane's rows with ambiguous bytes, re-encoded from the f64 quotient
       const int32_t ri = __ffs(amb) - 1;
       amb &= amb - 1;
@@ -868,11 +944,18 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
         clo |= cvt_pair<FMT>(l1, l0) << (8 * e);
         chi |= cvt_pair<FMT>(h1, h0) << (8 * e);
       }
-      const uint32_t diff = (clo ^ chi) | force;
+      const uint32_t diff = clo ^ chi;
 #pragma unroll
-      for (int e = 0; e < VEC; ++e)
-        if ((diff >> (8 * e)) & 0xFFu)
-          clo = (clo & ~(0xFFu << (8 * e))) | (encode_exact<FMT>(v[e], scale_of(pk[e], kMax)) << (8 * e));
+      for (int e = 0; e < VEC; ++e) {
+        if (!(((diff | force) >> (8 * e)) & 0xFFu)) continue;
+#ifdef FPSA_QTRACE
+        atomicAdd(&g_qcount[1], 1ull);
+#endif
+        const uint32_t lo = (clo >> (8 * e)) & 0xFFu, hi = (chi >> (8 * e)) & 0xFFu;
+        // a bracket out of range (force): every element takes the exact path
+        const uint32_t c = resolve_tie<FMT>(s_tie, lo, hi, v[e], pk[e], force == 0u);
+        clo = (clo & ~(0xFFu << (8 * e))) | (c << (8 * e));
+      }
       store_codes<VEC>(out + (int64_t)r * kTmaD, clo);
     }
     __syncwarp();
@@ -1359,6 +1442,9 @@ extern "C" int fpsa_decode(const uint8_t* codes, int64_t n, int fmt, const doubl
 }
 
 #ifdef FPSA_QTRACE
+extern "C" int fpsa_qtrace_counts(unsigned long long* out) {
+  return cudaMemcpyFromSymbol(out, fpsa::g_qcount, sizeof(fpsa::g_qcount)) == cudaSuccess ? 0 : 1;
+}
 extern "C" int fpsa_qtrace_timeline(long long* out) {
   cudaMemcpyFromSymbol(out, fpsa::g_qtl, sizeof(fpsa::g_qtl));
   return (int)(sizeof(fpsa::g_qtl) / sizeof(long long));

@@ -131,6 +131,40 @@ def test_natural_order_multihead_bf16(fpsa, shape):
         assert np.array_equal(vcodes[h, :, :tv, :].reshape(L, d), vc)
 
 
+@pytest.mark.parametrize("fmt_name", ["e4m3", "e5m2"])
+@pytest.mark.parametrize("peak_mant", [0x88, 0x8C, 0xE0])
+def test_bf16_tie_table_every_class(fpsa, fmt_name, peak_mant):
+    """The tie table of the TMA quantiser (exact ties of bf16 data resolved without f64 arithmetic) against
+    the oracle, bit for bit, with tiles whose values are multiples of the peak / 2^k and the peak's
+    significand 0x88 (136: not a multiple of 7, so only the classes with 7 | o tie), 0x8C (140 = 7 * 20) or
+    0xE0 (224 = 7 * 32: every class can tie), in both formats."""
+    fmt = fpsa.E4M3 if fmt_name == "e4m3" else fpsa.E5M2
+    grid, tile, H, d = (6, 10, 32), (3, 5, 16), 2, 128
+    L = grid[0] * grid[1] * grid[2]
+    gen = torch.Generator(device="cuda").manual_seed(3)
+    peak = float(np.frombuffer(np.array([peak_mant << 16 | (130 << 23)], dtype=np.uint32).tobytes(), np.float32)[0])
+    k = torch.randint(-255, 256, (L, H, d), generator=gen, device="cuda").float() * (peak / 256.0)
+    k[0::240, :, 0] = peak
+    x = k.to(torch.bfloat16)
+    plan = fpsa.FpsaPlan(grid, tile, (3, 3, 3), H, d, fmt)
+    plan.quantize(x, x, x, "lhd")
+    torch.cuda.synchronize()
+    perm = O.tile_perm(grid, tile)
+    tv, M = plan.tv, plan.M
+    qc = plan.q_codes.view(H, M, plan.pitch, d).cpu().numpy()
+    vc = plan.v_codes.view(H, M, plan.pitch, d).cpu().numpy()
+    xs = x.float().cpu().numpy()
+    ofmt = O.FORMATS[fmt_name]
+    for h in range(H):
+        xt = xs[perm, h, :]
+        c, s = O.quantize_qk_tilewise(xt, tv, ofmt)
+        assert np.array_equal(plan.q_scales.view(H, M)[h].cpu().numpy(), s)
+        assert np.array_equal(qc[h, :, :tv, :].reshape(L, d), c)
+        c, s = O.quantize_v_channelwise(xt, ofmt)
+        assert np.array_equal(plan.v_scales.view(H, d)[h].cpu().numpy(), s)
+        assert np.array_equal(vc[h, :, :tv, :].reshape(L, d), c)
+
+
 @pytest.mark.parametrize("tie_rich", [False, True])
 def test_bf16_exact_ties_natural_order(fpsa, tie_rich):
     """bf16 data hits exact fp8 midpoints often (e.g. 448*0.796875/4.25 == 84); ties go to even.

@@ -22,6 +22,12 @@ lib = L.lib()
 buf = (ctypes.c_longlong * (128 * 5))()
 lib.fpsa_qtrace_timeline.argtypes = [ctypes.POINTER(ctypes.c_longlong)]
 lib.fpsa_qtrace_timeline(buf)
+cnt = (ctypes.c_ulonglong * 4)()
+if hasattr(lib, "fpsa_qtrace_counts"):
+    lib.fpsa_qtrace_counts(cnt)
+    n_tiles = max(1, cnt[2])
+    print(f"fix-up loop: {cnt[0] / n_tiles / 24:.2f} trips per warp-tile, {cnt[1] / n_tiles:.1f} ambiguous bytes per tile "
+          f"({cnt[1] / n_tiles / (240 * 128) * 100:.3f} % of elements), over {cnt[2]} tiles")
 T = np.array(buf, dtype=np.int64).reshape(128, 5)
 T = T[(T > 0).all(1)]
 t0 = T[0, 0]
