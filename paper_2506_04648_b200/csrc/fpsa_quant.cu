@@ -653,7 +653,7 @@ __global__ void __launch_bounds__(kGenThreads) quant_chan_generic_kernel(const T
 // 24 consumer warps reduce the tile amax from shared memory and write the
 // codes.  HBM traffic is one read of q/k/v and one write of the codes.
 #ifndef FPSA_QUANT_WARPS
-#define FPSA_QUANT_WARPS 24  // measured best: 1.26 ms at C2 vs 1.31 (20), 1.28 (28), 1.37 (16), 1.56 (12)
+#define FPSA_QUANT_WARPS 20  // round 2 (one barrier, tie table): 1.113 ms vs 1.137 (24), 1.131 (16), 1.269 (28); round 1 (two barriers): 24 best
 #endif
 constexpr int kTmaConsumerWarps = FPSA_QUANT_WARPS;
 constexpr int kTmaThreads = (kTmaConsumerWarps + 1) * 32;
