@@ -17,7 +17,7 @@
 //   x     = S * (sq[u] * sk[v] * softmax_scale * log2 e)     per-tile factors
 //   m     = row max of the first key block (fixed for the item)
 //   P~    = e4m3(448 * 2^-tau * 2^(x - m))   re-quantised per key block,
-//           written back to TMEM over S(j) (4 codes per column)
+//           written to TMEM P~ buffer j % 2 (4 codes per column)
 //   [O|l] += P~ [V_j | 1]             tcgen05.mma N = D + 16, A = P~ from TMEM,
 //                                    B = V from smem (MN-major, V stored [keys][d])
 //                                    plus a constant "ones" MN atom: the extra
@@ -30,21 +30,22 @@
 // keys takes the exact row max, a second pass uses it with tau = 0
 // (DESIGN.md).
 //
-// TMEM: [O|l] (D + 16 columns), S(even) at column 256, S(odd) at 384.  With S
-// double-buffered, QK(j+1) runs while the softmax works on S(j), and the MMA
-// issue order PV(j), QK(j+2) never makes the softmax wait on its own P.
+// TMEM: [O|l] (D + 16 columns), P~ buffers at columns 160 / 192, S(even) at
+// column 256, S(odd) at 384.  S(j+2) is computed as soon as the owners of S(j)
+// have it in registers; PV(j) reads P~(j) from its own buffer.
 //
 // Warp roles (384 threads): warps w and w+4 (w < 4) share TMEM lane quarter w
 // (rows 32w..32w+31) and take alternate key blocks (ping-pong): warp w the
-// even steps, warp w+4 the odd ones, each computing whole 128-key rows and
-// writing their P~ over the first 32 columns of the step's S buffer, so one
-// warp's TMEM traffic and hand-off overlap the other's exp work.  Warp 8 is
-// the TMA producer (and TMEM allocator), warp 9 the MMA issuer, warp 10
-// claims work items (a global atomic counter: CTAs take the next item of the
-// longest-first list when they are ready for it, so no CTA is left with a
-// longer share) and prefetches their metadata, warp 11 is idle.  The claimed
-// (head, tile, block) triples reach the other roles through a 4-deep ring in
-// shared memory.
+// even steps, warp w+4 the odd ones, each computing whole 128-key rows.  Warp
+// 8 is the TMA producer (and TMEM allocator), warp 9 issues the QKs, warp 11
+// the PVs (split issue: QK and PV touch disjoint TMEM, and every PV comes from
+// the one PV warp in order), warp 10 claims work items (a global atomic
+// counter: CTAs take the next item of the longest-first list when they are
+// ready for it, so no CTA is left with a longer share) and prefetches their
+// metadata.  The claimed (head, tile, block) triples reach the other roles
+// through a 4-deep ring in shared memory.  Step barriers are reused every
+// second step, so none may run two phases ahead of its waiter (DESIGN.md,
+// "Phase discipline of the split issue").
 //
 // Normalised-P mode (template NORM, the reference's exact semantics,
 // attention.py:133-145): three passes over the keys of an item -- exact row
@@ -443,7 +444,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   static_assert(D + 16 <= 160 && 160 + 32 * kParts <= 256, "TMEM: O | P~ buffers | S buffers at 256 and 384");
   const float tau = p.exact ? 0.0f : p.tau;
 
-  if (warp >= kSoftmaxWarps) regs_dec<kRegsProducer>();  // producer warpgroup: TMA, MMA, 2 idle warps
+  if (warp >= kSoftmaxWarps) regs_dec<kRegsProducer>();  // producer warpgroup: TMA, QK, helper, PV warps
   if (warp == kTmaWarp) {
     // ------------------------------------------------------------ TMA producer (warp-uniform, one elected lane issues)
     if (lane == 0) {
